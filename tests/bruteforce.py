@@ -1,0 +1,126 @@
+"""Independent brute-force model of the Simulator, used ONLY to pin the oracle.
+
+It shares no code or data structure with oracle/xmo.c: there are no block
+objects, no free list, no prev/next links and no merge code. Each live segment
+is the sorted list of its *allocated* extents; the free blocks are, by
+definition, the gaps between those extents (BFC's coalescing maximality,
+SPEC.md:216, makes every free block a maximal gap). Best fit is an exhaustive
+minimum over all gaps (PAPER.md:258 (iii); SPEC.md:248 tie order (size, segment,
+offset)); a free simply deletes the extent, which merges the neighbouring gaps
+by construction. Reclamation deletes segments with no extents (PAPER.md:259-260,
+reading Q3). Runs in pure Python: only for traces of a few thousand events.
+"""
+from __future__ import annotations
+
+import bisect
+
+MiB = 1 << 20
+UNLIMITED = (1 << 64) - 1
+
+
+def rnd(req, g=512):
+    return max(g, -(-req // g) * g)
+
+
+def seg_size(s):
+    if s <= MiB:
+        return 2 * MiB
+    if s < 10 * MiB:
+        return 20 * MiB
+    return -(-s // (2 * MiB)) * (2 * MiB)
+
+
+def split_ok(small, rem, strict=True):
+    if small:
+        return rem >= 512
+    return rem > MiB if strict else rem >= MiB
+
+
+class Seg:
+    __slots__ = ("base", "size", "stream", "small", "ext")
+
+    def __init__(self, base, size, stream, small):
+        self.base, self.size, self.stream, self.small = base, size, stream, small
+        self.ext = []  # sorted [(start, end, id)]
+
+    def gaps(self):
+        a = self.base
+        for (s, e, _) in self.ext:
+            if s > a:
+                yield (a, s - a)
+            a = e
+        if a < self.base + self.size:
+            yield (a, self.base + self.size - a)
+
+
+def simulate(bytes_, tag, capacity=UNLIMITED, strict=True):
+    segs = []
+    where = {}     # id -> (seg, start, end, s, request)
+    nxt = 0
+    reserved = blk = tensor = 0
+    out = dict(peak_allocated=0, peak_allocated_idx=0, peak_allocated_blk=0,
+               peak_allocated_blk_idx=0, peak_reserved=0, peak_reserved_idx=0,
+               n_seg_alloc=0, n_seg_release=0, max_live_segments=0, status=0)
+    curve = []
+    i = 0
+    for i in range(len(bytes_)):
+        nb = int(bytes_[i])
+        bid = int(tag[i]) & ((1 << 28) - 1)
+        st = int(tag[i]) >> 28
+        if nb > 0:
+            s = rnd(nb)
+            small = s <= MiB
+            best = None
+            for g in segs:
+                if g.stream != st or g.small != small:
+                    continue
+                for (a, L) in g.gaps():
+                    if L >= s and (best is None or (L, a) < (best[0], best[1])):
+                        best = (L, a, g)
+            if best is None:
+                need = seg_size(s)
+                if reserved + need > capacity:
+                    keep = []
+                    for g in segs:
+                        if g.ext:
+                            keep.append(g)
+                        else:
+                            reserved -= g.size
+                            out["n_seg_release"] += 1
+                    segs = keep
+                    if reserved + need > capacity:
+                        out["status"] = 1
+                        break
+                g = Seg(nxt, need, st, small)
+                nxt += need
+                segs.append(g)
+                reserved += need
+                out["n_seg_alloc"] += 1
+                out["max_live_segments"] = max(out["max_live_segments"], len(segs))
+                best = (need, g.base, g)
+            L, a, g = best
+            take = s if split_ok(small, L - s, strict) else L
+            bisect.insort(g.ext, (a, a + take, bid))
+            where[bid] = (g, a, a + take, s)
+            blk += take
+            tensor += s
+        else:
+            g, a, e, s = where.pop(bid)
+            g.ext.remove((a, e, bid))
+            blk -= e - a
+            tensor -= s
+        if tensor > out["peak_allocated"]:
+            out["peak_allocated"], out["peak_allocated_idx"] = tensor, i
+        if blk > out["peak_allocated_blk"]:
+            out["peak_allocated_blk"], out["peak_allocated_blk_idx"] = blk, i
+        if reserved > out["peak_reserved"]:
+            out["peak_reserved"], out["peak_reserved_idx"] = reserved, i
+        curve.append((tensor, blk, reserved))
+    else:
+        i = len(bytes_)
+    out["events_done"] = i
+    out["final_reserved"] = reserved
+    out["final_allocated"] = tensor
+    out["final_allocated_blk"] = blk
+    out["n_free_blocks_end"] = sum(1 for g in segs for _ in g.gaps())
+    return out, curve

@@ -1,0 +1,108 @@
+"""Mutation check of the oracle's pins.
+
+Each mutant is a plausible one-token mistake in oracle/xmo.c (a dropped term,
+a wrong comparison, a swapped operand, a missing step). The test compiles the
+mutant to a temporary library and requires that the pins -- the cited hand
+goldens plus the gap-model brute force on a small fuzz slice -- reject it.
+This is evidence that the pins are strong enough to pin the oracle.
+"""
+import ctypes
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+import bruteforce
+import oracle
+from workloads import fuzz, hand
+
+SRC = os.path.join(os.path.dirname(oracle.__file__), "xmo.c")
+
+MUTANTS = [
+    ("round: drop ceil", "if (q * c->min_block < request) q += 1;", ""),
+    ("pool: < instead of <=", "return s <= c->small_size;", "return s < c->small_size;"),
+    ("segment: small buffer for large", "if (s < c->min_large_alloc) return c->large_buffer;",
+     "if (s < c->min_large_alloc) return c->small_buffer;"),
+    ("segment: <= min_large", "if (s < c->min_large_alloc)", "if (s <= c->min_large_alloc)"),
+    ("split: small >", "if (small_pool) return remaining >= c->min_block;",
+     "if (small_pool) return remaining > c->min_block;"),
+    ("split: large never", "if (c->large_split_strict) return remaining > c->small_size;",
+     "if (c->large_split_strict) return 0;"),
+    ("best fit: ignore stream", "B->small != small || B->stream != stream || B->size < s",
+     "B->small != small || B->size < s"),
+    ("best fit: worst fit", "B->size < S.blk[best].size ||", "B->size > S.blk[best].size ||"),
+    ("best fit: tie by high addr", "B->addr < S.blk[best].addr", "B->addr > S.blk[best].addr"),
+    ("capacity: >=", "if (S.reserved + a > cc.capacity) {           /* device refuses",
+     "if (S.reserved + a >= cc.capacity) {           /* device refuses"),
+    ("no reclamation", "release_cached(&S, out);                    /* reclaim",
+     "/* release_cached */;                    /* reclaim"),
+    ("no merge prev", "if (p >= 0 && !S.blk[p].allocated) {", "if (0) {"),
+    ("no merge next", "if (q >= 0 && !S.blk[q].allocated) {", "if (0) {"),
+    ("split remainder at low end", "R->addr = B->addr + s;", "R->addr = B->addr;"),
+    ("reserved not raised", "S.reserved += a;\n", "\n"),
+    ("alloc_blk counts request", "S.alloc_blk += S.blk[b].size;", "S.alloc_blk += s;"),
+    ("peak idx last", "if (S.reserved > out[F_PEAK_RES])", "if (S.reserved >= out[F_PEAK_RES])"),
+    ("release partial segments", "if (b->prev < 0 && b->next < 0) {", "if (b->prev < 0 || b->next < 0) {"),
+]
+
+
+def _build(src_text, d):
+    c = os.path.join(d, "m.c")
+    so = os.path.join(d, "m.so")
+    with open(c, "w") as f:
+        f.write(src_text)
+    subprocess.check_call(["gcc", "-O1", "-std=c99", "-shared", "-fPIC", "-w", "-o", so, c])
+    L = ctypes.CDLL(so)
+    P = ctypes.c_void_p
+    L.xmo_simulate.argtypes = [P, P, ctypes.c_int64, ctypes.POINTER(oracle._Cfg), ctypes.c_uint64,
+                               P, P, ctypes.c_int]
+    return L
+
+
+def _run(L, by, tg, cap):
+    by = np.ascontiguousarray(by, np.int64)
+    tg = np.ascontiguousarray(tg, np.uint32)
+    out = np.zeros(oracle.NF, np.uint64)
+    cv = np.zeros((len(by), 3), np.uint64)
+    c = oracle.Config().c()
+    rc = L.xmo_simulate(by.ctypes.data_as(P := ctypes.c_void_p), tg.ctypes.data_as(P), len(by),
+                        ctypes.byref(c), cap, out.ctypes.data_as(P), cv.ctypes.data_as(P), 0)
+    return rc, dict(zip(oracle.FIELDS, map(int, out))), cv
+
+
+def _pins_reject(L, golden):
+    tr = hand.all_named()
+    for name, g in golden.items():
+        b = tr[name]
+        rc, r, _ = _run(L, b.bytes, b.tag, int(b.capacity[0]))
+        if rc or any(r[k] != v for k, v in g["expect"].items()):
+            return f"golden {name}"
+    for corpus in (fuzz.spec1_corpus(120, 400, salt=21), fuzz.capacity_corpus(60, 300, salt=22),
+                   fuzz.small_size_corpus(40, 300, salt=23)):
+        for t in range(corpus.n_traces):
+            by, tg = corpus.trace(t)
+            cap = int(corpus.capacity[t])
+            rc, r, cv = _run(L, by, tg, cap)
+            b, bc = bruteforce.simulate(by, tg, cap)
+            if rc or any(r[k] != v for k, v in b.items()):
+                return f"bruteforce trace {t}"
+            n = b["events_done"]
+            if cv[:n].tolist() != [list(x) for x in bc[:n]]:
+                return f"bruteforce curve {t}"
+    return None
+
+
+def test_unmutated_passes(golden):
+    with tempfile.TemporaryDirectory() as d:
+        assert _pins_reject(_build(open(SRC).read(), d), golden) is None
+
+
+@pytest.mark.parametrize("name,old,new", MUTANTS, ids=[m[0] for m in MUTANTS])
+def test_mutant_rejected(name, old, new, golden):
+    src = open(SRC).read()
+    assert src.count(old) >= 1, f"mutation site missing: {name}"
+    with tempfile.TemporaryDirectory() as d:
+        L = _build(src.replace(old, new, 1), d)
+        assert _pins_reject(L, golden) is not None, f"pins did not catch mutant: {name}"
