@@ -1,0 +1,228 @@
+/*
+ * xmem.h -- C ABI of libxmem.so, the B200-native batched caching-allocator
+ * trace replayer (the data-parallel hot path of xMem, arXiv 2510.21048).
+ *
+ * What is computed. xMem's Simulator (§3.4) replays an
+ * ordered alloc/free event sequence through a two-level model of PyTorch's
+ * CUDA caching allocator -- (i) 512 B round-up, (ii) segments of 2 MiB /
+ * 20 MiB / 2 MiB-rounded size, (iii) best-fit-with-coalescing search, split
+ * and merge, (iv) caching of freed blocks, (v) OOM only after reclaiming
+ * cached segments fails -- and reports the peak of the segment-sum time
+ * series ("The Estimated Peak Memory is then identified as the maximum value
+ * in this time series"). libxmem does this for a BATCH of
+ * independent traces on one GPU, one warp per trace. The exact rules and
+ * every reading of the paper are in DESIGN.md §Readings (Q1-Q16).
+ *
+ * Conventions for every entry point:
+ *   - returns int: XM_OK (0) or a negative XM_E* code; never throws, never
+ *     aborts. xm_last_error() returns a thread-local message for the last
+ *     failing call on this thread.
+ *   - "host" pointers are CPU memory, "device" pointers are CUDA device memory
+ *     of the current device; the caller owns every pointer it passes in.
+ *   - device entry points are asynchronous on the given cudaStream_t (passed
+ *     as void* so this header needs no CUDA include) and never allocate
+ *     device memory: the caller provides scratch of xm_scratch_bytes().
+ *   - all sizes are in bytes unless a name says otherwise.
+ */
+#ifndef XMEM_H_
+#define XMEM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- errors */
+#define XM_OK 0
+#define XM_EINVAL (-1)  /* malformed argument or trace (contract violation,   */
+                        /* SPEC.md:231,249,258,267)                           */
+#define XM_ECUDA (-2)   /* a CUDA runtime call failed                         */
+#define XM_ENOMEM (-3)  /* host allocation failed, or scratch too small       */
+#define XM_ERANGE (-4)  /* a value exceeds a documented limit                 */
+
+/* ------------------------------------------------------- per-trace status */
+#define XM_T_OK 0        /* replayed every event                               */
+#define XM_T_OOM 1       /* simulated OOM (PAPER.md:260 (v); Eq. 1):  */
+                         /* a result, not an error (SPEC.md:284 D4)            */
+#define XM_T_OVERFLOW 2  /* state exceeded its arena (defensive; never occurs  */
+                         /* when scratch is sized by xm_scratch_bytes)          */
+
+/* -------------------------------------------------------------- modes */
+#define XM_FULL 0            /* full allocator replay (K2)                     */
+#define XM_ALLOCATED_ONLY 1  /* only peak_allocated / _idx via the segmented   */
+                             /* prefix-scan/max (K1). Exact only with unlimited */
+                             /* capacity, which it requires (else XM_EINVAL).   */
+
+/* Wire format limits (checked by xm_load_traces).                          */
+#define XM_ID_BITS 28          /* tag bits 0-27: block id                     */
+#define XM_STREAM_SHIFT 28     /* tag bits 28-31: stream (0..15)              */
+#define XM_MAX_REQUEST (1ull << 40)   /* |bytes| must be < 2^40 (1 TiB)       */
+#define XM_UNLIMITED UINT64_MAX
+
+/*
+ * Allocator constants (SPEC.md:210-213 SimConfig; defaults are the PyTorch
+ * CUDACachingAllocator constants the paper defers to, PAPER.md:257 footnote,
+ * confirmed in torch/include/c10/core/AllocatorConfig.h:17-25).
+ * xm_config_default() fills them. min_block must be a power of two and every
+ * other size a multiple of it.
+ */
+typedef struct {
+  uint64_t min_block;       /* 512      round-up granule, PAPER.md:154,256 (i)  */
+  uint64_t small_size;      /* 1 MiB    small-pool threshold (s <= small_size)  */
+  uint64_t small_buffer;    /* 2 MiB    small segment             */
+  uint64_t large_buffer;    /* 20 MiB   segment for small_size < s < min_large, */
+                            /*          PAPER.md:654                            */
+  uint64_t min_large_alloc; /* 10 MiB   at or above: round to round_large       */
+  uint64_t round_large;     /* 2 MiB                                            */
+  uint64_t capacity;        /* device capacity; XM_UNLIMITED (default) = none   */
+  uint32_t large_split_strict; /* 1 (default): large split iff remainder >     */
+                               /* small_size (torch); 0: >=       */
+  uint32_t mode;               /* XM_FULL (default) or XM_ALLOCATED_ONLY        */
+  uint32_t smem_per_warp;      /* shared-memory state budget per warp in bytes; */
+                               /* 0 = choose automatically                      */
+  uint32_t warps_per_cta;      /* 0 = default (4)                               */
+} xm_config;
+
+/*
+ * Per-trace result, 64 bytes, written by xm_simulate_batch at index t of the
+ * caller's trace order. Field names map to torch.cuda.memory_stats() keys.
+ * "idx" fields are the FIRST event index whose post-event value reaches the
+ * maximum (reading Q7); events at or after a failing index are not counted.
+ */
+typedef struct {
+  uint64_t peak_allocated;      /* max sum of round_up(request) of live blocks   */
+                                /* (the prefix-scan/max quantity)   */
+  uint64_t peak_allocated_blk;  /* max sum of allocated block sizes (SPEC.md:219;*/
+                                /* torch allocated_bytes.all.peak), reading Q2   */
+  uint64_t peak_reserved;       /* max sum of segment sizes = the paper's Mpeak  */
+                                /* (torch reserved_bytes.all.peak) */
+  uint64_t final_reserved;      /* reserved after the last processed event       */
+  uint32_t peak_allocated_idx;
+  uint32_t peak_allocated_blk_idx;
+  uint32_t peak_reserved_idx;
+  uint32_t n_seg_alloc;         /* segments obtained from the device level       */
+  uint32_t n_seg_release;       /* segments returned by reclamation (Q3)         */
+  uint32_t max_live_segments;
+  uint32_t events_done;         /* = n_events if status==XM_T_OK, else the index */
+                                /* of the failing event (reading Q9)             */
+  uint16_t status;              /* XM_T_*                                        */
+  uint16_t n_free_blocks_end;   /* free blocks after the last event, saturated   */
+                                /* at 65535 (== live segments for a closed trace)*/
+} xm_result;
+
+/* Batch summary computed by xm_peaks. */
+typedef struct {
+  uint64_t n_traces;
+  uint64_t events_done;         /* sum of events_done                            */
+  uint64_t n_oom;               /* traces with status XM_T_OOM                   */
+  uint64_t n_overflow;          /* traces with status XM_T_OVERFLOW (must be 0)  */
+  uint64_t max_peak_reserved;
+  uint64_t max_peak_allocated;
+  uint64_t sum_peak_reserved;
+  uint64_t n_predicted_oom;     /* Eq. 1:    */
+                                /* status==OOM or peak_reserved > capacity_for_eq1*/
+} xm_summary;
+
+/* Opaque validated + packed batch of traces (host memory, page-locked when   */
+/* CUDA is available).                                                        */
+typedef struct xm_traces xm_traces;
+
+/* Device view of a batch, as passed to xm_simulate_batch. All pointers are   */
+/* DEVICE memory owned by the caller, laid out exactly as xm_traces_views    */
+/* returns them (normally copied there by the caller).                        */
+typedef struct {
+  const int64_t* bytes;     /* [n_events] signed request bytes: +req alloc, -req free */
+  const uint32_t* tag;      /* [n_events] dense id (bits 0-26) | stream << 28         */
+  const int64_t* off;       /* [n_traces+1] trace t = events [off[t], off[t+1])      */
+  const uint32_t* n_ids;    /* [n_traces] dense id space of each trace (= max live)  */
+  const uint32_t* order;    /* [n_traces] processing order, longest first (LPT)      */
+  const uint64_t* capacity; /* [n_traces] per-trace capacity or NULL (cfg->capacity) */
+  int64_t n_traces;
+  int64_t n_events;
+  uint32_t max_ids;         /* max over n_ids                                        */
+  uint32_t max_events;      /* max trace length                                      */
+} xm_batch;
+
+/* Fill *cfg with the defaults above. */
+void xm_config_default(xm_config* cfg);
+
+/*
+ * Validate and pack a batch of host traces (SPEC.md:156-163 ordered sequence;
+ * signed-bytes convention SPEC.md:27).
+ *   bytes[n_events], tag[n_events], off[n_traces+1]: HOST, caller-owned, read only.
+ *   Array order is replay order (reading Q6). Block ids may be any 28-bit values;
+ *   they are renumbered densely (an id is reused after its free) so each trace's
+ *   id space is its maximum number of live blocks.
+ * Rejects (XM_EINVAL, *bad_trace = first offending trace): off not monotone or
+ *   off[0] != 0; a zero-byte event (reading Q8); |bytes| >=
+ *   XM_MAX_REQUEST (XM_ERANGE); an alloc of a live id; a free of a
+ *   non-live id or with |bytes| != the alloc's request; a trace
+ *   with more than 2^27 live blocks or 2^32-1 events (XM_ERANGE).
+ * On success *out is owned by the library until xm_free_traces(*out).
+ */
+int xm_load_traces(const int64_t* bytes, const uint32_t* tag, const int64_t* off,
+                   int64_t n_traces, xm_traces** out, int64_t* bad_trace);
+
+/* Borrow host views of a packed batch (valid until xm_free_traces). Any output */
+/* pointer may be NULL. The views fill an xm_batch after copying to device.     */
+int xm_traces_views(const xm_traces* tr, const int64_t** bytes, const uint32_t** tag,
+                    const int64_t** off, const uint32_t** n_ids, const uint32_t** order,
+                    int64_t* n_traces, int64_t* n_events, uint32_t* max_ids,
+                    uint32_t* max_events);
+
+void xm_free_traces(xm_traces* tr);
+
+/*
+ * Device scratch needed by xm_simulate_batch for this batch and config
+ * (work counters + per-warp global-memory state arenas for traces whose state
+ * does not fit the shared-memory budget). Host-only computation.
+ */
+size_t xm_scratch_bytes(const xm_batch* batch, const xm_config* cfg);
+
+/*
+ * Replay every trace of the batch on the current device,
+ * asynchronously on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   batch: host struct holding DEVICE pointers (see xm_batch).
+ *   d_scratch[scratch_bytes]: DEVICE scratch, >= xm_scratch_bytes(); contents
+ *     on entry are ignored.
+ *   d_out[n_traces]: DEVICE output, one xm_result per trace in caller order.
+ * Errors: XM_EINVAL (bad config: min_block not a power of two, sizes not
+ * multiples of it, XM_ALLOCATED_ONLY with finite capacity), XM_ENOMEM
+ * (scratch too small), XM_ECUDA (launch failure). A simulated OOM is a
+ * per-trace status, not an error.
+ */
+int xm_simulate_batch(const xm_batch* batch, const xm_config* cfg, void* d_scratch,
+                      size_t scratch_bytes, xm_result* d_out, void* stream);
+
+/*
+ * Per-trace results to host and a batch summary. Synchronises `stream`.
+ *   d_res[n]: DEVICE results. h_out[n]: HOST destination or NULL.
+ *   capacity_for_eq1: M_d^max of Eq. 1 for n_predicted_oom;
+ *     XM_UNLIMITED = only simulated OOMs count.
+ */
+int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_summary* h_sum,
+             uint64_t capacity_for_eq1, void* stream);
+
+/*
+ * End-to-end entry point with HOST buffers: copies the packed batch to the
+ * DEVICE workspace d_ws (>= xm_host_ws_bytes()), replays it, copies the
+ * results to h_out[n_traces] (HOST) and synchronises `stream`.
+ *   capacity: HOST [n_traces] per-trace capacities or NULL.
+ */
+size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg);
+int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_config* cfg,
+                     void* d_ws, size_t ws_bytes, xm_result* h_out, void* stream);
+
+/* Number of device kernel launches the last xm_simulate_batch on this thread */
+/* issued (for the bench's gpu_launches claim).                               */
+int xm_last_launch_count(void);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* xm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XMEM_H_ */

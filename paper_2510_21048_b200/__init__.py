@@ -1,0 +1,286 @@
+"""paper_2510_21048_b200 -- B200-native batched caching-allocator trace replay.
+
+Thin ctypes binding over libxmem.so (include/xmem.h): argument marshalling
+only. Every step of the hot path runs in the library's CUDA kernels; there is
+no Python or CPU fallback -- on a GPU box, a missing or unloadable library is
+a hard error. PyTorch is used for device memory and streams only.
+
+    tr  = load_traces(bytes, tag, off)          # xm_load_traces (host, validated)
+    dev = tr.to_device()                        # torch device tensors
+    res = simulate_batch(dev, Config())         # xm_simulate_batch -> uint8[T, 64] on device
+    pk  = peaks(res)                            # xm_peaks -> dict of numpy arrays
+    pk  = simulate_host(tr, Config())           # end to end with host buffers (xm_simulate_host)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import _build
+
+__all__ = ["Config", "Traces", "DeviceBatch", "load_traces", "simulate_batch", "peaks",
+           "simulate_host", "lib", "XMemError", "RESULT_DTYPE", "FIELDS", "UNLIMITED"]
+
+UNLIMITED = 0xFFFFFFFFFFFFFFFF
+XM_FULL, XM_ALLOCATED_ONLY = 0, 1
+STATUS = {0: "ok", 1: "oom", 2: "overflow"}
+
+# numpy view of xm_result (64 B, include/xmem.h)
+RESULT_DTYPE = np.dtype([
+    ("peak_allocated", "<u8"), ("peak_allocated_blk", "<u8"), ("peak_reserved", "<u8"),
+    ("final_reserved", "<u8"), ("peak_allocated_idx", "<u4"), ("peak_allocated_blk_idx", "<u4"),
+    ("peak_reserved_idx", "<u4"), ("n_seg_alloc", "<u4"), ("n_seg_release", "<u4"),
+    ("max_live_segments", "<u4"), ("events_done", "<u4"), ("status", "<u2"),
+    ("n_free_blocks_end", "<u2")])
+assert RESULT_DTYPE.itemsize == 64
+FIELDS = list(RESULT_DTYPE.names)
+
+
+class XMemError(RuntimeError):
+    pass
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("min_block", ctypes.c_uint64), ("small_size", ctypes.c_uint64),
+                ("small_buffer", ctypes.c_uint64), ("large_buffer", ctypes.c_uint64),
+                ("min_large_alloc", ctypes.c_uint64), ("round_large", ctypes.c_uint64),
+                ("capacity", ctypes.c_uint64), ("large_split_strict", ctypes.c_uint32),
+                ("mode", ctypes.c_uint32), ("smem_per_warp", ctypes.c_uint32),
+                ("warps_per_cta", ctypes.c_uint32)]
+
+
+class _Batch(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_void_p), ("tag", ctypes.c_void_p), ("off", ctypes.c_void_p),
+                ("n_ids", ctypes.c_void_p), ("order", ctypes.c_void_p),
+                ("capacity", ctypes.c_void_p), ("n_traces", ctypes.c_int64),
+                ("n_events", ctypes.c_int64), ("max_ids", ctypes.c_uint32),
+                ("max_events", ctypes.c_uint32)]
+
+
+class _Summary(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in
+                ("n_traces", "events_done", "n_oom", "n_overflow", "max_peak_reserved",
+                 "max_peak_allocated", "sum_peak_reserved", "n_predicted_oom")]
+
+
+@dataclass
+class Config:
+    """xm_config (include/xmem.h); defaults = torch CUDACachingAllocator constants."""
+    min_block: int = 512
+    small_size: int = 1 << 20
+    small_buffer: int = 2 << 20
+    large_buffer: int = 20 << 20
+    min_large_alloc: int = 10 << 20
+    round_large: int = 2 << 20
+    capacity: int = UNLIMITED
+    large_split_strict: int = 1
+    mode: int = XM_FULL
+    smem_per_warp: int = 0
+    warps_per_cta: int = 0
+
+    def c(self) -> _Cfg:
+        return _Cfg(self.min_block, self.small_size, self.small_buffer, self.large_buffer,
+                    self.min_large_alloc, self.round_large, self.capacity,
+                    self.large_split_strict, self.mode, self.smem_per_warp, self.warps_per_cta)
+
+
+_lib = None
+
+
+def lib():
+    """Load libxmem.so (building it in-tree if stale). Fails loudly."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path) or os.environ.get("XM_REBUILD"):
+            _build.build()
+        L = ctypes.CDLL(path)
+        P, I64, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
+        L.xm_config_default.argtypes = [P]
+        L.xm_load_traces.argtypes = [P, P, P, I64, ctypes.POINTER(P), ctypes.POINTER(I64)]
+        L.xm_traces_views.argtypes = [P] * 6 + [ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                                ctypes.POINTER(ctypes.c_uint32),
+                                                ctypes.POINTER(ctypes.c_uint32)]
+        L.xm_free_traces.argtypes = [P]
+        L.xm_free_traces.restype = None
+        L.xm_scratch_bytes.argtypes = [ctypes.POINTER(_Batch), ctypes.POINTER(_Cfg)]
+        L.xm_scratch_bytes.restype = ctypes.c_size_t
+        L.xm_simulate_batch.argtypes = [ctypes.POINTER(_Batch), ctypes.POINTER(_Cfg), P,
+                                        ctypes.c_size_t, P, P]
+        L.xm_peaks.argtypes = [P, I64, P, ctypes.POINTER(_Summary), U64, P]
+        L.xm_host_ws_bytes.argtypes = [P, ctypes.POINTER(_Cfg)]
+        L.xm_host_ws_bytes.restype = ctypes.c_size_t
+        L.xm_simulate_host.argtypes = [P, P, ctypes.POINTER(_Cfg), P, ctypes.c_size_t, P, P]
+        L.xm_last_error.restype = ctypes.c_char_p
+        L.xm_last_launch_count.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().xm_last_error().decode(errors="replace")
+        raise XMemError(f"{what} failed ({rc}): {msg}")
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Traces:
+    """A validated, renumbered, packed host batch (xm_traces, page-locked)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        L = lib()
+        ptrs = [ctypes.c_void_p() for _ in range(5)]
+        nt, ne = ctypes.c_int64(), ctypes.c_int64()
+        mi, me = ctypes.c_uint32(), ctypes.c_uint32()
+        _check(L.xm_traces_views(handle, *[ctypes.byref(p) for p in ptrs], ctypes.byref(nt),
+                                 ctypes.byref(ne), ctypes.byref(mi), ctypes.byref(me)),
+               "xm_traces_views")
+        self.n_traces, self.n_events = nt.value, ne.value
+        self.max_ids, self.max_events = mi.value, me.value
+
+        def view(p, dt, n):
+            if n == 0:
+                return np.zeros(0, dt)
+            buf = (ctypes.c_char * (np.dtype(dt).itemsize * n)).from_address(p.value)
+            return np.frombuffer(buf, dt, n)
+        self.bytes = view(ptrs[0], np.int64, self.n_events)
+        self.tag = view(ptrs[1], np.uint32, self.n_events)
+        self.off = view(ptrs[2], np.int64, self.n_traces + 1)
+        self.n_ids = view(ptrs[3], np.uint32, self.n_traces)
+        self.order = view(ptrs[4], np.uint32, self.n_traces)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.xm_free_traces(h)
+            self._h = None
+
+    def to_device(self, device=None, capacity: Optional[np.ndarray] = None,
+                  non_blocking: bool = False) -> "DeviceBatch":
+        import torch
+        device = torch.device(device or "cuda")
+
+        def t(a):
+            return torch.from_numpy(a).to(device, non_blocking=non_blocking)
+        cap = None
+        if capacity is not None:
+            cap = torch.from_numpy(np.ascontiguousarray(capacity, np.uint64).view(np.int64)).to(
+                device, non_blocking=non_blocking)
+        return DeviceBatch(t(self.bytes), t(self.tag.view(np.int32)), t(self.off),
+                           t(self.n_ids.view(np.int32)), t(self.order.view(np.int32)), cap,
+                           self.n_traces, self.n_events, self.max_ids, self.max_events)
+
+
+@dataclass
+class DeviceBatch:
+    bytes: "object"
+    tag: "object"
+    off: "object"
+    n_ids: "object"
+    order: "object"
+    capacity: "object"
+    n_traces: int
+    n_events: int
+    max_ids: int
+    max_events: int
+    _scratch: Dict = field(default_factory=dict)
+
+    def c(self) -> _Batch:
+        def p(x):
+            return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
+        return _Batch(p(self.bytes), p(self.tag), p(self.off), p(self.n_ids), p(self.order),
+                      p(self.capacity), self.n_traces, self.n_events, self.max_ids,
+                      self.max_events)
+
+
+def load_traces(bytes_: np.ndarray, tag: np.ndarray, off: np.ndarray) -> Traces:
+    """xm_load_traces: validate + renumber + pack host traces."""
+    b = np.ascontiguousarray(bytes_, np.int64)
+    g = np.ascontiguousarray(tag, np.uint32)
+    o = np.ascontiguousarray(off, np.int64)
+    h = ctypes.c_void_p()
+    bad = ctypes.c_int64(-1)
+    rc = lib().xm_load_traces(_np_ptr(b), _np_ptr(g), _np_ptr(o), len(o) - 1, ctypes.byref(h),
+                              ctypes.byref(bad))
+    if rc != 0:
+        msg = lib().xm_last_error().decode(errors="replace")
+        err = XMemError(f"xm_load_traces failed ({rc}) at trace {bad.value}: {msg}")
+        err.code, err.trace = rc, bad.value
+        raise err
+    return Traces(h)
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def scratch_bytes(dev: DeviceBatch, cfg: Config = Config()) -> int:
+    b, c = dev.c(), cfg.c()
+    return int(lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(c)))
+
+
+def simulate_batch(dev: DeviceBatch, cfg: Config = Config(), stream=None, out=None):
+    """xm_simulate_batch on the current (or given) torch stream.
+    Returns a uint8 device tensor [n_traces, 64] holding xm_result records."""
+    import torch
+    b, c = dev.c(), cfg.c()
+    need = int(lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(c)))
+    key = (cfg.mode, cfg.smem_per_warp, cfg.warps_per_cta)
+    scr = dev._scratch.get(key)
+    if scr is None or scr.numel() < need:
+        scr = torch.empty(max(need, 256), dtype=torch.uint8, device=dev.off.device)
+        dev._scratch[key] = scr
+    if out is None:
+        out = torch.empty((dev.n_traces, 64), dtype=torch.uint8, device=dev.off.device)
+    rc = lib().xm_simulate_batch(ctypes.byref(b), ctypes.byref(c), ctypes.c_void_p(scr.data_ptr()),
+                                 scr.numel(), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream))
+    _check(rc, "xm_simulate_batch")
+    return out
+
+
+def last_launch_count() -> int:
+    return int(lib().xm_last_launch_count())
+
+
+def peaks(res, capacity_for_eq1: int = UNLIMITED, stream=None):
+    """xm_peaks: device results -> (structured numpy array, summary dict)."""
+    n = res.shape[0]
+    h = np.zeros(n, RESULT_DTYPE)
+    s = _Summary()
+    rc = lib().xm_peaks(ctypes.c_void_p(res.data_ptr()), n, _np_ptr(h), ctypes.byref(s),
+                        ctypes.c_uint64(capacity_for_eq1), _stream_ptr(stream))
+    _check(rc, "xm_peaks")
+    return h, {k: int(getattr(s, k)) for k, _ in _Summary._fields_}
+
+
+def simulate_host(tr: Traces, cfg: Config = Config(), capacity: Optional[np.ndarray] = None,
+                  stream=None, workspace=None):
+    """xm_simulate_host: host buffers in, host results out (H2D + replay + D2H)."""
+    import torch
+    c = cfg.c()
+    need = int(lib().xm_host_ws_bytes(tr._h, ctypes.byref(c)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device="cuda")
+    h = np.zeros(tr.n_traces, RESULT_DTYPE)
+    cap = None
+    if capacity is not None:
+        cap = np.ascontiguousarray(capacity, np.uint64)
+    rc = lib().xm_simulate_host(tr._h, _np_ptr(cap) if cap is not None else None, ctypes.byref(c),
+                                ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                _np_ptr(h), _stream_ptr(stream))
+    _check(rc, "xm_simulate_host")
+    return h, workspace
+
+
+def as_dict(h: np.ndarray) -> Dict[str, np.ndarray]:
+    return {k: h[k].astype(np.uint64) for k in FIELDS}

@@ -1,0 +1,59 @@
+// xm_internal.h -- declarations shared by the product's translation units
+// (loader.cpp, capi.cu, replay.cu, scan.cu). Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "xmem.h"
+
+namespace xm_internal {
+
+int set_error(int code, const std::string& msg);
+void clear_error();
+bool cuda_usable();
+
+struct xm_traces_info {
+  const int64_t* bytes;
+  const uint32_t* tag;
+  const int64_t* off;
+  const uint32_t* n_ids;
+  const uint32_t* order;
+  int64_t n_traces, n_events;
+  uint32_t max_ids, max_events;
+};
+const xm_traces_info traces_info(const xm_traces* tr);
+
+// Allocator constants in units of min_block.
+struct UnitConfig {
+  uint32_t unit_shift;   // log2(min_block)
+  uint32_t small_u;      // small_size / min_block
+  uint32_t sbuf_u;       // small_buffer / min_block
+  uint32_t lbuf_u;       // large_buffer / min_block
+  uint32_t minlarge_u;   // min_large_alloc / min_block
+  uint32_t rlarge_u;     // round_large / min_block
+  uint32_t strict;       // large split iff rem > small (1) or >= (0)
+};
+
+// Launch geometry + scratch layout of the replay kernel for one batch.
+struct ReplayPlan {
+  int warps_per_cta;
+  int ctas;
+  uint32_t smem_per_warp;   // bytes of shared-memory state per warp
+  size_t arena_per_warp;    // bytes of global-memory state per warp (overflow path)
+  uint32_t arena_ids, arena_free;
+  size_t scratch_bytes;     // header + arenas
+};
+
+int make_unit_config(const xm_config* cfg, UnitConfig* u);
+ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg);
+
+// Kernel launchers (replay.cu / scan.cu). Return cudaError_t as int.
+int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
+                  const ReplayPlan& plan, void* d_scratch, xm_result* d_out, void* stream,
+                  int* n_launches);
+int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t scratch_bytes,
+                xm_result* d_out, void* stream, int* n_launches);
+size_t scan_scratch_bytes(const xm_batch* b);
+
+}  // namespace xm_internal

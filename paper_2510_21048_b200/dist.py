@@ -1,0 +1,74 @@
+"""Multi-GPU sharding of a trace batch.
+
+Traces are independent, so the path shards with no data-path collective:
+every rank computes the same deterministic longest-processing-time (LPT) plan
+from the per-trace event counts, replays only its shard, and the per-trace
+64 B results are gathered once per batch with one all_gather_into_tensor
+(NCCL over NVLink/NVSwitch; gloo on CPU for tests). Scaling is weak: each rank
+holds a fixed share of the work.
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+
+
+@dataclass
+class ShardPlan:
+    world: int
+    shards: List[np.ndarray]    # global trace indices per rank (in replay order)
+    events: np.ndarray          # events per rank
+
+    @property
+    def max_shard(self) -> int:
+        return max((len(s) for s in self.shards), default=0)
+
+
+def lpt_plan(lengths: np.ndarray, world: int) -> ShardPlan:
+    """Greedy LPT: traces by decreasing length, each to the least-loaded rank
+    (ties -> lowest rank). Deterministic for identical inputs on every rank."""
+    lengths = np.asarray(lengths, np.int64)
+    order = np.argsort(-lengths, kind="stable")
+    heap = [(0, r) for r in range(world)]
+    heapq.heapify(heap)
+    buckets: List[List[int]] = [[] for _ in range(world)]
+    loads = np.zeros(world, np.int64)
+    for t in order:
+        load, r = heapq.heappop(heap)
+        buckets[r].append(int(t))
+        load += int(lengths[t])
+        loads[r] = load
+        heapq.heappush(heap, (load, r))
+    return ShardPlan(world, [np.asarray(b, np.int64) for b in buckets], loads)
+
+
+def gather_results(local, plan: ShardPlan, rank: int, group=None):
+    """all_gather_into_tensor of per-rank uint8[T_r, 64] results (padded to the
+    largest shard). Returns uint8[T_total, 64] in GLOBAL trace order on every
+    rank (same device as `local`)."""
+    import torch
+    import torch.distributed as dist
+    W = plan.world
+    M = plan.max_shard
+    width = local.shape[1] if local.dim() == 2 else 64
+    pad = torch.zeros((M, width), dtype=torch.uint8, device=local.device)
+    pad[: local.shape[0]] = local
+    full = torch.empty((W * M, width), dtype=torch.uint8, device=local.device)
+    dist.all_gather_into_tensor(full, pad, group=group)
+    return reorder(full, plan)
+
+
+def reorder(full, plan: ShardPlan):
+    """[W*M, 64] rank-major padded results -> [T_total, 64] in global order."""
+    import torch
+    M = plan.max_shard
+    T = sum(len(s) for s in plan.shards)
+    src = np.concatenate([r * M + np.arange(len(s)) for r, s in enumerate(plan.shards)]) \
+        if T else np.zeros(0, np.int64)
+    dst = np.concatenate(plan.shards) if T else np.zeros(0, np.int64)
+    perm = np.empty(T, np.int64)
+    perm[dst] = src
+    return full.index_select(0, torch.from_numpy(perm).to(full.device))

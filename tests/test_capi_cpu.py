@@ -1,0 +1,141 @@
+"""The C-ABI library builds, loads, exports every declared symbol, and its
+host-side logic (validation, renumbering, LPT order) is correct. No GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2510_21048_b200 as xm
+from workloads import fuzz, hand
+from workloads.trace import TraceBuilder
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "xmem.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(xm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("xm_load_traces", "xm_simulate_batch", "xm_peaks", "xm_last_error",
+                 "xm_scratch_bytes", "xm_traces_views", "xm_free_traces", "xm_simulate_host"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = xm.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+        assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
+
+
+def test_result_struct_is_64_bytes():
+    assert xm.RESULT_DTYPE.itemsize == 64
+
+
+def test_config_default_matches_binding():
+    c = xm._Cfg()
+    xm.lib().xm_config_default(ctypes.byref(c))
+    d = xm.Config()
+    for f, _ in xm._Cfg._fields_:
+        assert getattr(c, f) == getattr(d, f), f
+
+
+def _max_live(by):
+    return int(np.cumsum(np.sign(by)).max()) if len(by) else 0
+
+
+def test_loader_renumbers_densely():
+    c = fuzz.spec1_corpus(50, 500, salt=31)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    assert tr.n_traces == 50 and tr.n_events == c.n_events
+    assert (tr.bytes == c.bytes).all() and (tr.off == c.off).all()
+    assert (tr.tag >> 28 == c.tag >> 28).all()                  # streams preserved
+    for t in range(c.n_traces):
+        a, b = c.off[t], c.off[t + 1]
+        by = c.bytes[a:b]
+        dense = tr.tag[a:b] & ((1 << 28) - 1)
+        raw = c.tag[a:b] & ((1 << 28) - 1)
+        assert tr.n_ids[t] == _max_live(by)
+        assert dense.max() < tr.n_ids[t]
+        # the renaming is a bijection between live raw ids and live dense ids
+        live = {}
+        for i in range(len(by)):
+            if by[i] > 0:
+                assert dense[i] not in live.values()
+                live[raw[i]] = dense[i]
+            else:
+                assert live.pop(raw[i]) == dense[i]
+    assert tr.max_ids == tr.n_ids.max()
+    assert tr.max_events == np.diff(c.off).max()
+
+
+def test_loader_lpt_order():
+    c = fuzz.spec1_corpus(40, 700, salt=32)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    L = np.diff(c.off)
+    assert sorted(tr.order.tolist()) == list(range(40))
+    assert (np.diff(L[tr.order]) <= 0).all()
+
+
+@pytest.mark.parametrize("events,code", [
+    ([(0, 1)], -1),                    # zero-byte request
+    ([(512, 1), (512, 1)], -1),        # alloc of a live id
+    ([(-512, 1)], -1),                 # free of a non-live id
+    ([(512, 1), (-1024, 1)], -1),      # free size mismatch
+    ([(1 << 40, 1)], -4),              # request >= 2^40 (XM_ERANGE)
+])
+def test_loader_rejects(events, code):
+    good = TraceBuilder().alloc(0, 100).free(0).end_trace().build()
+    by = np.concatenate([good.bytes, np.array([e[0] for e in events], np.int64)])
+    tg = np.concatenate([good.tag, np.array([e[1] for e in events], np.uint32)])
+    off = np.array([0, 2, len(by)], np.int64)
+    with pytest.raises(xm.XMemError) as e:
+        xm.load_traces(by, tg, off)
+    assert e.value.code == code and e.value.trace == 1
+
+
+def test_loader_accepts_id_reuse_and_empty_traces():
+    b = TraceBuilder()
+    b.alloc(7, 100).free(7).alloc(7, 200).free(7).end_trace()
+    b.end_trace()                                   # empty trace
+    b.alloc(1 << 27, 5, stream=3).free(1 << 27, stream=3).end_trace()
+    bt = b.build()
+    tr = xm.load_traces(bt.bytes, bt.tag, bt.off)
+    assert tr.n_ids.tolist() == [1, 0, 1]
+    assert (tr.tag[-2:] >> 28 == 3).all()
+
+
+def test_loader_bad_offsets():
+    with pytest.raises(xm.XMemError):
+        xm.load_traces(np.array([5, -5], np.int64), np.zeros(2, np.uint32),
+                       np.array([0, 2, 1], np.int64))
+
+
+def test_simulate_fails_loudly_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c = hand.h1(512, 3)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    b = xm._Batch(None, None, None, None, None, None, tr.n_traces, tr.n_events, tr.max_ids,
+                  tr.max_events)
+    cfg = xm.Config().c()
+    rc = xm.lib().xm_simulate_batch(ctypes.byref(b), ctypes.byref(cfg), None, 0, None, None)
+    assert rc != 0
+
+
+def test_scratch_sizing_is_host_only():
+    c = fuzz.spec1_corpus(10, 300, salt=33)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    b = xm._Batch(None, None, None, None, None, None, tr.n_traces, tr.n_events, tr.max_ids,
+                  tr.max_events)
+    cfg = xm.Config().c()
+    n = xm.lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(cfg))
+    assert n >= 256

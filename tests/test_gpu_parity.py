@@ -1,0 +1,145 @@
+"""CUDA path (libxmem.so, through the C-ABI) vs the oracle, bit-exact on every
+result field of every trace. Integer path: the bar is exact equality."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle
+import paper_2510_21048_b200 as xm
+from gpu_util import COMPARE, assert_parity, gpu_run, oracle_run
+from workloads import concat, fuzz, hand, suites
+from workloads.trace import TraceBuilder
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+def _check(batch, cfg=None, strict=1):
+    h, _ = gpu_run(batch, cfg)
+    o = oracle_run(batch, strict=strict, parallel=batch.n_events > 2_000_000)
+    assert_parity(batch, h, o)
+    return h
+
+
+def test_hand_traces(golden):
+    named = hand.all_named()
+    b = concat(list(named.values()))
+    h = _check(b)
+    names = list(named)
+    for name, g in golden.items():
+        t = names.index(name)
+        for k, v in g["expect"].items():
+            if k in COMPARE:
+                assert int(h[k][t]) == v, (name, k)
+
+
+def test_spec1_fuzz_corpus():
+    _check(fuzz.spec1_corpus(1000, 1000, salt=1))
+
+
+def test_small_pool_corpus():
+    _check(fuzz.small_size_corpus(400, 600, salt=2))
+
+
+def test_capacity_corpus_reclaim_and_oom():
+    b = fuzz.capacity_corpus(400, 800, salt=3)
+    h = _check(b)
+    assert (h["status"] == 1).sum() > 20 and (h["n_seg_release"] > 0).sum() > 20
+
+
+def test_spec_split_variant():
+    b = fuzz.spec1_corpus(200, 600, salt=4)
+    _check(b, xm.Config(large_split_strict=0), strict=0)
+
+
+def test_fragmentation_stress_spills_to_global_arena():
+    # 2048 free holes do not fit a 16 KB shared-memory slot: exercises the
+    # overflow -> global arena restart
+    b = concat([fuzz.fragmentation_stress(), fuzz.fragmentation_stress(8192, 1024, "frag2")])
+    _check(b, xm.Config(smem_per_warp=16384))
+    _check(b)
+
+
+@pytest.mark.parametrize("spw,wpc", [(4096, 1), (8192, 2), (24576, 4), (49152, 8)])
+def test_launch_geometries(spw, wpc):
+    b = concat([fuzz.spec1_corpus(150, 800, salt=7), fuzz.capacity_corpus(50, 500, salt=8)])
+    _check(b, xm.Config(smem_per_warp=spw, warps_per_cta=wpc))
+
+
+def test_edge_cases():
+    tb = TraceBuilder()
+    tb.end_trace()                                    # empty
+    tb.alloc(0, 1).end_trace()                        # open trace, one event
+    tb.alloc(0, (1 << 40) - 1).end_trace()            # largest request
+    tb.alloc(0, 3 << 30).free(0).alloc(1, 3 << 30).end_trace(capacity=4 << 30)
+    tb.alloc(0, 5 << 30).end_trace(capacity=4 << 30)  # oversize request -> OOM at 0
+    for s in range(16):                               # 16 streams
+        tb.alloc(s, 1000 + s, stream=s)
+    for s in range(16):
+        tb.free(s, stream=s)
+    tb.end_trace()
+    for i in range(70):                               # ragged tile tail: 70 events
+        tb.alloc(i, 512 * (i + 1))
+    tb.end_trace()
+    _check(tb.build())
+
+
+def test_config1_mlp():
+    _check(suites.config1())
+
+
+def test_config2_resnet50_sweep():
+    _check(suites.config2())
+
+
+def test_config3_bert_gpt2_streams():
+    _check(suites.config3())
+
+
+def test_config4_full_suite():
+    """BASELINE configs[3] at full size (5209 traces) in the bench's launch config."""
+    b = suites.config4()
+    h = _check(b)
+    assert (h["status"] == 2).sum() == 0
+
+
+def test_host_entry_point_matches_device_path():
+    b = concat([fuzz.capacity_corpus(100, 400, salt=9), suites.config1()])
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    cap = b.capacity
+    h_host, _ = xm.simulate_host(tr, xm.Config(), capacity=cap)
+    h_dev, _ = gpu_run(b)
+    assert (h_host == h_dev).all()
+
+
+def test_allocated_only_mode():
+    b = concat([fuzz.spec1_corpus(300, 1000, salt=10), suites.config2(), suites.config1()])
+    h, _ = gpu_run(b, xm.Config(mode=1))
+    o = oracle_run(b)
+    assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
+
+
+def test_determinism():
+    b = fuzz.capacity_corpus(200, 500, salt=11)
+    h1, _ = gpu_run(b)
+    h2, _ = gpu_run(b)
+    assert (h1 == h2).all()
+
+
+def test_summary_eq1():
+    b = hand.h7()
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    dev = tr.to_device(capacity=b.capacity)
+    res = xm.simulate_batch(dev)
+    _, s = xm.peaks(res)
+    assert s["n_oom"] == 1 and s["n_predicted_oom"] == 1
+    b2 = hand.h4("late")   # 196 MiB peak; Eq. 1 strict at M_max = 196 MiB
+    tr2 = xm.load_traces(b2.bytes, b2.tag, b2.off)
+    r2 = xm.simulate_batch(tr2.to_device())
+    assert xm.peaks(r2, capacity_for_eq1=196 << 20)[1]["n_predicted_oom"] == 0
+    assert xm.peaks(r2, capacity_for_eq1=(196 << 20) - 1)[1]["n_predicted_oom"] == 1

@@ -152,3 +152,44 @@ def mc_lengths(indices, salt: int = 6) -> np.ndarray:
 
 
 CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3, "cfg4": config4}
+
+
+# ---- the bench's global trace pool -------------------
+# index i <  5209: config 4 (ANOVA cells then MC draws with salt 5)
+# index i >= 5209: further MC draws (salt 6) -- N GPUs replay N*5209 traces.
+N_CFG4 = 5209
+N_ANOVA = 3903
+
+
+def _cell_len(cell):
+    name, opt, b, rep = cell
+    return len(_tpl(name, opt, "pos1")[0])
+
+
+def pool_lengths(n: int) -> np.ndarray:
+    cells = anova_cells()[:N_ANOVA]
+    out = np.zeros(n, np.int64)
+    for i in range(n):
+        if i < N_ANOVA:
+            out[i] = _cell_len(cells[i])
+        elif i < N_CFG4:
+            name, opt, b, zg, cap, _ = mc_draw(i - N_ANOVA, 5)
+            out[i] = len(_tpl(name, opt, zg)[0])
+        else:
+            name, opt, b, zg, cap, _ = mc_draw(i - N_CFG4, 6)
+            out[i] = len(_tpl(name, opt, zg)[0])
+    return out
+
+
+def pool_batch(indices) -> Batch:
+    cells = anova_cells()[:N_ANOVA]
+    items = []
+    for i in indices:
+        i = int(i)
+        if i < N_ANOVA:
+            items.append(anova_trace(i, cells[i]))
+        elif i < N_CFG4:
+            items.append(mc_trace(i - N_ANOVA, 5))
+        else:
+            items.append(mc_trace(i - N_CFG4, 6))
+    return _assemble(items)
