@@ -4,28 +4,37 @@
 // batch: (i) round-up, (ii) segment sizing, (iii) best-fit-with-coalescing
 // search / split / merge, (iv) caching, (v) two-level OOM with reclamation,
 // plus the time-series peaks. Rules and readings: DESIGN.md
-// §Readings; per-step citations inline.
+// §2 (Q1-Q18); per-step citations inline.
 //
-// Execution model:
-//  * persistent grid, one trace per warp, traces pulled longest-first from a
-//    global atomic work counter (host LPT order);
-//  * a trace's allocator state lives in the warp's shared-memory slot when it
-//    fits, else (or when the free list outgrows the slot) in the warp's
-//    global-memory arena, sized so it cannot overflow;
-//  * events stream through registers in 32-event tiles (coalesced loads,
-//    next tile prefetched while the current one is replayed); the allocated
-//    peak of each tile is a warp prefix-scan/max (a3);
-//  * the serial state machine is warp-uniform; the best-fit search is a
-//    warp-strided scan of the free list + ballot/__reduce_min_sync (a5).
+// Execution model (DESIGN.md §6 K2):
+//  * persistent grid, one CTA per SM, 16 warps per CTA, one trace per warp;
+//    traces are pulled longest-first (host LPT order) from one atomic counter;
+//  * each CTA owns a shared-memory HEAP (all of the SM's 227 KB, 512 B pages).
+//    A warp sizes a region for its trace's state (id space + a free-list
+//    guess), takes it FIFO (ticket lock) from the heap, replays, frees it. So
+//    occupancy adapts: few warps hold the big early traces, many hold the
+//    small later ones. A free list that outgrows its guess restarts the trace
+//    in a 4x larger region; a trace larger than the heap runs in a
+//    global-memory arena sized to the exact bound (never overflows);
+//  * events stream through registers in 32-event tiles (coalesced streaming
+//    loads, next tile prefetched); round-up and the allocated-bytes prefix
+//    scan of a tile are lane-parallel (a2, a3);
+//  * the serial state machine is warp-uniform (every lane computes the same
+//    scalars, so no broadcasts); the best-fit search scans the free list
+//    lane-strided with ONE packed 32-bit key per entry (class in the top 5
+//    bits, saturated size below) and __reduce_min_sync; exact (size, pos)
+//    tie-breaking falls back to a full compare only when needed (a5).
 //
-// State (structure of arrays; 21 B per record):
+// State (structure of arrays):
 //  A[id]  allocated block of dense id: pos u64, size u32, prev u32, next u32, cls u8
-//  F[f]   free block f (unordered list, nf entries): same fields
+//  F[f]   free block f (unordered, nf entries): pos u64, key u32, size u32, prev u32, next u32
 //  pos  = segment_index << 32 | offset_in_units  (bump addresses never reused:
 //         (size, pos) order == SPEC D2's (size, segment, offset), reading Q4)
 //  prev/next = address-order neighbours in the segment: kNone, an id, or kF|f
-//  cls  = stream << 1 | small_pool
+//  cls  = stream << 1 | small_pool ;  key = cls << 27 | min(size, 2^27-1)
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "xm_internal.h"
 
@@ -35,8 +44,24 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kF = 0x80000000u;
 constexpr uint32_t kIdMask = 0x07FFFFFFu;
 constexpr uint32_t kAllocBit = 0x08000000u;
+constexpr uint32_t kKeyBits = 27;
+constexpr uint32_t kKeyMax = (1u << kKeyBits) - 1u;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kStatusOk = XM_T_OK, kStatusOom = XM_T_OOM, kStatusOverflow = XM_T_OVERFLOW;
+
+// shared-memory heap geometry
+constexpr uint32_t kPage = 512;
+constexpr uint32_t kHdrBytes = 128;
+constexpr uint32_t kMaxDynSmem = 232448;  // 227 KB, the sm_100 per-CTA maximum
+constexpr uint32_t kMaxPages = (kMaxDynSmem - kHdrBytes) / kPage;  // 453
+constexpr uint32_t kBitmapWords = (kMaxPages + 31) / 32;          // 15
+static_assert(8 + 4 * kBitmapWords <= kHdrBytes, "heap header");
+
+struct HeapHdr {
+  int ticket;
+  int serving;
+  uint32_t bitmap[kBitmapWords];
+};
 
 struct KParams {
   const int64_t* __restrict__ bytes;
@@ -48,10 +73,11 @@ struct KParams {
   uint64_t cap_default;
   int64_t n_traces;
   xm_internal::UnitConfig u;
-  uint32_t smem_per_warp;
-  uint32_t* counter;
+  uint32_t heap_pages;       // pages per CTA heap
+  uint32_t* counter;         // [0] work counter; [1..] arena claim bitmap
   unsigned char* arena;
-  size_t arena_per_warp;
+  size_t arena_bytes;        // bytes per arena slot
+  uint32_t n_arena;
   uint32_t arena_ids, arena_free;
   xm_result* out;
 };
@@ -63,24 +89,15 @@ struct State {
   uint32_t* A_next;
   uint8_t* A_cls;
   uint64_t* F_pos;
+  uint32_t* F_key;
   uint32_t* F_size;
   uint32_t* F_prev;
   uint32_t* F_next;
-  uint8_t* F_cls;
   uint32_t cap_f;
 };
 
-constexpr size_t kRecordBytes = 21;
-
 __host__ __device__ inline size_t state_bytes(uint32_t na, uint32_t nf) {
-  return size_t(na + nf) * kRecordBytes + 16;
-}
-
-__host__ __device__ inline uint32_t free_cap(size_t budget, uint32_t na) {
-  size_t need = size_t(na) * kRecordBytes + 16;
-  if (budget <= need) return 0;
-  size_t c = (budget - need) / kRecordBytes;
-  return c > 0x7FFFFFFFu ? 0x7FFFFFFFu : uint32_t(c);
+  return size_t(na) * 21 + size_t(nf) * 24 + 16;
 }
 
 __device__ inline State carve(unsigned char* base, uint32_t na, uint32_t nf) {
@@ -91,13 +108,17 @@ __device__ inline State carve(unsigned char* base, uint32_t na, uint32_t nf) {
   S.A_size = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
   S.A_prev = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
   S.A_next = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
+  S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_prev = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_next = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.A_cls = p; p += na;
-  S.F_cls = p;
+  S.A_cls = p;
   S.cap_f = nf;
   return S;
+}
+
+__device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
+  return (cls << kKeyBits) | (size < kKeyMax ? size : kKeyMax);
 }
 
 __device__ __forceinline__ void set_next(const State& S, uint32_t ref, uint32_t v) {
@@ -116,10 +137,9 @@ __device__ __forceinline__ void set_prev(const State& S, uint32_t ref, uint32_t 
 __device__ __forceinline__ void f_remove(const State& S, uint32_t f, uint32_t& nf) {
   const uint32_t L = nf - 1;
   if (f != L) {
-    const uint32_t sz = S.F_size[L], pv = S.F_prev[L], nx = S.F_next[L];
+    const uint32_t k = S.F_key[L], sz = S.F_size[L], pv = S.F_prev[L], nx = S.F_next[L];
     const uint64_t pos = S.F_pos[L];
-    const uint8_t c = S.F_cls[L];
-    S.F_size[f] = sz; S.F_pos[f] = pos; S.F_prev[f] = pv; S.F_next[f] = nx; S.F_cls[f] = c;
+    S.F_key[f] = k; S.F_size[f] = sz; S.F_pos[f] = pos; S.F_prev[f] = pv; S.F_next[f] = nx;
     set_next(S, pv, kF | f);
     set_prev(S, nx, kF | f);
   }
@@ -145,19 +165,18 @@ __device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
 // framework allocator needs more memory, but the device indicates an OOM
 // error"): release every free block that spans a whole segment, in all pools
 // and streams. Warp-parallel stable compaction of the free list.
-__device__ void reclaim(const State& S, uint32_t& nf, uint64_t& reserved, uint32_t& n_release,
-                        uint32_t& live_segs) {
+__device__ __forceinline__ void reclaim(const State& S, uint32_t& nf, uint64_t& reserved,
+                                     uint32_t& n_release, uint32_t& live_segs) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t newn = 0, cnt = 0;
   uint64_t freed = 0;
   for (uint32_t base = 0; base < nf; base += 32) {
     const uint32_t f = base + lane;
     const bool valid = f < nf;
-    uint32_t sz = 0, pv = kNone, nx = kNone;
+    uint32_t k = 0, sz = 0, pv = kNone, nx = kNone;
     uint64_t pos = 0;
-    uint8_t c = 0;
     if (valid) {
-      sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = S.F_pos[f]; c = S.F_cls[f];
+      k = S.F_key[f]; sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = S.F_pos[f];
     }
     const bool whole = valid && pv == kNone && nx == kNone;
     const bool keep = valid && !whole;
@@ -167,7 +186,7 @@ __device__ void reclaim(const State& S, uint32_t& nf, uint64_t& reserved, uint32
     const uint32_t dst = newn + __popc(km & ((1u << lane) - 1u));
     __syncwarp();
     if (keep && dst != f) {
-      S.F_size[dst] = sz; S.F_pos[dst] = pos; S.F_prev[dst] = pv; S.F_next[dst] = nx; S.F_cls[dst] = c;
+      S.F_key[dst] = k; S.F_size[dst] = sz; S.F_pos[dst] = pos; S.F_prev[dst] = pv; S.F_next[dst] = nx;
       set_next(S, pv, kF | dst);
       set_prev(S, nx, kF | dst);
     }
@@ -182,48 +201,64 @@ __device__ void reclaim(const State& S, uint32_t& nf, uint64_t& reserved, uint32
   live_segs -= cnt;
 }
 
-struct Peaks {
-  uint64_t tensor_pk, blk_pk, res_pk;
-  uint32_t tensor_ix, blk_ix, res_ix;
-};
+// Exact best fit: min (size, pos) over entries of class cls with size >= s.
+// Used when the packed-key search cannot decide (ties, saturated sizes).
+__device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, uint32_t cls,
+                                                uint32_t s) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t bsz = kNone, bf = kNone;
+  uint64_t bpos = ~0ull;
+  for (uint32_t f = lane; f < nf; f += 32) {
+    const uint32_t k = S.F_key[f];
+    if ((k >> kKeyBits) != cls) continue;
+    const uint32_t sz = S.F_size[f];
+    if (sz < s) continue;
+    const uint64_t pos = S.F_pos[f];
+    if (sz < bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
+  }
+  const uint32_t m = __reduce_min_sync(kFull, bsz);
+  if (m == kNone) return kNone;
+  const bool c1 = bsz == m;
+  const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone;
+  const uint32_t mh = __reduce_min_sync(kFull, hi);
+  const uint32_t lo = (c1 && hi == mh) ? uint32_t(bpos) : kNone;
+  const uint32_t ml = __reduce_min_sync(kFull, lo);
+  const int wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
+  return __shfl_sync(kFull, bf, wl);
+}
 
-// Replays events [e0, e0+n) of one trace on state S. Returns status; on
-// XM_T_OVERFLOW the caller restarts the trace on a larger arena.
-__device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32_t n,
-                            uint64_t cap_u, xm_result& R) {
+// Replays events [e0, e0+n) of one trace on state S. Returns the status; on
+// XM_T_OVERFLOW the caller restarts the trace with a larger free list.
+__device__ __forceinline__ int replay_trace(const KParams& P, const State& S, int64_t e0,
+                                            uint32_t n, uint64_t cap_u, xm_result& R) {
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
   const uint64_t unit_m1 = (1ull << u.unit_shift) - 1;
+  const long long* __restrict__ by = reinterpret_cast<const long long*>(P.bytes) + e0;
+  const uint32_t* __restrict__ tg = P.tag + e0;
 
   uint32_t nf = 0, nseg = 0, live_segs = 0, max_live = 0, n_release = 0;
   uint64_t reserved = 0, blk = 0;
   int64_t tensor = 0;
-  Peaks pk{0, 0, 0, 0, 0, 0};
+  uint64_t pk_tensor = 0, pk_blk = 0, pk_res = 0;
+  uint32_t ix_tensor = 0, ix_blk = 0, ix_res = 0;
   int status = kStatusOk;
   uint32_t done_total = 0;
 
-  // tile prefetch registers
   int64_t b_nx = 0;
   uint32_t t_nx = 0;
-  if (lane < n) {
-    b_nx = __ldcs(reinterpret_cast<const long long*>(P.bytes) + e0 + lane);
-    t_nx = __ldcs(P.tag + e0 + lane);
-  }
+  if (lane < n) { b_nx = __ldcs(by + lane); t_nx = __ldcs(tg + lane); }
   for (uint32_t base = 0; base < n; base += 32) {
     const int64_t bc = b_nx;
     const uint32_t tc = t_nx;
     const uint32_t cnt = min(32u, n - base);
-    if (base + 32 + lane < n) {
-      b_nx = __ldcs(reinterpret_cast<const long long*>(P.bytes) + e0 + base + 32 + lane);
-      t_nx = __ldcs(P.tag + e0 + base + 32 + lane);
-    }
+    if (base + 32 + lane < n) { b_nx = __ldcs(by + base + 32 + lane); t_nx = __ldcs(tg + base + 32 + lane); }
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
-    const bool valid = lane < cnt;
     const bool is_alloc = bc > 0;
     const uint64_t mag = is_alloc ? uint64_t(bc) : uint64_t(-bc);
     const uint32_t su = uint32_t((mag + unit_m1) >> u.unit_shift);
     // ---- a3: tile prefix-scan of +-s (allocated tensor bytes) ----
-    int64_t d = valid ? (is_alloc ? int64_t(su) : -int64_t(su)) : 0;
+    int64_t d = lane < cnt ? (is_alloc ? int64_t(su) : -int64_t(su)) : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t y = __shfl_up_sync(kFull, d, o);
@@ -239,34 +274,30 @@ __device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32
       const uint32_t id = w & kIdMask;
       if (w & kAllocBit) {
         // ================= ALLOC =================
-        const uint32_t small = s <= u.small_u;                  // a4: pool
-        const uint8_t cls = uint8_t(((w >> 28) << 1) | small);  // per-stream pools (Q5)
-        // a5: best fit = min (size, pos) over free blocks of this class with size >= s
-        uint32_t bsz = kNone, bf = kNone;
-        uint64_t bpos = ~0ull;
+        const uint32_t small = s <= u.small_u;                     // a4: pool
+        const uint32_t cls = ((w >> 28) << 1) | small;             // per-stream pools (Q5)
+        // a5: best fit. Candidate iff key in [cls<<27 | min(s,max), cls<<27 | max].
+        const uint32_t lo = make_key(cls, s);
+        const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
+        uint32_t best = kNone, bf = kNone;
+        bool tie = false;
+#pragma unroll 2
         for (uint32_t f = lane; f < nf; f += 32) {
-          const uint32_t sz = S.F_size[f];
-          const uint8_t c = S.F_cls[f];
-          if (c == cls && sz >= s) {
-            const uint64_t pos = S.F_pos[f];
-            if (sz < bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
+          const uint32_t k = S.F_key[f];
+          if (k - lo <= span) {
+            tie |= k == best;
+            if (k < best) { best = k; bf = f; tie = false; }
           }
         }
-        const uint32_t m = __reduce_min_sync(kFull, bsz);
+        const bool has = bf != kNone;
+        const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone);
+        const unsigned win = __ballot_sync(kFull, has && best == m);
         uint32_t fsel = kNone;
-        if (m != kNone) {
-          const unsigned tie = __ballot_sync(kFull, bsz == m);
-          int wl;
-          if ((tie & (tie - 1u)) == 0u) {
-            wl = __ffs(tie) - 1;
-          } else {
-            const uint32_t hi = bsz == m ? uint32_t(bpos >> 32) : kNone;
-            const uint32_t mh = __reduce_min_sync(kFull, hi);
-            const uint32_t lo = (bsz == m && hi == mh) ? uint32_t(bpos) : kNone;
-            const uint32_t ml = __reduce_min_sync(kFull, lo);
-            wl = __ffs(__ballot_sync(kFull, bsz == m && hi == mh && uint32_t(bpos) == ml)) - 1;
-          }
-          fsel = __shfl_sync(kFull, bf, wl);
+        if (win) {
+          const bool slow = (win & (win - 1u)) || __any_sync(kFull, has && best == m && tie) ||
+                            (m & kKeyMax) == kKeyMax;
+          if (!slow) fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
+          else fsel = best_fit_exact(S, nf, cls, s);
         }
         uint32_t bsize, bprev, bnext;
         uint64_t bposu;
@@ -276,8 +307,8 @@ __device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32
           if (small) a = u.sbuf_u;
           else if (s < u.minlarge_u) a = u.lbuf_u;
           else a = uint32_t((uint64_t(s) + u.rlarge_u - 1) / u.rlarge_u * u.rlarge_u);
-          if (reserved + a > cap_u) {                 // device level refuses (Q10)
-            reclaim(S, nf, reserved, n_release, live_segs);   // reclaim cached segments (Q3)
+          if (reserved + a > cap_u) {                          // device level refuses (Q10)
+            reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
             if (reserved + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
           bsize = a;
@@ -288,6 +319,7 @@ __device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32
           live_segs += 1;
           max_live = max(max_live, live_segs);
           reserved += a;
+          if (reserved > pk_res) { pk_res = reserved; ix_res = base + j; }
         } else {
           bsize = S.F_size[fsel];
           bprev = S.F_prev[fsel];
@@ -297,95 +329,101 @@ __device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
         const bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
+        uint32_t asize;
         if (split) {
           uint32_t r;
           if (fsel != kNone) {
-            r = fsel;                                // remainder keeps the free entry
+            r = fsel;                                  // remainder keeps the free entry
           } else {
             if (nf >= S.cap_f) { status = kStatusOverflow; break; }
             r = nf++;
-            S.F_next[r] = kNone;                     // new segment: no right neighbour
-            S.F_cls[r] = cls;
+            S.F_next[r] = kNone;                       // new segment: no right neighbour
           }
           S.F_pos[r] = bposu + s;
+          S.F_key[r] = make_key(cls, rem);
           S.F_size[r] = rem;
           S.F_prev[r] = id;
-          S.A_size[id] = s;
           S.A_next[id] = kF | r;
+          asize = s;
         } else {
-          S.A_size[id] = bsize;
           S.A_next[id] = bnext;
           set_prev(S, bnext, id);
           if (fsel != kNone) f_remove(S, fsel, nf);
+          asize = bsize;
         }
+        S.A_size[id] = asize;
         S.A_pos[id] = bposu;
         S.A_prev[id] = bprev;
-        S.A_cls[id] = cls;
+        S.A_cls[id] = uint8_t(cls);
         set_next(S, bprev, id);
-        blk += split ? s : bsize;
+        blk += asize;
+        // a9: peaks only move up on allocs, first index (Q7)
+        if (blk > pk_blk) { pk_blk = blk; ix_blk = base + j; }
       } else {
         // ================= FREE =================
         const uint32_t sz = S.A_size[id];
         const uint32_t p = S.A_prev[id];
         const uint32_t q = S.A_next[id];
-        const uint64_t pos = S.A_pos[id];
-        const uint8_t cls = S.A_cls[id];
         blk -= sz;
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
         // a8: coalesce with free neighbours; reserved unchanged (PAPER.md:259 (iv))
-        if (pf && qf) {
-          const uint32_t P_ = p & ~kF, N_ = q & ~kF;
-          const uint32_t nn = S.F_next[N_];
-          S.F_size[P_] = S.F_size[P_] + sz + S.F_size[N_];
+        if (pf) {
+          const uint32_t P_ = p & ~kF;
+          uint32_t nsz = S.F_size[P_] + sz;
+          uint32_t nn = q;
+          if (qf) {
+            const uint32_t N_ = q & ~kF;
+            nsz += S.F_size[N_];
+            nn = S.F_next[N_];
+          }
+          S.F_size[P_] = nsz;
+          S.F_key[P_] = make_key(S.A_cls[id], nsz);
           S.F_next[P_] = nn;
           set_prev(S, nn, p);
-          f_remove(S, N_, nf);
-        } else if (pf) {
-          const uint32_t P_ = p & ~kF;
-          S.F_size[P_] = S.F_size[P_] + sz;
-          S.F_next[P_] = q;
-          set_prev(S, q, p);
+          if (qf) f_remove(S, q & ~kF, nf);
         } else if (qf) {
           const uint32_t N_ = q & ~kF;
-          S.F_pos[N_] = pos;
-          S.F_size[N_] = S.F_size[N_] + sz;
+          const uint32_t nsz = S.F_size[N_] + sz;
+          S.F_pos[N_] = S.A_pos[id];
+          S.F_size[N_] = nsz;
+          S.F_key[N_] = make_key(S.A_cls[id], nsz);
           S.F_prev[N_] = p;
           set_next(S, p, q);
         } else {
           if (nf >= S.cap_f) { status = kStatusOverflow; break; }
           const uint32_t r = nf++;
-          S.F_pos[r] = pos; S.F_size[r] = sz; S.F_prev[r] = p; S.F_next[r] = q; S.F_cls[r] = cls;
+          S.F_pos[r] = S.A_pos[id];
+          S.F_size[r] = sz;
+          S.F_key[r] = make_key(S.A_cls[id], sz);
+          S.F_prev[r] = p;
+          S.F_next[r] = q;
           set_next(S, p, kF | r);
           set_prev(S, q, kF | r);
         }
       }
-      // a9: time series peaks, first index (Q7)
-      const uint32_t ev = base + j;
-      if (blk > pk.blk_pk) { pk.blk_pk = blk; pk.blk_ix = ev; }
-      if (reserved > pk.res_pk) { pk.res_pk = reserved; pk.res_ix = ev; }
-      __syncwarp();
     }
     // a3: allocated-tensor peak over the processed prefix of this tile
     const int64_t v = lane < j ? cur : INT64_MIN;
     const int64_t mx = warp_max_i64(v);
-    if (j > 0 && mx > int64_t(pk.tensor_pk)) {
+    if (j > 0 && mx > int64_t(pk_tensor)) {
       const unsigned bm = __ballot_sync(kFull, v == mx);
-      pk.tensor_pk = uint64_t(mx);
-      pk.tensor_ix = base + __ffs(bm) - 1;
+      pk_tensor = uint64_t(mx);
+      ix_tensor = base + __ffs(bm) - 1;
     }
     tensor = __shfl_sync(kFull, cur, 31);
     done_total = base + j;
+    __syncwarp();
     if (status != kStatusOk) break;
   }
   const uint32_t sh = u.unit_shift;
-  R.peak_allocated = pk.tensor_pk << sh;
-  R.peak_allocated_blk = pk.blk_pk << sh;
-  R.peak_reserved = pk.res_pk << sh;
+  R.peak_allocated = pk_tensor << sh;
+  R.peak_allocated_blk = pk_blk << sh;
+  R.peak_reserved = pk_res << sh;
   R.final_reserved = reserved << sh;
-  R.peak_allocated_idx = pk.tensor_ix;
-  R.peak_allocated_blk_idx = pk.blk_ix;
-  R.peak_reserved_idx = pk.res_ix;
+  R.peak_allocated_idx = ix_tensor;
+  R.peak_allocated_blk_idx = ix_blk;
+  R.peak_reserved_idx = ix_res;
   R.n_seg_alloc = nseg;
   R.n_seg_release = n_release;
   R.max_live_segments = max_live;
@@ -395,13 +433,74 @@ __device__ int replay_trace(const KParams& P, const State& S, int64_t e0, uint32
   return status;
 }
 
-__global__ void __launch_bounds__(256) k_replay(KParams P) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// ---- shared-memory heap (one per CTA) --------------------------------------
+__device__ __forceinline__ bool page_used(const HeapHdr* h, uint32_t p) {
+  const volatile uint32_t* bm = h->bitmap;
+  return (bm[p >> 5] >> (p & 31)) & 1u;
+}
+
+// lane 0 only. FIFO (ticket) first-fit allocation of `np` contiguous pages.
+__device__ uint32_t heap_alloc(HeapHdr* h, uint32_t total, uint32_t np) {
+  const int t = atomicAdd(&h->ticket, 1);
+  while (*(volatile int*)&h->serving != t) __nanosleep(128);
+  uint32_t start;
+  for (;;) {
+    start = kNone;
+    uint32_t p = 0;
+    while (p + np <= total) {
+      if (page_used(h, p)) { ++p; continue; }
+      uint32_t q = p + 1;
+      while (q < p + np && !page_used(h, q)) ++q;
+      if (q == p + np) { start = p; break; }
+      p = q + 1;
+    }
+    if (start != kNone) break;
+    __nanosleep(512);
+  }
+  for (uint32_t p = start; p < start + np;) {
+    const uint32_t w = p >> 5, b0 = p & 31;
+    const uint32_t nb = min(32u - b0, start + np - p);
+    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
+    atomicOr(&h->bitmap[w], mask);
+    p += nb;
+  }
+  __threadfence_block();
+  atomicAdd(&h->serving, 1);
+  return start;
+}
+
+__device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np) {
+  for (uint32_t p = start; p < start + np;) {
+    const uint32_t w = p >> 5, b0 = p & 31;
+    const uint32_t nb = min(32u - b0, start + np - p);
+    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
+    atomicAnd(&h->bitmap[w], ~mask);
+    p += nb;
+  }
+}
+
+// lane 0 only: claim a global arena slot (spins while all are busy)
+__device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
+  for (;;) {
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t m = 1u << (i & 31);
+      if (!(atomicOr(&bits[i >> 5], m) & m)) return i;
+    }
+    __nanosleep(1024);
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  HeapHdr* hdr = reinterpret_cast<HeapHdr*>(smem);
+  unsigned char* pages = smem + kHdrBytes;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
-  unsigned char* my_smem = smem + size_t(warp) * P.smem_per_warp;
-  unsigned char* my_arena = P.arena + size_t(gwarp) * P.arena_per_warp;
+  if (threadIdx.x == 0) {
+    hdr->ticket = 0;
+    hdr->serving = 0;
+    for (uint32_t i = 0; i < kBitmapWords; ++i) hdr->bitmap[i] = 0;
+  }
+  __syncthreads();
   for (;;) {
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(P.counter, 1u);
@@ -414,15 +513,34 @@ __global__ void __launch_bounds__(256) k_replay(KParams P) {
     const uint64_t cap = P.capacity ? P.capacity[t] : P.cap_default;
     const uint64_t cap_u = cap >> P.u.unit_shift;
     xm_result R;
+    const uint32_t nf_exact = n + 1;              // nf <= events
+    uint32_t nfc = min(nf_exact, na / 4 + 96);
     int st = kStatusOverflow;
-    const uint32_t fc = free_cap(P.smem_per_warp, na);
-    if (fc >= 32) {
-      const State S = carve(my_smem, na, fc);
+    for (;;) {
+      const uint32_t np = uint32_t((state_bytes(na, nfc) + kPage - 1) / kPage);
+      if (np > P.heap_pages) break;
+      uint32_t start = 0;
+      if (lane == 0) start = heap_alloc(hdr, P.heap_pages, np);
+      start = __shfl_sync(kFull, start, 0);
+      const State S = carve(pages + size_t(start) * kPage, na, nfc);
       st = replay_trace(P, S, e0, n, cap_u, R);
+      __syncwarp();
+      if (lane == 0) heap_free(hdr, start, np);
+      if (st != kStatusOverflow || nfc >= nf_exact) break;
+      nfc = min(nf_exact, nfc * 4);
     }
-    if (st == kStatusOverflow && na <= P.arena_ids) {
-      const State S = carve(my_arena, na, P.arena_free);
+    if (st == kStatusOverflow) {
+      // global arena, exact bound: cannot overflow
+      uint32_t slot = 0;
+      if (lane == 0) slot = arena_claim(P.counter + 1, P.n_arena);
+      slot = __shfl_sync(kFull, slot, 0);
+      const State S = carve(P.arena + size_t(slot) * P.arena_bytes, na, nf_exact);
       st = replay_trace(P, S, e0, n, cap_u, R);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
+      }
     }
     if (lane == 0) P.out[t] = R;
     __syncwarp();
@@ -439,34 +557,30 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   if (cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 4;
-  if (p.warps_per_cta > 8) p.warps_per_cta = 8;
-  uint32_t spw = cfg->smem_per_warp;
-  if (spw == 0) {
-    // enough for the largest id space plus a free list of 512 entries, capped so
-    // that 4 warps fit in one SM's 227 KB
-    size_t want = state_bytes(b->max_ids, 512);
-    size_t capb = (227u * 1024u) / size_t(p.warps_per_cta);
-    spw = uint32_t(want < capb ? want : capb);
-    if (spw < 4096) spw = 4096;
-  }
-  spw = (spw + 15u) & ~15u;
-  p.smem_per_warp = spw;
-  const size_t smem_cta = size_t(spw) * p.warps_per_cta;
-  int per_sm = smem_cta ? int((227u * 1024u) / smem_cta) : 8;
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm * p.warps_per_cta > 64) per_sm = 64 / p.warps_per_cta;
-  p.ctas = sms * per_sm;
+  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 16;
+  if (p.warps_per_cta > 16) p.warps_per_cta = 16;
+  if (p.warps_per_cta < 1) p.warps_per_cta = 1;
+  // heap: the whole per-CTA maximum unless capped (smem_per_warp x warps)
+  size_t heap = size_t(kMaxPages) * kPage;
+  if (cfg->smem_per_warp) heap = std::min(heap, size_t(cfg->smem_per_warp) * p.warps_per_cta);
+  if (heap < kPage) heap = kPage;
+  p.heap_pages = uint32_t(heap / kPage);
+  p.ctas = sms;
   const int64_t warps_total = int64_t(p.ctas) * p.warps_per_cta;
   if (b->n_traces < warps_total) {
     p.ctas = int((b->n_traces + p.warps_per_cta - 1) / p.warps_per_cta);
     if (p.ctas < 1) p.ctas = 1;
   }
-  // global arena: exact bound (nf <= n_events, SPEC invariants; K2)
+  // global arenas (exact bound): a pool of slots, claimed only by traces whose
+  // state cannot live in shared memory
   p.arena_ids = b->max_ids;
   p.arena_free = b->max_events + 1;
   p.arena_per_warp = (state_bytes(p.arena_ids, p.arena_free) + 255) & ~size_t(255);
-  p.scratch_bytes = 256 + size_t(p.ctas) * p.warps_per_cta * p.arena_per_warp;
+  const int64_t tw = int64_t(p.ctas) * p.warps_per_cta;
+  const uint32_t n_arena = uint32_t(std::min<int64_t>(std::min<int64_t>(tw, 64),
+                                                      std::max<int64_t>(1, b->n_traces)));
+  p.n_arena = n_arena;
+  p.scratch_bytes = 256 + size_t(n_arena) * p.arena_per_warp;
   return p;
 }
 
@@ -484,16 +598,17 @@ int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
   P.cap_default = cfg->capacity;
   P.n_traces = b->n_traces;
   P.u = u;
-  P.smem_per_warp = plan.smem_per_warp;
+  P.heap_pages = plan.heap_pages;
   P.counter = static_cast<uint32_t*>(d_scratch);
   P.arena = static_cast<unsigned char*>(d_scratch) + 256;
-  P.arena_per_warp = plan.arena_per_warp;
+  P.arena_bytes = plan.arena_per_warp;
+  P.n_arena = plan.n_arena;
   P.arena_ids = plan.arena_ids;
   P.arena_free = plan.arena_free;
   P.out = d_out;
   cudaError_t e = cudaMemsetAsync(d_scratch, 0, 256, st);
   if (e != cudaSuccess) return int(e);
-  const size_t smem = size_t(plan.smem_per_warp) * plan.warps_per_cta;
+  const size_t smem = kHdrBytes + size_t(plan.heap_pages) * kPage;
   e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return int(e);
   k_replay<<<plan.ctas, plan.warps_per_cta * 32, smem, st>>>(P);

@@ -39,8 +39,9 @@ struct UnitConfig {
 struct ReplayPlan {
   int warps_per_cta;
   int ctas;
-  uint32_t smem_per_warp;   // bytes of shared-memory state per warp
-  size_t arena_per_warp;    // bytes of global-memory state per warp (overflow path)
+  uint32_t heap_pages;      // shared-memory heap pages (512 B) per CTA
+  size_t arena_per_warp;    // bytes per global-memory arena slot (overflow path)
+  uint32_t n_arena;         // arena slots in scratch
   uint32_t arena_ids, arena_free;
   size_t scratch_bytes;     // header + arenas
 };

@@ -58,10 +58,11 @@ def test_spec_split_variant():
 
 
 def test_fragmentation_stress_spills_to_global_arena():
-    # 2048 free holes do not fit a 16 KB shared-memory slot: exercises the
-    # overflow -> global arena restart
+    # 2048 free holes outgrow the initial free-list guess (restart in a 4x
+    # region); with a 16 KB heap the state cannot live in shared memory at all
+    # (global arena path)
     b = concat([fuzz.fragmentation_stress(), fuzz.fragmentation_stress(8192, 1024, "frag2")])
-    _check(b, xm.Config(smem_per_warp=16384))
+    _check(b, xm.Config(smem_per_warp=16384, warps_per_cta=1))
     _check(b)
 
 
