@@ -38,6 +38,20 @@
 
 #include "xm_internal.h"
 
+#ifdef XM_DEBUG
+#include <cstdio>
+#define XM_CHECK(cond, ...)                                   \
+  do {                                                        \
+    if (!(cond)) {                                            \
+      printf("XM_CHECK %s:%d: ", __FILE__, __LINE__);         \
+      printf(__VA_ARGS__);                                    \
+      __trap();                                               \
+    }                                                         \
+  } while (0)
+#else
+#define XM_CHECK(cond, ...) do {} while (0)
+#endif
+
 namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -123,18 +137,21 @@ __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
 
 __device__ __forceinline__ void set_next(const State& S, uint32_t ref, uint32_t v) {
   if (ref == kNone) return;
+  XM_CHECK(!(ref & kF) || (ref & ~kF) < S.cap_f, "set_next ref=%x cap=%u\n", ref, S.cap_f);
   if (ref & kF) S.F_next[ref & ~kF] = v;
   else S.A_next[ref] = v;
 }
 
 __device__ __forceinline__ void set_prev(const State& S, uint32_t ref, uint32_t v) {
   if (ref == kNone) return;
+  XM_CHECK(!(ref & kF) || (ref & ~kF) < S.cap_f, "set_prev ref=%x cap=%u\n", ref, S.cap_f);
   if (ref & kF) S.F_prev[ref & ~kF] = v;
   else S.A_prev[ref] = v;
 }
 
 // Remove free entry f by moving the last entry into its slot (warp-uniform).
 __device__ __forceinline__ void f_remove(const State& S, uint32_t f, uint32_t& nf) {
+  XM_CHECK(nf >= 1 && f < nf, "f_remove f=%u nf=%u\n", f, nf);
   const uint32_t L = nf - 1;
   if (f != L) {
     const uint32_t k = S.F_key[L], sz = S.F_size[L], pv = S.F_prev[L], nx = S.F_next[L];
@@ -216,6 +233,7 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, 
     const uint64_t pos = S.F_pos[f];
     if (sz < bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
   }
+  __syncwarp();
   const uint32_t m = __reduce_min_sync(kFull, bsz);
   if (m == kNone) return kNone;
   const bool c1 = bsz == m;
@@ -229,6 +247,14 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, 
 
 // Replays events [e0, e0+n) of one trace on state S. Returns the status; on
 // XM_T_OVERFLOW the caller restarts the trace with a larger free list.
+//
+// Warp-uniform execution: every lane runs the same bookkeeping on the same
+// values (loads of the same address are broadcasts; stores of the same value
+// to the same address are benign), so no broadcasts are needed. This is only
+// correct while the warp is CONVERGED: a split lane group would re-read state
+// another group already updated. The only lane-dependent branches are the
+// best-fit scan loop (reconverges before the reduction) and lane-0 regions in
+// the caller, each closed by __syncwarp(); every event also ends with one.
 __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, int64_t e0,
                                             uint32_t n, uint64_t cap_u, xm_result& R) {
   const uint32_t lane = threadIdx.x & 31;
@@ -253,6 +279,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
     const uint32_t tc = t_nx;
     const uint32_t cnt = min(32u, n - base);
     if (base + 32 + lane < n) { b_nx = __ldcs(by + base + 32 + lane); t_nx = __ldcs(tg + base + 32 + lane); }
+    __syncwarp();                                       // reconverge after the lane-dependent branch
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;
     const uint64_t mag = is_alloc ? uint64_t(bc) : uint64_t(-bc);
@@ -276,28 +303,50 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
         // ================= ALLOC =================
         const uint32_t small = s <= u.small_u;                     // a4: pool
         const uint32_t cls = ((w >> 28) << 1) | small;             // per-stream pools (Q5)
-        // a5: best fit. Candidate iff key in [cls<<27 | min(s,max), cls<<27 | max].
+        // a5: best fit = min (size, pos) over free blocks of class cls with
+        // size >= s. Candidate iff key in [cls<<27 | min(s,max), cls<<27 | max];
+        // equal keys are ordered by pos, loaded only on a tie.
         const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
         uint32_t best = kNone, bf = kNone;
-        bool tie = false;
-#pragma unroll 2
+        uint64_t bpos = ~0ull;          // valid iff bpos_ok
+        bool bpos_ok = false;
         for (uint32_t f = lane; f < nf; f += 32) {
           const uint32_t k = S.F_key[f];
           if (k - lo <= span) {
-            tie |= k == best;
-            if (k < best) { best = k; bf = f; tie = false; }
+            if (k < best) {
+              best = k; bf = f; bpos_ok = false;
+            } else if (k == best) {
+              if (!bpos_ok) { bpos = S.F_pos[bf]; bpos_ok = true; }
+              const uint64_t pos = S.F_pos[f];
+              if (pos < bpos) { bf = f; bpos = pos; }
+            }
           }
         }
+        __syncwarp();                                   // reconverge after the scan
         const bool has = bf != kNone;
         const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone);
-        const unsigned win = __ballot_sync(kFull, has && best == m);
         uint32_t fsel = kNone;
-        if (win) {
-          const bool slow = (win & (win - 1u)) || __any_sync(kFull, has && best == m && tie) ||
-                            (m & kKeyMax) == kKeyMax;
-          if (!slow) fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
-          else fsel = best_fit_exact(S, nf, cls, s);
+        if (m != kNone || __any_sync(kFull, has)) {
+          if ((m & kKeyMax) == kKeyMax) {
+            fsel = best_fit_exact(S, nf, cls, s);          // saturated sizes: exact compare
+          } else {
+            const bool c1 = has && best == m;
+            const unsigned win = __ballot_sync(kFull, c1);
+            int wl;
+            if ((win & (win - 1u)) == 0u) {
+              wl = __ffs(win) - 1;
+            } else {                                       // size tie across lanes: min pos
+              if (c1 && !bpos_ok) bpos = S.F_pos[bf];
+              __syncwarp();
+              const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone;
+              const uint32_t mh = __reduce_min_sync(kFull, hi);
+              const uint32_t lo2 = (c1 && hi == mh) ? uint32_t(bpos) : kNone;
+              const uint32_t ml = __reduce_min_sync(kFull, lo2);
+              wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
+            }
+            fsel = __shfl_sync(kFull, bf, wl);
+          }
         }
         uint32_t bsize, bprev, bnext;
         uint64_t bposu;
@@ -357,14 +406,13 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
         S.A_cls[id] = uint8_t(cls);
         set_next(S, bprev, id);
         blk += asize;
-        // a9: peaks only move up on allocs, first index (Q7)
+        // a9: the block peak only moves up on allocs, first index (Q7)
         if (blk > pk_blk) { pk_blk = blk; ix_blk = base + j; }
       } else {
         // ================= FREE =================
         const uint32_t sz = S.A_size[id];
         const uint32_t p = S.A_prev[id];
         const uint32_t q = S.A_next[id];
-        blk -= sz;
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
         // a8: coalesce with free neighbours; reserved unchanged (PAPER.md:259 (iv))
@@ -401,8 +449,11 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
           set_next(S, p, kF | r);
           set_prev(S, q, kF | r);
         }
+        blk -= sz;
       }
+      __syncwarp();
     }
+    __syncwarp();
     // a3: allocated-tensor peak over the processed prefix of this tile
     const int64_t v = lane < j ? cur : INT64_MIN;
     const int64_t mx = warp_max_i64(v);
@@ -413,7 +464,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
     }
     tensor = __shfl_sync(kFull, cur, 31);
     done_total = base + j;
-    __syncwarp();
+    XM_CHECK(nf <= S.cap_f, "nf=%u cap=%u base=%u\n", nf, S.cap_f, base);
     if (status != kStatusOk) break;
   }
   const uint32_t sh = u.unit_shift;
@@ -434,58 +485,99 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
 }
 
 // ---- shared-memory heap (one per CTA) --------------------------------------
-__device__ __forceinline__ bool page_used(const HeapHdr* h, uint32_t p) {
-  const volatile uint32_t* bm = h->bitmap;
-  return (bm[p >> 5] >> (p & 31)) & 1u;
+// All heap and arena routines are called by the WHOLE warp with warp-uniform
+// control flow: single-lane work is predicated and its result broadcast, and
+// every wait loop tests a broadcast (uniform) condition. A lane-0-only branch
+// around a spinning call would leave the warp split into lane groups for the
+// rest of the trace, which breaks the warp-uniform replay (see replay_trace).
+__device__ __forceinline__ uint32_t bitmap_word(const HeapHdr* h, uint32_t w) {
+  return reinterpret_cast<const volatile uint32_t*>(h->bitmap)[w];
 }
 
-// lane 0 only. FIFO (ticket) first-fit allocation of `np` contiguous pages.
-__device__ uint32_t heap_alloc(HeapHdr* h, uint32_t total, uint32_t np) {
-  const int t = atomicAdd(&h->ticket, 1);
-  while (*(volatile int*)&h->serving != t) __nanosleep(128);
+// Is [p, p+np) free? (reads the bitmap word by word)
+__device__ __forceinline__ bool run_free(const HeapHdr* h, uint32_t p, uint32_t np) {
+  const uint32_t e = p + np;
+  for (uint32_t q = p; q < e;) {
+    const uint32_t w = q >> 5, b0 = q & 31;
+    const uint32_t nb = min(32u - b0, e - q);
+    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
+    if (bitmap_word(h, w) & mask) return false;
+    q += nb;
+  }
+  return true;
+}
+
+// stats: [0] restarts, [1] arena runs, [2] heap wait rounds, [3] ticket wait rounds
+__device__ uint32_t heap_alloc(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats) {
+  const uint32_t lane = threadIdx.x & 31;
+  int t = 0;
+  if (lane == 0) t = atomicAdd(&h->ticket, 1);
+  t = __shfl_sync(kFull, t, 0);
+  uint32_t tw = 0, hw = 0;
+  for (;;) {                                                   // FIFO: wait for our ticket
+    const int srv = __shfl_sync(kFull, *(volatile int*)&h->serving, 0);
+    if (srv == t) break;
+    __nanosleep(128);
+    ++tw;
+  }
   uint32_t start;
-  for (;;) {
-    start = kNone;
-    uint32_t p = 0;
-    while (p + np <= total) {
-      if (page_used(h, p)) { ++p; continue; }
-      uint32_t q = p + 1;
-      while (q < p + np && !page_used(h, q)) ++q;
-      if (q == p + np) { start = p; break; }
-      p = q + 1;
-    }
+  for (;;) {                                                   // first fit, lane-parallel
+    uint32_t cand = kNone;
+    for (uint32_t p = lane; p + np <= total; p += 32)
+      if (run_free(h, p, np)) { cand = p; break; }
+    __syncwarp();
+    start = __reduce_min_sync(kFull, cand);
     if (start != kNone) break;
     __nanosleep(512);
+    ++hw;
   }
-  for (uint32_t p = start; p < start + np;) {
-    const uint32_t w = p >> 5, b0 = p & 31;
-    const uint32_t nb = min(32u - b0, start + np - p);
-    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
-    atomicOr(&h->bitmap[w], mask);
-    p += nb;
+  // claim: lane k sets word (start>>5)+k of the range
+  const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
+  for (uint32_t w = w0 + lane; w <= w1; w += 32) {
+    const uint32_t lo = max(start, w << 5), hi = min(start + np, (w + 1) << 5);
+    const uint32_t nb = hi - lo;
+    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo & 31);
+    const uint32_t old = atomicOr(&h->bitmap[w], mask);
+    XM_CHECK((old & mask) == 0, "heap overlap start=%u np=%u\n", start, np);
+    (void)old;
   }
+  __syncwarp();
   __threadfence_block();
-  atomicAdd(&h->serving, 1);
+  if (lane == 0) {
+    atomicAdd(&h->serving, 1);
+    if (tw) atomicAdd(stats + 3, tw);
+    if (hw) atomicAdd(stats + 2, hw);
+  }
+  __syncwarp();
   return start;
 }
 
 __device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np) {
-  for (uint32_t p = start; p < start + np;) {
-    const uint32_t w = p >> 5, b0 = p & 31;
-    const uint32_t nb = min(32u - b0, start + np - p);
-    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
+  __syncwarp();
+  for (uint32_t w = w0 + lane; w <= w1; w += 32) {
+    const uint32_t lo = max(start, w << 5), hi = min(start + np, (w + 1) << 5);
+    const uint32_t nb = hi - lo;
+    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo & 31);
     atomicAnd(&h->bitmap[w], ~mask);
-    p += nb;
   }
+  __syncwarp();
 }
 
-// lane 0 only: claim a global arena slot (spins while all are busy)
+// Claim a global arena slot (whole warp; spins while all are busy).
 __device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
   for (;;) {
-    for (uint32_t i = 0; i < n; ++i) {
-      const uint32_t m = 1u << (i & 31);
-      if (!(atomicOr(&bits[i >> 5], m) & m)) return i;
+    uint32_t got = kNone;
+    if (lane == 0) {
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t m = 1u << (i & 31);
+        if (!(atomicOr(&bits[i >> 5], m) & m)) { got = i; break; }
+      }
     }
+    got = __shfl_sync(kFull, got, 0);
+    if (got != kNone) return got;
     __nanosleep(1024);
   }
 }
@@ -519,28 +611,23 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     for (;;) {
       const uint32_t np = uint32_t((state_bytes(na, nfc) + kPage - 1) / kPage);
       if (np > P.heap_pages) break;
-      uint32_t start = 0;
-      if (lane == 0) start = heap_alloc(hdr, P.heap_pages, np);
-      start = __shfl_sync(kFull, start, 0);
+      const uint32_t start = heap_alloc(hdr, P.heap_pages, np, P.counter + 32);
       const State S = carve(pages + size_t(start) * kPage, na, nfc);
       st = replay_trace(P, S, e0, n, cap_u, R);
-      __syncwarp();
-      if (lane == 0) heap_free(hdr, start, np);
+      heap_free(hdr, start, np);
       if (st != kStatusOverflow || nfc >= nf_exact) break;
+      if (lane == 0) atomicAdd(P.counter + 32, 1u);
       nfc = min(nf_exact, nfc * 4);
     }
     if (st == kStatusOverflow) {
       // global arena, exact bound: cannot overflow
-      uint32_t slot = 0;
-      if (lane == 0) slot = arena_claim(P.counter + 1, P.n_arena);
-      slot = __shfl_sync(kFull, slot, 0);
+      const uint32_t slot = arena_claim(P.counter + 1, P.n_arena);
+      if (lane == 0) atomicAdd(P.counter + 33, 1u);
       const State S = carve(P.arena + size_t(slot) * P.arena_bytes, na, nf_exact);
       st = replay_trace(P, S, e0, n, cap_u, R);
       __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
-      }
+      __threadfence();
+      if (lane == 0) atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
     }
     if (lane == 0) P.out[t] = R;
     __syncwarp();
