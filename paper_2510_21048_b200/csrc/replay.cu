@@ -7,26 +7,26 @@
 // §2 (Q1-Q18); per-step citations inline.
 //
 // Execution model (DESIGN.md §6 K2):
-//  * persistent grid, one CTA per SM, 16 warps per CTA, one trace per warp;
-//    traces are pulled longest-first (host LPT order) from one atomic counter;
-//  * each CTA owns a shared-memory HEAP (all of the SM's 227 KB, 512 B pages).
-//    A warp sizes a region for its trace's state (id space + a free-list
-//    guess), takes it FIFO (ticket lock) from the heap, replays, frees it. So
-//    occupancy adapts: few warps hold the big early traces, many hold the
-//    small later ones. A free list that outgrows its guess restarts the trace
-//    in a 4x larger region; a trace larger than the heap runs in a
-//    global-memory arena sized to the exact bound (never overflows);
+//  * persistent grid, one CTA per SM, up to 16 warps per CTA, one trace per
+//    warp; traces are pulled longest-first (host LPT order) from one counter;
+//  * each CTA owns a shared-memory HEAP (the SM's 227 KB in 512 B pages). A
+//    warp takes (FIFO) one region for its trace: the id-indexed records (A,
+//    fixed size) followed by a small free list (F). When the free list fills,
+//    it moves to a region twice as large, if one can be claimed without
+//    waiting (entries keep their indices); otherwise the trace restarts in a
+//    global-memory arena sized to the exact bound. Occupancy thus adapts to
+//    the traces actually running;
 //  * events stream through registers in 32-event tiles (coalesced streaming
 //    loads, next tile prefetched); round-up and the allocated-bytes prefix
 //    scan of a tile are lane-parallel (a2, a3);
 //  * the serial state machine is warp-uniform (every lane computes the same
 //    scalars, so no broadcasts); the best-fit search scans the free list
 //    lane-strided with ONE packed 32-bit key per entry (class in the top 5
-//    bits, saturated size below) and __reduce_min_sync; exact (size, pos)
-//    tie-breaking falls back to a full compare only when needed (a5).
+//    bits, saturated size below) and __reduce_min_sync; ties in size are
+//    broken by pos, loaded only when needed (a5).
 //
 // State (structure of arrays):
-//  A[id]  allocated block of dense id: pos u64, size u32, prev u32, next u32, cls u8
+//  A[id]  allocated block of dense id: pos u64 (cls in bits 59-63), size u32, prev u32, next u32
 //  F[f]   free block f (unordered, nf entries): pos u64, key u32, size u32, prev u32, next u32
 //  pos  = segment_index << 32 | offset_in_units  (bump addresses never reused:
 //         (size, pos) order == SPEC D2's (size, segment, offset), reading Q4)
@@ -101,7 +101,6 @@ struct State {
   uint32_t* A_size;
   uint32_t* A_prev;
   uint32_t* A_next;
-  uint8_t* A_cls;
   uint64_t* F_pos;
   uint32_t* F_key;
   uint32_t* F_size;
@@ -110,25 +109,30 @@ struct State {
   uint32_t cap_f;
 };
 
+constexpr uint32_t kPosBits = 59;                 // A_pos: cls in bits 59-63
+constexpr uint64_t kPosMask = (1ull << kPosBits) - 1;
+constexpr uint32_t kMaxSegs = 1u << 27;           // segment index must fit bits 32-58
+
+__host__ __device__ inline size_t a_bytes(uint32_t na) { return size_t(na) * 20; }
+__host__ __device__ inline size_t f_bytes(uint32_t nf) { return size_t(nf) * 24; }
 __host__ __device__ inline size_t state_bytes(uint32_t na, uint32_t nf) {
-  return size_t(na) * 21 + size_t(nf) * 24 + 16;
+  return a_bytes(na) + f_bytes(nf) + 16;
 }
 
-__device__ inline State carve(unsigned char* base, uint32_t na, uint32_t nf) {
-  State S;
-  unsigned char* p = base;
+__device__ __forceinline__ void carve_a(State& S, unsigned char* p, uint32_t na) {
   S.A_pos = reinterpret_cast<uint64_t*>(p); p += size_t(na) * 8;
-  S.F_pos = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
   S.A_size = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
   S.A_prev = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
-  S.A_next = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
+  S.A_next = reinterpret_cast<uint32_t*>(p);
+}
+
+__device__ __forceinline__ void carve_f(State& S, unsigned char* p, uint32_t nf) {
+  S.F_pos = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
   S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_prev = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.F_next = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.A_cls = p;
+  S.F_next = reinterpret_cast<uint32_t*>(p);
   S.cap_f = nf;
-  return S;
 }
 
 __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
@@ -149,20 +153,6 @@ __device__ __forceinline__ void set_prev(const State& S, uint32_t ref, uint32_t 
   else S.A_prev[ref] = v;
 }
 
-// Remove free entry f by moving the last entry into its slot (warp-uniform).
-__device__ __forceinline__ void f_remove(const State& S, uint32_t f, uint32_t& nf) {
-  XM_CHECK(nf >= 1 && f < nf, "f_remove f=%u nf=%u\n", f, nf);
-  const uint32_t L = nf - 1;
-  if (f != L) {
-    const uint32_t k = S.F_key[L], sz = S.F_size[L], pv = S.F_prev[L], nx = S.F_next[L];
-    const uint64_t pos = S.F_pos[L];
-    S.F_key[f] = k; S.F_size[f] = sz; S.F_pos[f] = pos; S.F_prev[f] = pv; S.F_next[f] = nx;
-    set_next(S, pv, kF | f);
-    set_prev(S, nx, kF | f);
-  }
-  nf = L;
-}
-
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -176,6 +166,194 @@ __device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
     v = w > v ? w : v;
   }
   return v;
+}
+
+// ---- shared-memory heap (one per CTA) --------------------------------------
+// All heap and arena routines are called by the WHOLE warp with warp-uniform
+// control flow: single-lane work is predicated and its result broadcast, and
+// every wait loop tests a broadcast (uniform) condition. (A lane-0-only branch
+// around a spinning call can leave the warp split into lane groups, which
+// breaks the warp-uniform replay below.) Pages are claimed with atomicOr on
+// the bitmap and rolled back on conflict, so a FIFO allocation and a
+// non-blocking free-list growth can race safely.
+__device__ __forceinline__ uint32_t bitmap_word(const HeapHdr* h, uint32_t w) {
+  return reinterpret_cast<const volatile uint32_t*>(h->bitmap)[w];
+}
+
+__device__ __forceinline__ uint32_t range_mask(uint32_t w, uint32_t start, uint32_t np) {
+  const uint32_t lo = max(start, w << 5), hi = min(start + np, (w + 1) << 5);
+  const uint32_t nb = hi - lo;
+  return (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo & 31);
+}
+
+// Is [p, p+np) free? (reads the bitmap word by word)
+__device__ __forceinline__ bool run_free(const HeapHdr* h, uint32_t p, uint32_t np) {
+  for (uint32_t w = p >> 5; w <= (p + np - 1) >> 5; ++w)
+    if (bitmap_word(h, w) & range_mask(w, p, np)) return false;
+  return true;
+}
+
+// lowest start of np free pages (lane-parallel), or kNone
+__device__ __forceinline__ uint32_t first_fit(const HeapHdr* h, uint32_t total, uint32_t np) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t cand = kNone;
+  for (uint32_t p = lane; p + np <= total; p += 32)
+    if (run_free(h, p, np)) { cand = p; break; }
+  __syncwarp();
+  return __reduce_min_sync(kFull, cand);
+}
+
+// claim [start, start+np) atomically; on conflict undo our bits and fail
+__device__ __forceinline__ bool try_claim(HeapHdr* h, uint32_t start, uint32_t np) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
+  uint32_t w = w0 + lane, mine = 0;
+  bool clash = false;
+  if (w <= w1) {
+    const uint32_t m = range_mask(w, start, np);
+    const uint32_t old = atomicOr(&h->bitmap[w], m);
+    mine = m & ~old;
+    clash = (old & m) != 0;
+  }
+  const bool any_clash = __any_sync(kFull, clash);
+  if (any_clash && mine) atomicAnd(&h->bitmap[w], ~mine);
+  __syncwarp();
+  return !any_clash;
+}
+
+// stats: [0] spills to the global arena, [1] arena runs, [2] heap wait rounds,
+//        [3] ticket wait rounds, [4] free-list growths
+//
+// Admission is FIFO per CTA: a warp takes a ticket, waits for its turn, and only
+// then pulls its next trace from the global longest-first order and waits for
+// room; so every CTA starts its traces in LPT order and holds at most one
+// pulled-but-not-started trace. Waits back off exponentially so that idle
+// warps do not steal issue slots from the replaying ones.
+__device__ void ticket_acquire(HeapHdr* h, uint32_t* stats) {
+  const uint32_t lane = threadIdx.x & 31;
+  int t = 0;
+  if (lane == 0) t = atomicAdd(&h->ticket, 1);
+  t = __shfl_sync(kFull, t, 0);
+  uint32_t tw = 0, nap = 256;
+  for (;;) {
+    const int srv = __shfl_sync(kFull, *(volatile int*)&h->serving, 0);
+    if (srv == t) break;
+    __nanosleep(nap);
+    nap = min(nap * 2, 16384u);
+    ++tw;
+  }
+  if (lane == 0 && tw) atomicAdd(stats + 3, tw);
+  __syncwarp();
+}
+
+__device__ void ticket_release(HeapHdr* h) {
+  const uint32_t lane = threadIdx.x & 31;
+  __syncwarp();
+  __threadfence_block();
+  if (lane == 0) atomicAdd(&h->serving, 1);
+  __syncwarp();
+}
+
+// Wait (holding the ticket) until np pages can be claimed. Admission keeps a
+// reserve of free pages for the free-list growth of the traces already running
+// (unless the heap would otherwise sit idle).
+__device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t reserve = total / 8;
+  uint32_t start, hw = 0, nap = 256;
+  for (;;) {
+    uint32_t used = 0;
+    for (uint32_t w = lane; w < kBitmapWords; w += 32) used += __popc(bitmap_word(h, w));
+    used = __reduce_add_sync(kFull, used);
+    const bool admit = used == 0 || used + np + reserve <= total;
+    start = admit ? first_fit(h, total, np) : kNone;
+    if (start != kNone && try_claim(h, start, np)) break;
+    __nanosleep(nap);
+    nap = min(nap * 2, 16384u);
+    ++hw;
+  }
+  if (lane == 0 && hw) atomicAdd(stats + 2, hw);
+  __syncwarp();
+  return start;
+}
+
+// non-blocking: one attempt, kNone on failure
+__device__ uint32_t heap_try_alloc(HeapHdr* h, uint32_t total, uint32_t np) {
+  const uint32_t start = first_fit(h, total, np);
+  if (start == kNone || !try_claim(h, start, np)) return kNone;
+  return start;
+}
+
+__device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np) {
+  const uint32_t lane = threadIdx.x & 31;
+  __syncwarp();
+  if (np == 0) return;
+  __threadfence_block();
+  for (uint32_t w = (start >> 5) + lane; w <= (start + np - 1) >> 5; w += 32)
+    atomicAnd(&h->bitmap[w], ~range_mask(w, start, np));
+  __syncwarp();
+}
+
+// Claim a global arena slot (whole warp; spins while all are busy).
+__device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t got = kNone;
+    if (lane == 0) {
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t m = 1u << (i & 31);
+        if (!(atomicOr(&bits[i >> 5], m) & m)) { got = i; break; }
+      }
+    }
+    got = __shfl_sync(kFull, got, 0);
+    if (got != kNone) return got;
+    __nanosleep(1024);
+  }
+}
+
+// Where the free list lives, for growth.
+struct Grow {
+  HeapHdr* h;
+  unsigned char* pages;
+  uint32_t total;
+  uint32_t fstart, fnp;     // current F pages in the heap (kNone: not in the heap)
+  uint32_t* stats;
+};
+
+// Move the free list to a region twice as large (entries keep their indices).
+// Non-blocking: returns false if no such region is free right now.
+__device__ __forceinline__ bool grow_f(State& S, Grow& G, uint32_t nf) {
+  if (G.fstart == kNone) return false;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t ncap = S.cap_f * 2 + 32;
+  const uint32_t np = uint32_t((f_bytes(ncap) + kPage - 1) / kPage);
+  if (np > G.total) return false;
+  uint32_t st = kNone;
+  for (int tries = 0; tries < 64; ++tries) {          // short bounded wait, then give up
+    st = heap_try_alloc(G.h, G.total, np);
+    if (st != kNone) break;
+    __nanosleep(1000);
+  }
+  if (st == kNone) return false;
+  State T = S;
+  carve_f(T, G.pages + size_t(st) * kPage, ncap);
+  for (uint32_t f = lane; f < nf; f += 32) {
+    T.F_pos[f] = S.F_pos[f];
+    T.F_key[f] = S.F_key[f];
+    T.F_size[f] = S.F_size[f];
+    T.F_prev[f] = S.F_prev[f];
+    T.F_next[f] = S.F_next[f];
+  }
+  __syncwarp();
+  heap_free(G.h, G.fstart, G.fnp);
+#ifdef XM_TRACE
+  if (lane == 0) printf("grow cap %u -> %u nf=%u old[%u,+%u) new[%u,+%u)\n", S.cap_f, ncap, nf, G.fstart, G.fnp, st, np);
+#endif
+  G.fstart = st;
+  G.fnp = np;
+  S = T;
+  if (lane == 0) atomicAdd(G.stats + 4, 1u);
+  return true;
 }
 
 // Reclamation (reading Q3; PAPER.md:259 (iv) "Cached blocks persist until the
@@ -245,17 +423,19 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, 
   return __shfl_sync(kFull, bf, wl);
 }
 
-// Replays events [e0, e0+n) of one trace on state S. Returns the status; on
-// XM_T_OVERFLOW the caller restarts the trace with a larger free list.
+// Replays events [e0, e0+n) of one trace on state S. Returns the status
+// (XM_T_OVERFLOW when the free list can no longer grow in shared memory: the
+// caller restarts the trace in a global arena).
 //
-// Warp-uniform execution: every lane runs the same bookkeeping on the same
-// values (loads of the same address are broadcasts; stores of the same value
-// to the same address are benign), so no broadcasts are needed. This is only
-// correct while the warp is CONVERGED: a split lane group would re-read state
-// another group already updated. The only lane-dependent branches are the
-// best-fit scan loop (reconverges before the reduction) and lane-0 regions in
-// the caller, each closed by __syncwarp(); every event also ends with one.
-__device__ __forceinline__ int replay_trace(const KParams& P, const State& S, int64_t e0,
+// Execution discipline. Every lane runs the same bookkeeping on the same values
+// (loads of one address are broadcasts, stores of one value to one address are
+// benign), so nothing is broadcast. Under independent thread scheduling the
+// warp may nevertheless run as several lane groups; to stay correct then,
+// every event is split into a LOAD phase and a STORE phase separated by
+// __syncwarp(): no lane stores before every lane has loaded, so a lagging
+// group can never read state this event already changed, and the barrier at
+// the end of the event orders the stores before the next event's loads.
+__device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G, int64_t e0,
                                             uint32_t n, uint64_t cap_u, xm_result& R) {
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
@@ -279,7 +459,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
     const uint32_t tc = t_nx;
     const uint32_t cnt = min(32u, n - base);
     if (base + 32 + lane < n) { b_nx = __ldcs(by + base + 32 + lane); t_nx = __ldcs(tg + base + 32 + lane); }
-    __syncwarp();                                       // reconverge after the lane-dependent branch
+    __syncwarp();
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;
     const uint64_t mag = is_alloc ? uint64_t(bc) : uint64_t(-bc);
@@ -309,7 +489,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
         const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
         uint32_t best = kNone, bf = kNone;
-        uint64_t bpos = ~0ull;          // valid iff bpos_ok
+        uint64_t bpos = ~0ull;
         bool bpos_ok = false;
         for (uint32_t f = lane; f < nf; f += 32) {
           const uint32_t k = S.F_key[f];
@@ -323,7 +503,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
             }
           }
         }
-        __syncwarp();                                   // reconverge after the scan
+        __syncwarp();
         const bool has = bf != kNone;
         const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone);
         uint32_t fsel = kNone;
@@ -348,7 +528,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
             fsel = __shfl_sync(kFull, bf, wl);
           }
         }
-        uint32_t bsize, bprev, bnext;
+        // ---- load phase (plus the rare reclaim / growth, each self-contained) ----
+        uint32_t bsize, bprev = kNone, bnext = kNone;
         uint64_t bposu;
         if (fsel == kNone) {
           // a4/a6: new segment from the device level (PAPER.md:259 (iv), 169, 654)
@@ -360,9 +541,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
             reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
             if (reserved + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
+          if (nseg >= kMaxSegs) { status = kStatusOverflow; break; }   // pos field limit
           bsize = a;
-          bprev = kNone;
-          bnext = kNone;
           bposu = uint64_t(nseg) << 32;
           nseg += 1;
           live_segs += 1;
@@ -378,13 +558,23 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
         const bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
+        if (split && fsel == kNone && nf >= S.cap_f && !grow_f(S, G, nf)) {
+          status = kStatusOverflow;
+          break;
+        }
+        const bool remove = !split && fsel != kNone;     // the whole free block is taken
+        const uint32_t L = nf - 1;
+        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
+        uint64_t lpos = 0;
+        if (remove && fsel != L) {
+          lk = S.F_key[L]; lsz = S.F_size[L]; lpv = S.F_prev[L]; lnx = S.F_next[L]; lpos = S.F_pos[L];
+        }
+        __syncwarp();
+        // ---- store phase ----
         uint32_t asize;
         if (split) {
-          uint32_t r;
-          if (fsel != kNone) {
-            r = fsel;                                  // remainder keeps the free entry
-          } else {
-            if (nf >= S.cap_f) { status = kStatusOverflow; break; }
+          uint32_t r = fsel;                           // remainder keeps the free entry
+          if (fsel == kNone) {
             r = nf++;
             S.F_next[r] = kNone;                       // new segment: no right neighbour
           }
@@ -397,53 +587,83 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
         } else {
           S.A_next[id] = bnext;
           set_prev(S, bnext, id);
-          if (fsel != kNone) f_remove(S, fsel, nf);
+          if (remove) {                                // move the last entry into fsel
+            if (fsel != L) {
+              S.F_key[fsel] = lk; S.F_size[fsel] = lsz; S.F_pos[fsel] = lpos;
+              S.F_prev[fsel] = lpv; S.F_next[fsel] = lnx;
+              set_next(S, lpv, kF | fsel);
+              set_prev(S, lnx, kF | fsel);
+            }
+            nf = L;
+          }
           asize = bsize;
         }
         S.A_size[id] = asize;
-        S.A_pos[id] = bposu;
+        S.A_pos[id] = bposu | (uint64_t(cls) << kPosBits);
         S.A_prev[id] = bprev;
-        S.A_cls[id] = uint8_t(cls);
         set_next(S, bprev, id);
         blk += asize;
         // a9: the block peak only moves up on allocs, first index (Q7)
         if (blk > pk_blk) { pk_blk = blk; ix_blk = base + j; }
       } else {
         // ================= FREE =================
+        // ---- load phase ----
         const uint32_t sz = S.A_size[id];
         const uint32_t p = S.A_prev[id];
         const uint32_t q = S.A_next[id];
+        const uint64_t apos = S.A_pos[id];
+        const uint32_t acls = uint32_t(apos >> kPosBits);
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
-        // a8: coalesce with free neighbours; reserved unchanged (PAPER.md:259 (iv))
+        const uint32_t P_ = p & ~kF, N_ = q & ~kF;
+        uint32_t psz = 0, nsz0 = 0, nnx = kNone;
+        if (pf) psz = S.F_size[P_];
+        if (qf) { nsz0 = S.F_size[N_]; nnx = S.F_next[N_]; }
+        if (!pf && !qf && nf >= S.cap_f && !grow_f(S, G, nf)) {
+          status = kStatusOverflow;
+          break;
+        }
+        const uint32_t L = nf - 1;                        // for removing N_ (both free)
+        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
+        uint64_t lpos = 0;
+        if (pf && qf && N_ != L) {
+          lk = S.F_key[L]; lsz = S.F_size[L]; lpv = S.F_prev[L]; lnx = S.F_next[L]; lpos = S.F_pos[L];
+        }
+        __syncwarp();
+        // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
+        // (PAPER.md:259 (iv)) ----
         if (pf) {
-          const uint32_t P_ = p & ~kF;
-          uint32_t nsz = S.F_size[P_] + sz;
-          uint32_t nn = q;
-          if (qf) {
-            const uint32_t N_ = q & ~kF;
-            nsz += S.F_size[N_];
-            nn = S.F_next[N_];
-          }
+          const uint32_t nsz = psz + sz + (qf ? nsz0 : 0u);
+          const uint32_t nn = qf ? nnx : q;
+          const uint32_t nk = make_key(acls, nsz);
           S.F_size[P_] = nsz;
-          S.F_key[P_] = make_key(S.A_cls[id], nsz);
+          S.F_key[P_] = nk;
           S.F_next[P_] = nn;
           set_prev(S, nn, p);
-          if (qf) f_remove(S, q & ~kF, nf);
+          if (qf) {                                   // drop N_: move the last entry there
+            if (N_ != L) {
+              if (L == P_) {                          // the last entry is the merged one
+                lk = nk; lsz = nsz; lnx = nn;
+              }
+              S.F_key[N_] = lk; S.F_size[N_] = lsz; S.F_pos[N_] = lpos;
+              S.F_prev[N_] = lpv; S.F_next[N_] = lnx;
+              set_next(S, lpv, kF | N_);
+              set_prev(S, lnx, kF | N_);
+            }
+            nf = L;
+          }
         } else if (qf) {
-          const uint32_t N_ = q & ~kF;
-          const uint32_t nsz = S.F_size[N_] + sz;
-          S.F_pos[N_] = S.A_pos[id];
+          const uint32_t nsz = nsz0 + sz;
+          S.F_pos[N_] = apos & kPosMask;
           S.F_size[N_] = nsz;
-          S.F_key[N_] = make_key(S.A_cls[id], nsz);
+          S.F_key[N_] = make_key(acls, nsz);
           S.F_prev[N_] = p;
           set_next(S, p, q);
         } else {
-          if (nf >= S.cap_f) { status = kStatusOverflow; break; }
           const uint32_t r = nf++;
-          S.F_pos[r] = S.A_pos[id];
+          S.F_pos[r] = apos & kPosMask;
           S.F_size[r] = sz;
-          S.F_key[r] = make_key(S.A_cls[id], sz);
+          S.F_key[r] = make_key(acls, sz);
           S.F_prev[r] = p;
           S.F_next[r] = q;
           set_next(S, p, kF | r);
@@ -484,104 +704,6 @@ __device__ __forceinline__ int replay_trace(const KParams& P, const State& S, in
   return status;
 }
 
-// ---- shared-memory heap (one per CTA) --------------------------------------
-// All heap and arena routines are called by the WHOLE warp with warp-uniform
-// control flow: single-lane work is predicated and its result broadcast, and
-// every wait loop tests a broadcast (uniform) condition. A lane-0-only branch
-// around a spinning call would leave the warp split into lane groups for the
-// rest of the trace, which breaks the warp-uniform replay (see replay_trace).
-__device__ __forceinline__ uint32_t bitmap_word(const HeapHdr* h, uint32_t w) {
-  return reinterpret_cast<const volatile uint32_t*>(h->bitmap)[w];
-}
-
-// Is [p, p+np) free? (reads the bitmap word by word)
-__device__ __forceinline__ bool run_free(const HeapHdr* h, uint32_t p, uint32_t np) {
-  const uint32_t e = p + np;
-  for (uint32_t q = p; q < e;) {
-    const uint32_t w = q >> 5, b0 = q & 31;
-    const uint32_t nb = min(32u - b0, e - q);
-    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
-    if (bitmap_word(h, w) & mask) return false;
-    q += nb;
-  }
-  return true;
-}
-
-// stats: [0] restarts, [1] arena runs, [2] heap wait rounds, [3] ticket wait rounds
-__device__ uint32_t heap_alloc(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats) {
-  const uint32_t lane = threadIdx.x & 31;
-  int t = 0;
-  if (lane == 0) t = atomicAdd(&h->ticket, 1);
-  t = __shfl_sync(kFull, t, 0);
-  uint32_t tw = 0, hw = 0;
-  for (;;) {                                                   // FIFO: wait for our ticket
-    const int srv = __shfl_sync(kFull, *(volatile int*)&h->serving, 0);
-    if (srv == t) break;
-    __nanosleep(128);
-    ++tw;
-  }
-  uint32_t start;
-  for (;;) {                                                   // first fit, lane-parallel
-    uint32_t cand = kNone;
-    for (uint32_t p = lane; p + np <= total; p += 32)
-      if (run_free(h, p, np)) { cand = p; break; }
-    __syncwarp();
-    start = __reduce_min_sync(kFull, cand);
-    if (start != kNone) break;
-    __nanosleep(512);
-    ++hw;
-  }
-  // claim: lane k sets word (start>>5)+k of the range
-  const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
-  for (uint32_t w = w0 + lane; w <= w1; w += 32) {
-    const uint32_t lo = max(start, w << 5), hi = min(start + np, (w + 1) << 5);
-    const uint32_t nb = hi - lo;
-    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo & 31);
-    const uint32_t old = atomicOr(&h->bitmap[w], mask);
-    XM_CHECK((old & mask) == 0, "heap overlap start=%u np=%u\n", start, np);
-    (void)old;
-  }
-  __syncwarp();
-  __threadfence_block();
-  if (lane == 0) {
-    atomicAdd(&h->serving, 1);
-    if (tw) atomicAdd(stats + 3, tw);
-    if (hw) atomicAdd(stats + 2, hw);
-  }
-  __syncwarp();
-  return start;
-}
-
-__device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
-  __syncwarp();
-  for (uint32_t w = w0 + lane; w <= w1; w += 32) {
-    const uint32_t lo = max(start, w << 5), hi = min(start + np, (w + 1) << 5);
-    const uint32_t nb = hi - lo;
-    const uint32_t mask = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo & 31);
-    atomicAnd(&h->bitmap[w], ~mask);
-  }
-  __syncwarp();
-}
-
-// Claim a global arena slot (whole warp; spins while all are busy).
-__device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
-  const uint32_t lane = threadIdx.x & 31;
-  for (;;) {
-    uint32_t got = kNone;
-    if (lane == 0) {
-      for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t m = 1u << (i & 31);
-        if (!(atomicOr(&bits[i >> 5], m) & m)) { got = i; break; }
-      }
-    }
-    got = __shfl_sync(kFull, got, 0);
-    if (got != kNone) return got;
-    __nanosleep(1024);
-  }
-}
-
 __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   HeapHdr* hdr = reinterpret_cast<HeapHdr*>(smem);
@@ -593,11 +715,16 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     for (uint32_t i = 0; i < kBitmapWords; ++i) hdr->bitmap[i] = 0;
   }
   __syncthreads();
+  uint32_t* stats = P.counter + 32;
   for (;;) {
+    ticket_acquire(hdr, stats);
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(P.counter, 1u);
     k = __shfl_sync(kFull, k, 0);
-    if (int64_t(k) >= P.n_traces) break;
+    if (int64_t(k) >= P.n_traces) {
+      ticket_release(hdr);
+      break;
+    }
     const uint32_t t = P.order[k];
     const int64_t e0 = P.off[t];
     const uint32_t n = uint32_t(P.off[t + 1] - e0);
@@ -606,25 +733,39 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     const uint64_t cap_u = cap >> P.u.unit_shift;
     xm_result R;
     const uint32_t nf_exact = n + 1;              // nf <= events
-    uint32_t nfc = min(nf_exact, na / 4 + 96);
     int st = kStatusOverflow;
-    for (;;) {
-      const uint32_t np = uint32_t((state_bytes(na, nfc) + kPage - 1) / kPage);
-      if (np > P.heap_pages) break;
-      const uint32_t start = heap_alloc(hdr, P.heap_pages, np, P.counter + 32);
-      const State S = carve(pages + size_t(start) * kPage, na, nfc);
-      st = replay_trace(P, S, e0, n, cap_u, R);
-      heap_free(hdr, start, np);
-      if (st != kStatusOverflow || nfc >= nf_exact) break;
-      if (lane == 0) atomicAdd(P.counter + 32, 1u);
-      nfc = min(nf_exact, nfc * 4);
+    // shared-memory region: A (fixed) then an initial free list
+    const uint32_t npa = max(1u, uint32_t((a_bytes(na) + kPage - 1) / kPage));
+    const uint32_t nfc = min(nf_exact, na / 2 + 64);
+    const uint32_t npf = uint32_t((f_bytes(nfc) + kPage - 1) / kPage);
+    if (npa + npf <= P.heap_pages) {
+      const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);
+      ticket_release(hdr);
+      State S;
+      carve_a(S, pages + size_t(start) * kPage, na);
+      carve_f(S, pages + size_t(start + npa) * kPage, nfc);
+      Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
+      st = replay_trace(P, S, G, e0, n, cap_u, R);
+      heap_free(hdr, start, npa);                  // A pages
+      heap_free(hdr, G.fstart, G.fnp);             // current F pages (maybe moved)
+      if (st == kStatusOverflow && lane == 0) atomicAdd(stats, 1u);
+      __syncwarp();
+    } else {
+      ticket_release(hdr);
     }
     if (st == kStatusOverflow) {
-      // global arena, exact bound: cannot overflow
+      // global arena, exact bound (cannot overflow unless the segment index does)
       const uint32_t slot = arena_claim(P.counter + 1, P.n_arena);
-      if (lane == 0) atomicAdd(P.counter + 33, 1u);
-      const State S = carve(P.arena + size_t(slot) * P.arena_bytes, na, nf_exact);
-      st = replay_trace(P, S, e0, n, cap_u, R);
+      if (lane == 0) atomicAdd(stats + 1, 1u);
+      unsigned char* base = P.arena + size_t(slot) * P.arena_bytes;
+      State S;
+      carve_a(S, base, na);
+      carve_f(S, base + ((a_bytes(P.arena_ids) + 15) & ~size_t(15)), nf_exact);
+      Grow G{hdr, pages, P.heap_pages, kNone, 0, stats};
+      st = replay_trace(P, S, G, e0, n, cap_u, R);
+#ifdef XM_TRACE
+      if (lane == 0) printf("trace %u arena slot %u status %d res=%llu\n", t, slot, st, (unsigned long long)R.peak_reserved);
+#endif
       __syncwarp();
       __threadfence();
       if (lane == 0) atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));

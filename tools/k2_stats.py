@@ -19,6 +19,6 @@ for wpc in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,8,16").spl
         e0.record(); xm.simulate_batch(dev, cfg, out=out); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     scr = list(dev._scratch.values())[-1]
-    st = scr[128:144].view(torch.int32).cpu().numpy()
+    st = scr[128:160].view(torch.int32).cpu().numpy()
     ev = int(xm.peaks(out)[0]["events_done"].astype(np.int64).sum())
-    print(f"wpc={wpc:2d} ms={min(ts):8.2f} ev/s={ev/min(ts)*1e3:.3e} restarts={st[0]} arena={st[1]} heap_spins={st[2]} ticket_spins={st[3]}", flush=True)
+    print(f"wpc={wpc:2d} ms={min(ts):8.2f} ev/s={ev/min(ts)*1e3:.3e} spills={st[0]} arena={st[1]} heap_wait={st[2]} ticket_wait={st[3]} grows={st[4]}", flush=True)
