@@ -8,14 +8,18 @@
 //
 // Execution model (DESIGN.md §6 K2):
 //  * persistent grid, one CTA per SM, up to 16 warps per CTA, one trace per
-//    warp; traces are pulled longest-first (host LPT order) from one counter;
+//    warp; traces are pulled longest-first (host LPT order), each CTA admitting
+//    them FIFO;
 //  * each CTA owns a shared-memory HEAP (the SM's 227 KB in 512 B pages). A
-//    warp takes (FIFO) one region for its trace: the id-indexed records (A,
-//    fixed size) followed by a small free list (F). When the free list fills,
-//    it moves to a region twice as large, if one can be claimed without
-//    waiting (entries keep their indices); otherwise the trace restarts in a
-//    global-memory arena sized to the exact bound. Occupancy thus adapts to
-//    the traces actually running;
+//    trace's state is two regions of it: the id-indexed records of allocated
+//    blocks (A, fixed size) and the free list (F), which moves to a region
+//    twice as large when it fills (entries keep their indices). Occupancy thus
+//    adapts to the traces actually running. Shared-memory state uses the
+//    NARROW layout (32-bit addresses, 16-bit links: 13 B per A record, 16 B
+//    per F entry); a trace that exceeds it (>= 32767 live blocks or free
+//    blocks, >= 2 TiB of segments ever created) or cannot grow restarts in a
+//    global-memory arena with the WIDE layout (64-bit addresses, 32-bit links),
+//    sized to the exact bound so it cannot overflow;
 //  * events stream through registers in 32-event tiles (coalesced streaming
 //    loads, next tile prefetched); round-up and the allocated-bytes prefix
 //    scan of a tile are lane-parallel (a2, a3);
@@ -23,13 +27,13 @@
 //    scalars, so no broadcasts); the best-fit search scans the free list
 //    lane-strided with ONE packed 32-bit key per entry (class in the top 5
 //    bits, saturated size below) and __reduce_min_sync; ties in size are
-//    broken by pos, loaded only when needed (a5).
+//    broken by address, loaded only when needed (a5).
 //
 // State (structure of arrays):
-//  A[id]  allocated block of dense id: pos u64 (cls in bits 59-63), size u32, prev u32, next u32
-//  F[f]   free block f (unordered, nf entries): pos u64, key u32, size u32, prev u32, next u32
-//  pos  = segment_index << 32 | offset_in_units  (bump addresses never reused:
-//         (size, pos) order == SPEC D2's (size, segment, offset), reading Q4)
+//  A[id]  allocated block of dense id: addr, size u32, prev, next, cls u8
+//  F[f]   free block f (unordered, nf entries): key u32, size u32, addr, prev, next
+//  addr = bump address in units of min_block (segments are never reused, so
+//         (size, addr) order == SPEC D2's (size, segment, offset), reading Q4)
 //  prev/next = address-order neighbours in the segment: kNone, an id, or kF|f
 //  cls  = stream << 1 | small_pool ;  key = cls << 27 | min(size, 2^27-1)
 #include <cuda_runtime.h>
@@ -54,8 +58,7 @@
 
 namespace {
 
-constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr uint32_t kF = 0x80000000u;
+constexpr uint32_t kNone32 = 0xFFFFFFFFu;
 constexpr uint32_t kIdMask = 0x07FFFFFFu;
 constexpr uint32_t kAllocBit = 0x08000000u;
 constexpr uint32_t kKeyBits = 27;
@@ -88,7 +91,7 @@ struct KParams {
   int64_t n_traces;
   xm_internal::UnitConfig u;
   uint32_t heap_pages;       // pages per CTA heap
-  uint32_t* counter;         // [0] work counter; [1..] arena claim bitmap
+  uint32_t* counter;         // [0] work counter; [1..2] arena claim bitmap; [32..] stats
   unsigned char* arena;
   size_t arena_bytes;        // bytes per arena slot
   uint32_t n_arena;
@@ -96,42 +99,71 @@ struct KParams {
   xm_result* out;
 };
 
+// ---- the two state layouts ---------------------------------------------------
+struct Narrow {                       // shared memory
+  using Addr = uint32_t;
+  using Link = uint16_t;
+  static constexpr uint32_t kNone = 0xFFFFu;
+  static constexpr uint32_t kF = 0x8000u;
+  static constexpr uint32_t kMaxIdx = 0x7FFFu;          // ids and free entries < 32767
+  static constexpr uint64_t kMaxAddr = 0xFFFFFFFFull;   // bump addresses < 2^32 units
+  static constexpr size_t kABytes = 4 + 4 + 2 + 2 + 1;  // 13
+  static constexpr size_t kFBytes = 4 + 4 + 4 + 2 + 2;  // 16
+};
+struct Wide {                         // global-memory arena
+  using Addr = uint64_t;
+  using Link = uint32_t;
+  static constexpr uint32_t kNone = 0xFFFFFFFFu;
+  static constexpr uint32_t kF = 0x80000000u;
+  static constexpr uint32_t kMaxIdx = 0x7FFFFFFFu;
+  static constexpr uint64_t kMaxAddr = ~0ull;
+  static constexpr size_t kABytes = 8 + 4 + 4 + 4 + 1;  // 21
+  static constexpr size_t kFBytes = 8 + 4 + 4 + 4 + 4;  // 24
+};
+
+template <class L>
 struct State {
-  uint64_t* A_pos;
+  typename L::Addr* A_pos;
   uint32_t* A_size;
-  uint32_t* A_prev;
-  uint32_t* A_next;
-  uint64_t* F_pos;
+  typename L::Link* A_prev;
+  typename L::Link* A_next;
+  uint8_t* A_cls;
+  typename L::Addr* F_pos;
   uint32_t* F_key;
   uint32_t* F_size;
-  uint32_t* F_prev;
-  uint32_t* F_next;
+  typename L::Link* F_prev;
+  typename L::Link* F_next;
   uint32_t cap_f;
 };
 
-constexpr uint32_t kPosBits = 59;                 // A_pos: cls in bits 59-63
-constexpr uint64_t kPosMask = (1ull << kPosBits) - 1;
-constexpr uint32_t kMaxSegs = 1u << 27;           // segment index must fit bits 32-58
+template <class L>
+__host__ __device__ inline size_t a_bytes(uint32_t na) { return size_t(na) * L::kABytes + 32; }
+template <class L>
+__host__ __device__ inline size_t f_bytes(uint32_t nf) { return size_t(nf) * L::kFBytes + 16; }
 
-__host__ __device__ inline size_t a_bytes(uint32_t na) { return size_t(na) * 20; }
-__host__ __device__ inline size_t f_bytes(uint32_t nf) { return size_t(nf) * 24; }
-__host__ __device__ inline size_t state_bytes(uint32_t na, uint32_t nf) {
-  return a_bytes(na) + f_bytes(nf) + 16;
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// arrays ordered by element size so every array stays naturally aligned
+template <class L>
+__device__ __forceinline__ void carve_a(State<L>& S, unsigned char* p, uint32_t na) {
+  using A = typename L::Addr;
+  using K = typename L::Link;
+  S.A_pos = reinterpret_cast<A*>(p); p += align16(size_t(na) * sizeof(A));
+  S.A_size = reinterpret_cast<uint32_t*>(p); p += align16(size_t(na) * 4);
+  S.A_prev = reinterpret_cast<K*>(p); p += size_t(na) * sizeof(K);
+  S.A_next = reinterpret_cast<K*>(p); p += size_t(na) * sizeof(K);
+  S.A_cls = p;
 }
 
-__device__ __forceinline__ void carve_a(State& S, unsigned char* p, uint32_t na) {
-  S.A_pos = reinterpret_cast<uint64_t*>(p); p += size_t(na) * 8;
-  S.A_size = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
-  S.A_prev = reinterpret_cast<uint32_t*>(p); p += size_t(na) * 4;
-  S.A_next = reinterpret_cast<uint32_t*>(p);
-}
-
-__device__ __forceinline__ void carve_f(State& S, unsigned char* p, uint32_t nf) {
-  S.F_pos = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
+template <class L>
+__device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t nf) {
+  using A = typename L::Addr;
+  using K = typename L::Link;
+  S.F_pos = reinterpret_cast<A*>(p); p += align16(size_t(nf) * sizeof(A));
   S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.F_prev = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.F_next = reinterpret_cast<uint32_t*>(p);
+  S.F_prev = reinterpret_cast<K*>(p); p += size_t(nf) * sizeof(K);
+  S.F_next = reinterpret_cast<K*>(p);
   S.cap_f = nf;
 }
 
@@ -139,18 +171,18 @@ __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
   return (cls << kKeyBits) | (size < kKeyMax ? size : kKeyMax);
 }
 
-__device__ __forceinline__ void set_next(const State& S, uint32_t ref, uint32_t v) {
-  if (ref == kNone) return;
-  XM_CHECK(!(ref & kF) || (ref & ~kF) < S.cap_f, "set_next ref=%x cap=%u\n", ref, S.cap_f);
-  if (ref & kF) S.F_next[ref & ~kF] = v;
-  else S.A_next[ref] = v;
+template <class L>
+__device__ __forceinline__ void set_next(const State<L>& S, uint32_t ref, uint32_t v) {
+  if (ref == L::kNone) return;
+  if (ref & L::kF) S.F_next[ref & ~L::kF] = typename L::Link(v);
+  else S.A_next[ref] = typename L::Link(v);
 }
 
-__device__ __forceinline__ void set_prev(const State& S, uint32_t ref, uint32_t v) {
-  if (ref == kNone) return;
-  XM_CHECK(!(ref & kF) || (ref & ~kF) < S.cap_f, "set_prev ref=%x cap=%u\n", ref, S.cap_f);
-  if (ref & kF) S.F_prev[ref & ~kF] = v;
-  else S.A_prev[ref] = v;
+template <class L>
+__device__ __forceinline__ void set_prev(const State<L>& S, uint32_t ref, uint32_t v) {
+  if (ref == L::kNone) return;
+  if (ref & L::kF) S.F_prev[ref & ~L::kF] = typename L::Link(v);
+  else S.A_prev[ref] = typename L::Link(v);
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
@@ -172,10 +204,9 @@ __device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
 // All heap and arena routines are called by the WHOLE warp with warp-uniform
 // control flow: single-lane work is predicated and its result broadcast, and
 // every wait loop tests a broadcast (uniform) condition. (A lane-0-only branch
-// around a spinning call can leave the warp split into lane groups, which
-// breaks the warp-uniform replay below.) Pages are claimed with atomicOr on
-// the bitmap and rolled back on conflict, so a FIFO allocation and a
-// non-blocking free-list growth can race safely.
+// around a spinning call can leave the warp split into lane groups.) Pages are
+// claimed with atomicOr on the bitmap and rolled back on conflict, so the
+// FIFO admission and a non-blocking free-list growth can race safely.
 __device__ __forceinline__ uint32_t bitmap_word(const HeapHdr* h, uint32_t w) {
   return reinterpret_cast<const volatile uint32_t*>(h->bitmap)[w];
 }
@@ -193,10 +224,10 @@ __device__ __forceinline__ bool run_free(const HeapHdr* h, uint32_t p, uint32_t 
   return true;
 }
 
-// lowest start of np free pages (lane-parallel), or kNone
+// lowest start of np free pages (lane-parallel), or kNone32
 __device__ __forceinline__ uint32_t first_fit(const HeapHdr* h, uint32_t total, uint32_t np) {
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t cand = kNone;
+  uint32_t cand = kNone32;
   for (uint32_t p = lane; p + np <= total; p += 32)
     if (run_free(h, p, np)) { cand = p; break; }
   __syncwarp();
@@ -207,7 +238,8 @@ __device__ __forceinline__ uint32_t first_fit(const HeapHdr* h, uint32_t total, 
 __device__ __forceinline__ bool try_claim(HeapHdr* h, uint32_t start, uint32_t np) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w0 = start >> 5, w1 = (start + np - 1) >> 5;
-  uint32_t w = w0 + lane, mine = 0;
+  const uint32_t w = w0 + lane;
+  uint32_t mine = 0;
   bool clash = false;
   if (w <= w1) {
     const uint32_t m = range_mask(w, start, np);
@@ -221,7 +253,7 @@ __device__ __forceinline__ bool try_claim(HeapHdr* h, uint32_t start, uint32_t n
   return !any_clash;
 }
 
-// stats: [0] spills to the global arena, [1] arena runs, [2] heap wait rounds,
+// stats: [0] restarts in the arena, [1] arena runs, [2] heap wait rounds,
 //        [3] ticket wait rounds, [4] free-list growths
 //
 // Admission is FIFO per CTA: a warp takes a ticket, waits for its turn, and only
@@ -266,8 +298,8 @@ __device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t
     for (uint32_t w = lane; w < kBitmapWords; w += 32) used += __popc(bitmap_word(h, w));
     used = __reduce_add_sync(kFull, used);
     const bool admit = used == 0 || used + np + reserve <= total;
-    start = admit ? first_fit(h, total, np) : kNone;
-    if (start != kNone && try_claim(h, start, np)) break;
+    start = admit ? first_fit(h, total, np) : kNone32;
+    if (start != kNone32 && try_claim(h, start, np)) break;
     __nanosleep(nap);
     nap = min(nap * 2, 16384u);
     ++hw;
@@ -277,10 +309,10 @@ __device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t
   return start;
 }
 
-// non-blocking: one attempt, kNone on failure
+// non-blocking: one attempt, kNone32 on failure
 __device__ uint32_t heap_try_alloc(HeapHdr* h, uint32_t total, uint32_t np) {
   const uint32_t start = first_fit(h, total, np);
-  if (start == kNone || !try_claim(h, start, np)) return kNone;
+  if (start == kNone32 || !try_claim(h, start, np)) return kNone32;
   return start;
 }
 
@@ -298,7 +330,7 @@ __device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np) {
 __device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
   const uint32_t lane = threadIdx.x & 31;
   for (;;) {
-    uint32_t got = kNone;
+    uint32_t got = kNone32;
     if (lane == 0) {
       for (uint32_t i = 0; i < n; ++i) {
         const uint32_t m = 1u << (i & 31);
@@ -306,7 +338,7 @@ __device__ uint32_t arena_claim(uint32_t* bits, uint32_t n) {
       }
     }
     got = __shfl_sync(kFull, got, 0);
-    if (got != kNone) return got;
+    if (got != kNone32) return got;
     __nanosleep(1024);
   }
 }
@@ -316,26 +348,28 @@ struct Grow {
   HeapHdr* h;
   unsigned char* pages;
   uint32_t total;
-  uint32_t fstart, fnp;     // current F pages in the heap (kNone: not in the heap)
+  uint32_t fstart, fnp;     // current F pages in the heap (kNone32: not in the heap)
   uint32_t* stats;
 };
 
-// Move the free list to a region twice as large (entries keep their indices).
-// Non-blocking: returns false if no such region is free right now.
-__device__ __forceinline__ bool grow_f(State& S, Grow& G, uint32_t nf) {
-  if (G.fstart == kNone) return false;
+// Move the free list to a region about twice as large (entries keep their
+// indices). Returns false if the layout's index limit is reached or no region
+// frees up within a short bounded wait.
+template <class L>
+__device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
+  if (G.fstart == kNone32 || S.cap_f >= L::kMaxIdx) return false;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t ncap = S.cap_f * 2 + 32;
-  const uint32_t np = uint32_t((f_bytes(ncap) + kPage - 1) / kPage);
+  const uint32_t ncap = min(S.cap_f * 2 + 32, L::kMaxIdx);
+  const uint32_t np = uint32_t((f_bytes<L>(ncap) + kPage - 1) / kPage);
   if (np > G.total) return false;
-  uint32_t st = kNone;
-  for (int tries = 0; tries < 64; ++tries) {          // short bounded wait, then give up
+  uint32_t st = kNone32;
+  for (int tries = 0; tries < 64; ++tries) {
     st = heap_try_alloc(G.h, G.total, np);
-    if (st != kNone) break;
+    if (st != kNone32) break;
     __nanosleep(1000);
   }
-  if (st == kNone) return false;
-  State T = S;
+  if (st == kNone32) return false;
+  State<L> T = S;
   carve_f(T, G.pages + size_t(st) * kPage, ncap);
   for (uint32_t f = lane; f < nf; f += 32) {
     T.F_pos[f] = S.F_pos[f];
@@ -346,34 +380,34 @@ __device__ __forceinline__ bool grow_f(State& S, Grow& G, uint32_t nf) {
   }
   __syncwarp();
   heap_free(G.h, G.fstart, G.fnp);
-#ifdef XM_TRACE
-  if (lane == 0) printf("grow cap %u -> %u nf=%u old[%u,+%u) new[%u,+%u)\n", S.cap_f, ncap, nf, G.fstart, G.fnp, st, np);
-#endif
   G.fstart = st;
   G.fnp = np;
   S = T;
   if (lane == 0) atomicAdd(G.stats + 4, 1u);
+  __syncwarp();
   return true;
 }
 
 // Reclamation (reading Q3; PAPER.md:259 (iv) "Cached blocks persist until the
 // framework allocator needs more memory, but the device indicates an OOM
 // error"): release every free block that spans a whole segment, in all pools
-// and streams. Warp-parallel stable compaction of the free list.
-__device__ __forceinline__ void reclaim(const State& S, uint32_t& nf, uint64_t& reserved,
-                                     uint32_t& n_release, uint32_t& live_segs) {
+// and streams. Warp-parallel stable compaction of the free list (lanes write
+// distinct entries; barriers separate the reads of each chunk from its writes).
+template <class L>
+__device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_t& reserved,
+                                        uint32_t& n_release, uint32_t& live_segs) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t newn = 0, cnt = 0;
   uint64_t freed = 0;
   for (uint32_t base = 0; base < nf; base += 32) {
     const uint32_t f = base + lane;
     const bool valid = f < nf;
-    uint32_t k = 0, sz = 0, pv = kNone, nx = kNone;
-    uint64_t pos = 0;
+    uint32_t k = 0, sz = 0, pv = L::kNone, nx = L::kNone;
+    typename L::Addr pos = 0;
     if (valid) {
       k = S.F_key[f]; sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = S.F_pos[f];
     }
-    const bool whole = valid && pv == kNone && nx == kNone;
+    const bool whole = valid && pv == L::kNone && nx == L::kNone;
     const bool keep = valid && !whole;
     const unsigned km = __ballot_sync(kFull, keep);
     const unsigned wm = __ballot_sync(kFull, whole);
@@ -381,9 +415,10 @@ __device__ __forceinline__ void reclaim(const State& S, uint32_t& nf, uint64_t& 
     const uint32_t dst = newn + __popc(km & ((1u << lane) - 1u));
     __syncwarp();
     if (keep && dst != f) {
-      S.F_key[dst] = k; S.F_size[dst] = sz; S.F_pos[dst] = pos; S.F_prev[dst] = pv; S.F_next[dst] = nx;
-      set_next(S, pv, kF | dst);
-      set_prev(S, nx, kF | dst);
+      S.F_key[dst] = k; S.F_size[dst] = sz; S.F_pos[dst] = pos;
+      S.F_prev[dst] = typename L::Link(pv); S.F_next[dst] = typename L::Link(nx);
+      set_next(S, pv, L::kF | dst);
+      set_prev(S, nx, L::kF | dst);
     }
     __syncwarp();
     newn += __popc(km);
@@ -396,12 +431,13 @@ __device__ __forceinline__ void reclaim(const State& S, uint32_t& nf, uint64_t& 
   live_segs -= cnt;
 }
 
-// Exact best fit: min (size, pos) over entries of class cls with size >= s.
-// Used when the packed-key search cannot decide (ties, saturated sizes).
-__device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, uint32_t cls,
-                                                uint32_t s) {
+// Exact best fit: min (size, addr) over entries of class cls with size >= s.
+// Used when the packed-key search cannot decide (sizes >= 2^27 units).
+template <class L>
+__device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t nf, uint32_t cls,
+                                                   uint32_t s) {
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t bsz = kNone, bf = kNone;
+  uint32_t bsz = kNone32, bf = kNone32;
   uint64_t bpos = ~0ull;
   for (uint32_t f = lane; f < nf; f += 32) {
     const uint32_t k = S.F_key[f];
@@ -413,19 +449,19 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, 
   }
   __syncwarp();
   const uint32_t m = __reduce_min_sync(kFull, bsz);
-  if (m == kNone) return kNone;
+  if (m == kNone32) return kNone32;
   const bool c1 = bsz == m;
-  const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone;
+  const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone32;
   const uint32_t mh = __reduce_min_sync(kFull, hi);
-  const uint32_t lo = (c1 && hi == mh) ? uint32_t(bpos) : kNone;
+  const uint32_t lo = (c1 && hi == mh) ? uint32_t(bpos) : kNone32;
   const uint32_t ml = __reduce_min_sync(kFull, lo);
   const int wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
   return __shfl_sync(kFull, bf, wl);
 }
 
 // Replays events [e0, e0+n) of one trace on state S. Returns the status
-// (XM_T_OVERFLOW when the free list can no longer grow in shared memory: the
-// caller restarts the trace in a global arena).
+// (XM_T_OVERFLOW when the state outgrows the layout or cannot grow: the caller
+// restarts the trace in a WIDE global arena).
 //
 // Execution discipline. Every lane runs the same bookkeeping on the same values
 // (loads of one address are broadcasts, stores of one value to one address are
@@ -435,8 +471,11 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State& S, uint32_t nf, 
 // __syncwarp(): no lane stores before every lane has loaded, so a lagging
 // group can never read state this event already changed, and the barrier at
 // the end of the event orders the stores before the next event's loads.
-__device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G, int64_t e0,
+template <class L>
+__device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow& G, int64_t e0,
                                             uint32_t n, uint64_t cap_u, xm_result& R) {
+  using Link = typename L::Link;
+  constexpr uint32_t kNone = L::kNone, kF = L::kF;
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
   const uint64_t unit_m1 = (1ull << u.unit_shift) - 1;
@@ -444,7 +483,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
   const uint32_t* __restrict__ tg = P.tag + e0;
 
   uint32_t nf = 0, nseg = 0, live_segs = 0, max_live = 0, n_release = 0;
-  uint64_t reserved = 0, blk = 0;
+  uint64_t reserved = 0, blk = 0, bump = 0;
   int64_t tensor = 0;
   uint64_t pk_tensor = 0, pk_blk = 0, pk_res = 0;
   uint32_t ix_tensor = 0, ix_blk = 0, ix_res = 0;
@@ -483,12 +522,12 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
         // ================= ALLOC =================
         const uint32_t small = s <= u.small_u;                     // a4: pool
         const uint32_t cls = ((w >> 28) << 1) | small;             // per-stream pools (Q5)
-        // a5: best fit = min (size, pos) over free blocks of class cls with
+        // a5: best fit = min (size, addr) over free blocks of class cls with
         // size >= s. Candidate iff key in [cls<<27 | min(s,max), cls<<27 | max];
-        // equal keys are ordered by pos, loaded only on a tie.
+        // equal keys are ordered by addr, loaded only on a tie.
         const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
-        uint32_t best = kNone, bf = kNone;
+        uint32_t best = kNone32, bf = kNone32;
         uint64_t bpos = ~0ull;
         bool bpos_ok = false;
         for (uint32_t f = lane; f < nf; f += 32) {
@@ -504,10 +543,10 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
           }
         }
         __syncwarp();
-        const bool has = bf != kNone;
-        const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone);
-        uint32_t fsel = kNone;
-        if (m != kNone || __any_sync(kFull, has)) {
+        const bool has = bf != kNone32;
+        const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone32);
+        uint32_t fsel = kNone32;
+        if (m != kNone32 || __any_sync(kFull, has)) {
           if ((m & kKeyMax) == kKeyMax) {
             fsel = best_fit_exact(S, nf, cls, s);          // saturated sizes: exact compare
           } else {
@@ -516,12 +555,12 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
             int wl;
             if ((win & (win - 1u)) == 0u) {
               wl = __ffs(win) - 1;
-            } else {                                       // size tie across lanes: min pos
+            } else {                                       // size tie across lanes: min addr
               if (c1 && !bpos_ok) bpos = S.F_pos[bf];
               __syncwarp();
-              const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone;
+              const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone32;
               const uint32_t mh = __reduce_min_sync(kFull, hi);
-              const uint32_t lo2 = (c1 && hi == mh) ? uint32_t(bpos) : kNone;
+              const uint32_t lo2 = (c1 && hi == mh) ? uint32_t(bpos) : kNone32;
               const uint32_t ml = __reduce_min_sync(kFull, lo2);
               wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
             }
@@ -531,7 +570,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
         // ---- load phase (plus the rare reclaim / growth, each self-contained) ----
         uint32_t bsize, bprev = kNone, bnext = kNone;
         uint64_t bposu;
-        if (fsel == kNone) {
+        if (fsel == kNone32) {
           // a4/a6: new segment from the device level (PAPER.md:259 (iv), 169, 654)
           uint32_t a;
           if (small) a = u.sbuf_u;
@@ -541,9 +580,10 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
             reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
             if (reserved + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
-          if (nseg >= kMaxSegs) { status = kStatusOverflow; break; }   // pos field limit
+          if (bump + a > L::kMaxAddr) { status = kStatusOverflow; break; }  // address width
           bsize = a;
-          bposu = uint64_t(nseg) << 32;
+          bposu = bump;                                        // bump address, never reused
+          bump += a;
           nseg += 1;
           live_segs += 1;
           max_live = max(max_live, live_segs);
@@ -558,49 +598,50 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
         const bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
-        if (split && fsel == kNone && nf >= S.cap_f && !grow_f(S, G, nf)) {
+        if (split && fsel == kNone32 && nf >= S.cap_f && !grow_f(S, G, nf)) {
           status = kStatusOverflow;
           break;
         }
-        const bool remove = !split && fsel != kNone;     // the whole free block is taken
-        const uint32_t L = nf - 1;
+        const bool remove = !split && fsel != kNone32;  // the whole free block is taken
+        const uint32_t Lx = nf - 1;
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
-        if (remove && fsel != L) {
-          lk = S.F_key[L]; lsz = S.F_size[L]; lpv = S.F_prev[L]; lnx = S.F_next[L]; lpos = S.F_pos[L];
+        if (remove && fsel != Lx) {
+          lk = S.F_key[Lx]; lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = S.F_pos[Lx];
         }
         __syncwarp();
         // ---- store phase ----
         uint32_t asize;
         if (split) {
           uint32_t r = fsel;                           // remainder keeps the free entry
-          if (fsel == kNone) {
+          if (fsel == kNone32) {
             r = nf++;
-            S.F_next[r] = kNone;                       // new segment: no right neighbour
+            S.F_next[r] = Link(kNone);                 // new segment: no right neighbour
           }
           S.F_pos[r] = bposu + s;
           S.F_key[r] = make_key(cls, rem);
           S.F_size[r] = rem;
-          S.F_prev[r] = id;
-          S.A_next[id] = kF | r;
+          S.F_prev[r] = Link(id);
+          S.A_next[id] = Link(kF | r);
           asize = s;
         } else {
-          S.A_next[id] = bnext;
+          S.A_next[id] = Link(bnext);
           set_prev(S, bnext, id);
           if (remove) {                                // move the last entry into fsel
-            if (fsel != L) {
+            if (fsel != Lx) {
               S.F_key[fsel] = lk; S.F_size[fsel] = lsz; S.F_pos[fsel] = lpos;
-              S.F_prev[fsel] = lpv; S.F_next[fsel] = lnx;
+              S.F_prev[fsel] = Link(lpv); S.F_next[fsel] = Link(lnx);
               set_next(S, lpv, kF | fsel);
               set_prev(S, lnx, kF | fsel);
             }
-            nf = L;
+            nf = Lx;
           }
           asize = bsize;
         }
         S.A_size[id] = asize;
-        S.A_pos[id] = bposu | (uint64_t(cls) << kPosBits);
-        S.A_prev[id] = bprev;
+        S.A_pos[id] = bposu;
+        S.A_prev[id] = Link(bprev);
+        S.A_cls[id] = uint8_t(cls);
         set_next(S, bprev, id);
         blk += asize;
         // a9: the block peak only moves up on allocs, first index (Q7)
@@ -612,7 +653,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
         const uint32_t p = S.A_prev[id];
         const uint32_t q = S.A_next[id];
         const uint64_t apos = S.A_pos[id];
-        const uint32_t acls = uint32_t(apos >> kPosBits);
+        const uint32_t acls = S.A_cls[id];
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
         const uint32_t P_ = p & ~kF, N_ = q & ~kF;
@@ -623,11 +664,11 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
           status = kStatusOverflow;
           break;
         }
-        const uint32_t L = nf - 1;                        // for removing N_ (both free)
+        const uint32_t Lx = nf - 1;                      // for removing N_ (both free)
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
-        if (pf && qf && N_ != L) {
-          lk = S.F_key[L]; lsz = S.F_size[L]; lpv = S.F_prev[L]; lnx = S.F_next[L]; lpos = S.F_pos[L];
+        if (pf && qf && N_ != Lx) {
+          lk = S.F_key[Lx]; lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = S.F_pos[Lx];
         }
         __syncwarp();
         // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
@@ -638,34 +679,34 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State& S, Grow& G,
           const uint32_t nk = make_key(acls, nsz);
           S.F_size[P_] = nsz;
           S.F_key[P_] = nk;
-          S.F_next[P_] = nn;
+          S.F_next[P_] = Link(nn);
           set_prev(S, nn, p);
           if (qf) {                                   // drop N_: move the last entry there
-            if (N_ != L) {
-              if (L == P_) {                          // the last entry is the merged one
+            if (N_ != Lx) {
+              if (Lx == P_) {                         // the last entry is the merged one
                 lk = nk; lsz = nsz; lnx = nn;
               }
               S.F_key[N_] = lk; S.F_size[N_] = lsz; S.F_pos[N_] = lpos;
-              S.F_prev[N_] = lpv; S.F_next[N_] = lnx;
+              S.F_prev[N_] = Link(lpv); S.F_next[N_] = Link(lnx);
               set_next(S, lpv, kF | N_);
               set_prev(S, lnx, kF | N_);
             }
-            nf = L;
+            nf = Lx;
           }
         } else if (qf) {
           const uint32_t nsz = nsz0 + sz;
-          S.F_pos[N_] = apos & kPosMask;
+          S.F_pos[N_] = apos;
           S.F_size[N_] = nsz;
           S.F_key[N_] = make_key(acls, nsz);
-          S.F_prev[N_] = p;
+          S.F_prev[N_] = Link(p);
           set_next(S, p, q);
         } else {
           const uint32_t r = nf++;
-          S.F_pos[r] = apos & kPosMask;
+          S.F_pos[r] = apos;
           S.F_size[r] = sz;
           S.F_key[r] = make_key(acls, sz);
-          S.F_prev[r] = p;
-          S.F_next[r] = q;
+          S.F_prev[r] = Link(p);
+          S.F_next[r] = Link(q);
           set_next(S, p, kF | r);
           set_prev(S, q, kF | r);
         }
@@ -734,14 +775,14 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     xm_result R;
     const uint32_t nf_exact = n + 1;              // nf <= events
     int st = kStatusOverflow;
-    // shared-memory region: A (fixed) then an initial free list
-    const uint32_t npa = max(1u, uint32_t((a_bytes(na) + kPage - 1) / kPage));
-    const uint32_t nfc = min(nf_exact, na / 2 + 64);
-    const uint32_t npf = uint32_t((f_bytes(nfc) + kPage - 1) / kPage);
-    if (npa + npf <= P.heap_pages) {
+    // shared memory, NARROW layout: A region + an initial free list
+    const uint32_t npa = uint32_t((a_bytes<Narrow>(na) + kPage - 1) / kPage);
+    const uint32_t nfc = min(min(nf_exact, na / 4 + 64), Narrow::kMaxIdx);
+    const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc) + kPage - 1) / kPage);
+    if (na <= Narrow::kMaxIdx && npa + npf <= P.heap_pages) {
       const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);
       ticket_release(hdr);
-      State S;
+      State<Narrow> S;
       carve_a(S, pages + size_t(start) * kPage, na);
       carve_f(S, pages + size_t(start + npa) * kPage, nfc);
       Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
@@ -754,21 +795,20 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       ticket_release(hdr);
     }
     if (st == kStatusOverflow) {
-      // global arena, exact bound (cannot overflow unless the segment index does)
+      // global arena, WIDE layout, exact bound (cannot overflow)
       const uint32_t slot = arena_claim(P.counter + 1, P.n_arena);
       if (lane == 0) atomicAdd(stats + 1, 1u);
+      __syncwarp();
       unsigned char* base = P.arena + size_t(slot) * P.arena_bytes;
-      State S;
+      State<Wide> S;
       carve_a(S, base, na);
-      carve_f(S, base + ((a_bytes(P.arena_ids) + 15) & ~size_t(15)), nf_exact);
-      Grow G{hdr, pages, P.heap_pages, kNone, 0, stats};
+      carve_f(S, base + align16(a_bytes<Wide>(P.arena_ids)), nf_exact);
+      Grow G{hdr, pages, P.heap_pages, kNone32, 0, stats};
       st = replay_trace(P, S, G, e0, n, cap_u, R);
-#ifdef XM_TRACE
-      if (lane == 0) printf("trace %u arena slot %u status %d res=%llu\n", t, slot, st, (unsigned long long)R.peak_reserved);
-#endif
       __syncwarp();
       __threadfence();
       if (lane == 0) atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
+      __syncwarp();
     }
     if (lane == 0) P.out[t] = R;
     __syncwarp();
@@ -803,7 +843,7 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   // state cannot live in shared memory
   p.arena_ids = b->max_ids;
   p.arena_free = b->max_events + 1;
-  p.arena_per_warp = (state_bytes(p.arena_ids, p.arena_free) + 255) & ~size_t(255);
+  p.arena_per_warp = (align16(a_bytes<Wide>(p.arena_ids)) + f_bytes<Wide>(p.arena_free) + 255) & ~size_t(255);
   const int64_t tw = int64_t(p.ctas) * p.warps_per_cta;
   const uint32_t n_arena = uint32_t(std::min<int64_t>(std::min<int64_t>(tw, 64),
                                                       std::max<int64_t>(1, b->n_traces)));
