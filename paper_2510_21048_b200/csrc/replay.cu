@@ -108,7 +108,8 @@ struct Narrow {                       // shared memory
   static constexpr uint32_t kMaxIdx = 0x7FFFu;          // ids and free entries < 32767
   static constexpr uint64_t kMaxAddr = 0xFFFFFFFFull;   // bump addresses < 2^32 units
   static constexpr size_t kABytes = 4 + 4 + 2 + 2 + 1;  // 13
-  static constexpr size_t kFBytes = 4 + 4 + 4 + 2 + 2;  // 16
+  static constexpr size_t kFBytes = 8 + 4 + 2 + 2;      // 16: (key<<32 | addr) packed
+  static constexpr bool kPacked = true;
 };
 struct Wide {                         // global-memory arena
   using Addr = uint64_t;
@@ -119,6 +120,7 @@ struct Wide {                         // global-memory arena
   static constexpr uint64_t kMaxAddr = ~0ull;
   static constexpr size_t kABytes = 8 + 4 + 4 + 4 + 1;  // 21
   static constexpr size_t kFBytes = 8 + 4 + 4 + 4 + 4;  // 24
+  static constexpr bool kPacked = false;
 };
 
 template <class L>
@@ -128,8 +130,9 @@ struct State {
   typename L::Link* A_prev;
   typename L::Link* A_next;
   uint8_t* A_cls;
-  typename L::Addr* F_pos;
-  uint32_t* F_key;
+  uint64_t* F_kp;            // Narrow: key << 32 | addr (one load per scanned entry)
+  typename L::Addr* F_pos;   // Wide: addr
+  uint32_t* F_key;           // Wide: key
   uint32_t* F_size;
   typename L::Link* F_prev;
   typename L::Link* F_next;
@@ -159,8 +162,12 @@ template <class L>
 __device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t nf) {
   using A = typename L::Addr;
   using K = typename L::Link;
-  S.F_pos = reinterpret_cast<A*>(p); p += align16(size_t(nf) * sizeof(A));
-  S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
+  if constexpr (L::kPacked) {
+    S.F_kp = reinterpret_cast<uint64_t*>(p); p += align16(size_t(nf) * 8);
+  } else {
+    S.F_pos = reinterpret_cast<A*>(p); p += align16(size_t(nf) * sizeof(A));
+    S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
+  }
   S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   S.F_prev = reinterpret_cast<K*>(p); p += size_t(nf) * sizeof(K);
   S.F_next = reinterpret_cast<K*>(p);
@@ -169,6 +176,27 @@ __device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t 
 
 __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
   return (cls << kKeyBits) | (size < kKeyMax ? size : kKeyMax);
+}
+
+// free-entry key / address accessors (packed in one word for the narrow layout)
+template <class L>
+__device__ __forceinline__ uint32_t fkey(const State<L>& S, uint32_t f) {
+  if constexpr (L::kPacked) return uint32_t(S.F_kp[f] >> 32);
+  else return S.F_key[f];
+}
+template <class L>
+__device__ __forceinline__ uint64_t fpos(const State<L>& S, uint32_t f) {
+  if constexpr (L::kPacked) return uint32_t(S.F_kp[f]);
+  else return S.F_pos[f];
+}
+template <class L>
+__device__ __forceinline__ void set_kp(const State<L>& S, uint32_t f, uint32_t key, uint64_t pos) {
+  if constexpr (L::kPacked) {
+    S.F_kp[f] = (uint64_t(key) << 32) | uint32_t(pos);
+  } else {
+    S.F_key[f] = key;
+    S.F_pos[f] = pos;
+  }
 }
 
 template <class L>
@@ -362,18 +390,26 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   const uint32_t ncap = min(S.cap_f * 2 + 32, L::kMaxIdx);
   const uint32_t np = uint32_t((f_bytes<L>(ncap) + kPage - 1) / kPage);
   if (np > G.total) return false;
-  uint32_t st = kNone32;
-  for (int tries = 0; tries < 64; ++tries) {
+  // Bounded wait (~2 ms): running traces finish and free pages long before a
+  // trace here could be restarted elsewhere; only when every resident trace is
+  // waiting to grow does this give up.
+  uint32_t st = kNone32, nap = 512;
+  for (int tries = 0; tries < 256; ++tries) {
     st = heap_try_alloc(G.h, G.total, np);
     if (st != kNone32) break;
-    __nanosleep(1000);
+    __nanosleep(nap);
+    nap = min(nap * 2, 8192u);
   }
   if (st == kNone32) return false;
   State<L> T = S;
   carve_f(T, G.pages + size_t(st) * kPage, ncap);
   for (uint32_t f = lane; f < nf; f += 32) {
-    T.F_pos[f] = S.F_pos[f];
-    T.F_key[f] = S.F_key[f];
+    if constexpr (L::kPacked) {
+      T.F_kp[f] = S.F_kp[f];
+    } else {
+      T.F_pos[f] = S.F_pos[f];
+      T.F_key[f] = S.F_key[f];
+    }
     T.F_size[f] = S.F_size[f];
     T.F_prev[f] = S.F_prev[f];
     T.F_next[f] = S.F_next[f];
@@ -405,7 +441,7 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
     uint32_t k = 0, sz = 0, pv = L::kNone, nx = L::kNone;
     typename L::Addr pos = 0;
     if (valid) {
-      k = S.F_key[f]; sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = S.F_pos[f];
+      k = fkey(S, f); sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = fpos(S, f);
     }
     const bool whole = valid && pv == L::kNone && nx == L::kNone;
     const bool keep = valid && !whole;
@@ -415,7 +451,7 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
     const uint32_t dst = newn + __popc(km & ((1u << lane) - 1u));
     __syncwarp();
     if (keep && dst != f) {
-      S.F_key[dst] = k; S.F_size[dst] = sz; S.F_pos[dst] = pos;
+      set_kp(S, dst, k, pos); S.F_size[dst] = sz;
       S.F_prev[dst] = typename L::Link(pv); S.F_next[dst] = typename L::Link(nx);
       set_next(S, pv, L::kF | dst);
       set_prev(S, nx, L::kF | dst);
@@ -440,11 +476,11 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t n
   uint32_t bsz = kNone32, bf = kNone32;
   uint64_t bpos = ~0ull;
   for (uint32_t f = lane; f < nf; f += 32) {
-    const uint32_t k = S.F_key[f];
+    const uint32_t k = fkey(S, f);
     if ((k >> kKeyBits) != cls) continue;
     const uint32_t sz = S.F_size[f];
     if (sz < s) continue;
-    const uint64_t pos = S.F_pos[f];
+    const uint64_t pos = fpos(S, f);
     if (sz < bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
   }
   __syncwarp();
@@ -527,44 +563,75 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         // equal keys are ordered by addr, loaded only on a tie.
         const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
-        uint32_t best = kNone32, bf = kNone32;
-        uint64_t bpos = ~0ull;
-        bool bpos_ok = false;
-        for (uint32_t f = lane; f < nf; f += 32) {
-          const uint32_t k = S.F_key[f];
-          if (k - lo <= span) {
-            if (k < best) {
-              best = k; bf = f; bpos_ok = false;
-            } else if (k == best) {
-              if (!bpos_ok) { bpos = S.F_pos[bf]; bpos_ok = true; }
-              const uint64_t pos = S.F_pos[f];
-              if (pos < bpos) { bf = f; bpos = pos; }
+        uint32_t fsel = kNone32;
+        if constexpr (L::kPacked) {
+          // one 64-bit load per entry: (key, addr) compares lexicographically
+          // as (size, addr) for unsaturated sizes; uniform trip count, no
+          // divergence (the body is predicated)
+          const uint64_t lo64 = uint64_t(lo) << 32;
+          const uint64_t span64 = (uint64_t(span) << 32) | 0xFFFFFFFFull;
+          uint64_t best = ~0ull;
+          uint32_t bf = kNone32;
+#pragma unroll 4
+          for (uint32_t b0 = 0; b0 < nf; b0 += 32) {
+            const uint32_t f = b0 + lane;
+            if (f < nf) {
+              const uint64_t kp = S.F_kp[f];
+              if (kp - lo64 <= span64 && kp < best) { best = kp; bf = f; }
             }
           }
-        }
-        __syncwarp();
-        const bool has = bf != kNone32;
-        const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone32);
-        uint32_t fsel = kNone32;
-        if (m != kNone32 || __any_sync(kFull, has)) {
-          if ((m & kKeyMax) == kKeyMax) {
-            fsel = best_fit_exact(S, nf, cls, s);          // saturated sizes: exact compare
-          } else {
-            const bool c1 = has && best == m;
-            const unsigned win = __ballot_sync(kFull, c1);
-            int wl;
-            if ((win & (win - 1u)) == 0u) {
-              wl = __ffs(win) - 1;
-            } else {                                       // size tie across lanes: min addr
-              if (c1 && !bpos_ok) bpos = S.F_pos[bf];
-              __syncwarp();
-              const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone32;
-              const uint32_t mh = __reduce_min_sync(kFull, hi);
-              const uint32_t lo2 = (c1 && hi == mh) ? uint32_t(bpos) : kNone32;
-              const uint32_t ml = __reduce_min_sync(kFull, lo2);
-              wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
+          const bool has = bf != kNone32;
+          const uint32_t bh = uint32_t(best >> 32);
+          const uint32_t mh = __reduce_min_sync(kFull, bh);
+          if (__any_sync(kFull, has)) {
+            if ((mh & kKeyMax) == kKeyMax) {
+              fsel = best_fit_exact(S, nf, cls, s);        // saturated sizes: exact compare
+            } else {
+              const bool c1 = has && bh == mh;
+              const uint32_t ml = __reduce_min_sync(kFull, c1 ? uint32_t(best) : kNone32);
+              const unsigned win = __ballot_sync(kFull, c1 && uint32_t(best) == ml);
+              fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
             }
-            fsel = __shfl_sync(kFull, bf, wl);
+          }
+        } else {
+          uint32_t best = kNone32, bf = kNone32;
+          uint64_t bpos = ~0ull;
+          bool bpos_ok = false;
+          for (uint32_t f = lane; f < nf; f += 32) {
+            const uint32_t k = S.F_key[f];
+            if (k - lo <= span) {
+              if (k < best) {
+                best = k; bf = f; bpos_ok = false;
+              } else if (k == best) {
+                if (!bpos_ok) { bpos = S.F_pos[bf]; bpos_ok = true; }
+                const uint64_t pos = S.F_pos[f];
+                if (pos < bpos) { bf = f; bpos = pos; }
+              }
+            }
+          }
+          __syncwarp();
+          const bool has = bf != kNone32;
+          const uint32_t m = __reduce_min_sync(kFull, has ? best : kNone32);
+          if (m != kNone32 || __any_sync(kFull, has)) {
+            if ((m & kKeyMax) == kKeyMax) {
+              fsel = best_fit_exact(S, nf, cls, s);        // saturated sizes: exact compare
+            } else {
+              const bool c1 = has && best == m;
+              const unsigned win = __ballot_sync(kFull, c1);
+              int wl;
+              if ((win & (win - 1u)) == 0u) {
+                wl = __ffs(win) - 1;
+              } else {                                     // size tie across lanes: min addr
+                if (c1 && !bpos_ok) bpos = S.F_pos[bf];
+                __syncwarp();
+                const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone32;
+                const uint32_t mh = __reduce_min_sync(kFull, hi);
+                const uint32_t lo2 = (c1 && hi == mh) ? uint32_t(bpos) : kNone32;
+                const uint32_t ml = __reduce_min_sync(kFull, lo2);
+                wl = __ffs(__ballot_sync(kFull, c1 && hi == mh && uint32_t(bpos) == ml)) - 1;
+              }
+              fsel = __shfl_sync(kFull, bf, wl);
+            }
           }
         }
         // ---- load phase (plus the rare reclaim / growth, each self-contained) ----
@@ -593,7 +660,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           bsize = S.F_size[fsel];
           bprev = S.F_prev[fsel];
           bnext = S.F_next[fsel];
-          bposu = S.F_pos[fsel];
+          bposu = fpos(S, fsel);
         }
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
@@ -607,7 +674,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
         if (remove && fsel != Lx) {
-          lk = S.F_key[Lx]; lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = S.F_pos[Lx];
+          lk = fkey(S, Lx); lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = fpos(S, Lx);
         }
         __syncwarp();
         // ---- store phase ----
@@ -618,8 +685,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
             r = nf++;
             S.F_next[r] = Link(kNone);                 // new segment: no right neighbour
           }
-          S.F_pos[r] = bposu + s;
-          S.F_key[r] = make_key(cls, rem);
+          set_kp(S, r, make_key(cls, rem), bposu + s);
           S.F_size[r] = rem;
           S.F_prev[r] = Link(id);
           S.A_next[id] = Link(kF | r);
@@ -629,7 +695,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           set_prev(S, bnext, id);
           if (remove) {                                // move the last entry into fsel
             if (fsel != Lx) {
-              S.F_key[fsel] = lk; S.F_size[fsel] = lsz; S.F_pos[fsel] = lpos;
+              set_kp(S, fsel, lk, lpos); S.F_size[fsel] = lsz;
               S.F_prev[fsel] = Link(lpv); S.F_next[fsel] = Link(lnx);
               set_next(S, lpv, kF | fsel);
               set_prev(S, lnx, kF | fsel);
@@ -658,7 +724,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         const bool qf = q != kNone && (q & kF);
         const uint32_t P_ = p & ~kF, N_ = q & ~kF;
         uint32_t psz = 0, nsz0 = 0, nnx = kNone;
-        if (pf) psz = S.F_size[P_];
+        uint64_t ppos = 0;
+        if (pf) { psz = S.F_size[P_]; ppos = fpos(S, P_); }
         if (qf) { nsz0 = S.F_size[N_]; nnx = S.F_next[N_]; }
         if (!pf && !qf && nf >= S.cap_f && !grow_f(S, G, nf)) {
           status = kStatusOverflow;
@@ -668,7 +735,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
         if (pf && qf && N_ != Lx) {
-          lk = S.F_key[Lx]; lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = S.F_pos[Lx];
+          lk = fkey(S, Lx); lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = fpos(S, Lx);
         }
         __syncwarp();
         // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
@@ -678,7 +745,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           const uint32_t nn = qf ? nnx : q;
           const uint32_t nk = make_key(acls, nsz);
           S.F_size[P_] = nsz;
-          S.F_key[P_] = nk;
+          set_kp(S, P_, nk, ppos);
           S.F_next[P_] = Link(nn);
           set_prev(S, nn, p);
           if (qf) {                                   // drop N_: move the last entry there
@@ -686,7 +753,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
               if (Lx == P_) {                         // the last entry is the merged one
                 lk = nk; lsz = nsz; lnx = nn;
               }
-              S.F_key[N_] = lk; S.F_size[N_] = lsz; S.F_pos[N_] = lpos;
+              set_kp(S, N_, lk, lpos); S.F_size[N_] = lsz;
               S.F_prev[N_] = Link(lpv); S.F_next[N_] = Link(lnx);
               set_next(S, lpv, kF | N_);
               set_prev(S, lnx, kF | N_);
@@ -695,16 +762,14 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           }
         } else if (qf) {
           const uint32_t nsz = nsz0 + sz;
-          S.F_pos[N_] = apos;
+          set_kp(S, N_, make_key(acls, nsz), apos);
           S.F_size[N_] = nsz;
-          S.F_key[N_] = make_key(acls, nsz);
           S.F_prev[N_] = Link(p);
           set_next(S, p, q);
         } else {
           const uint32_t r = nf++;
-          S.F_pos[r] = apos;
+          set_kp(S, r, make_key(acls, sz), apos);
           S.F_size[r] = sz;
-          S.F_key[r] = make_key(acls, sz);
           S.F_prev[r] = Link(p);
           S.F_next[r] = Link(q);
           set_next(S, p, kF | r);
@@ -825,7 +890,7 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   if (cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 16;
+  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 12;
   if (p.warps_per_cta > 16) p.warps_per_cta = 16;
   if (p.warps_per_cta < 1) p.warps_per_cta = 1;
   // heap: the whole per-CTA maximum unless capped (smem_per_warp x warps)
