@@ -9,15 +9,18 @@
 //
 // Flat, trace-oblivious decomposition so that long traces never bound the
 // launch (DESIGN.md §6 K1):
-//   K1z  tile_trace[c] = trace owning the first event of tile c   (T threads)
-//   K1a  one CTA per TILE-event tile: 8 contiguous events per thread, a
-//        segmented scan of the monoid (sum, max-prefix, argmax) across the
-//        CTA; traces wholly inside a tile are finished here, the tile's first
-//        and last pieces are stored for the traces that cross tile edges
-//   K1b  one thread per crossing trace folds its pieces (~len/TILE of them)
-// HBM traffic: 8 B/event read once + ~52 B/tile + 64 B/trace written.
+//   K1z  row_trace[r] = trace owning the first event of 16-event row r
+//   K1a  persistent CTAs over 4096-event tiles (cp.async double-buffered in
+//        shared memory), 16 contiguous events per thread. A tile
+//        with no trace start inside (the common case) is one piece: plain
+//        scan + argmax. Otherwise a segmented scan of the monoid (sum,
+//        max-prefix, argmax); traces wholly inside the tile are finished here
+//        and the tile's first/last pieces are stored for crossing traces
+//   K1b  one thread per crossing trace folds its pieces (~len/4096 of them)
+// HBM traffic: 8 B/event read once + 0.5 B/event row map + 48 B/tile + 64 B/trace.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "xm_internal.h"
@@ -26,36 +29,53 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kThreads = 256;
-constexpr int kPer = 8;                      // events per thread
-constexpr int kTile = kThreads * kPer;       // 2048 events per CTA
+constexpr int kPer = 16;                     // events per thread
+constexpr int kTile = kThreads * kPer;       // 4096 events per CTA
 constexpr int kWarps = kThreads / 32;
 constexpr int64_t kNeg = INT64_MIN;
 
-// piece monoid: sum of deltas, max prefix (relative to the piece start), its
-// flat event index. Identity: (0, kNeg, -1). combine(A, B) = A then B.
+// piece monoid as stored between kernels: sum of deltas, max prefix (relative
+// to the piece start, kNeg if empty), flat index of its first occurrence
 struct Mono {
   int64_t sum, mx, arg;
 };
 
-__device__ __forceinline__ Mono mono_id() { return Mono{0, kNeg, -1}; }
+// register form: tile-relative argmax; tr = trace of the head the piece
+// starts at (meaningful only for pieces that start at a head in this tile)
+struct MonoR {
+  int64_t sum, mx;
+  int32_t arg;
+  uint32_t tr;
+};
 
-__device__ __forceinline__ Mono combine(const Mono& a, const Mono& b) {
-  Mono r;
+__device__ __forceinline__ MonoR mono_id() { return MonoR{0, kNeg, -1, 0}; }
+
+// A then B (strict >: the earlier index wins ties)
+__device__ __forceinline__ MonoR combine(const MonoR& a, const MonoR& b) {
+  MonoR r;
   r.sum = a.sum + b.sum;
-  if (b.mx != kNeg && (a.mx == kNeg || a.sum + b.mx > a.mx)) {   // strict: first index wins
-    r.mx = a.sum + b.mx;
-    r.arg = b.arg;
-  } else {
-    r.mx = a.mx;
-    r.arg = a.arg;
-  }
+  const int64_t cand = a.sum + b.mx;
+  const bool take_b = b.mx != kNeg && cand > a.mx;
+  r.mx = take_b ? cand : a.mx;
+  r.arg = take_b ? b.arg : a.arg;
+  r.tr = a.tr;
   return r;
 }
 
+__device__ __forceinline__ Mono combine_g(const Mono& a, const Mono& b) {
+  Mono r;
+  r.sum = a.sum + b.sum;
+  const int64_t cand = a.sum + b.mx;
+  const bool take_b = b.mx != kNeg && cand > a.mx;
+  r.mx = take_b ? cand : a.mx;
+  r.arg = take_b ? b.arg : a.arg;
+  return r;
+}
+
+// +ceil(b/2^sh) for an alloc (b > 0), -ceil(-b/2^sh) = floor(b/2^sh) for a free:
+// one arithmetic shift either way
 __device__ __forceinline__ int64_t rounded_delta(int64_t b, uint32_t sh) {
-  const uint64_t mag = b > 0 ? uint64_t(b) : uint64_t(-b);
-  const int64_t s = int64_t((mag + ((1ull << sh) - 1)) >> sh);
-  return b > 0 ? s : -s;
+  return (b + (b > 0 ? int64_t((1ull << sh) - 1) : 0)) >> sh;
 }
 
 struct SParams {
@@ -64,211 +84,236 @@ struct SParams {
   int64_t n_traces, n_events;
   uint32_t unit_shift;
   int64_t n_tiles;
-  uint32_t* tile_trace;     // [n_tiles]
-  Mono* tile_first;         // [n_tiles] piece before the tile's first head
-  Mono* tile_last;          // [n_tiles] piece from the tile's last head
+  uint32_t* row_trace;      // [n_tiles * kThreads] trace owning each thread row's first event
+  Mono* tile_first;         // [n_tiles] piece before the tile's first trace start
+  Mono* tile_last;          // [n_tiles] piece from the tile's last trace start
   xm_result* out;
 };
 
-__device__ __forceinline__ void write_result(const SParams& P, uint32_t t, const Mono& m) {
+__device__ __forceinline__ Mono to_global(const MonoR& m, int64_t t0e) {
+  return Mono{m.sum, m.mx, m.arg < 0 ? -1 : t0e + m.arg};
+}
+
+__device__ __forceinline__ void write_result(const SParams& P, uint32_t t, int64_t mx,
+                                             int64_t arg_flat) {
   const int64_t o = P.off[t];
   xm_result R{};
-  const int64_t mx = m.mx > 0 ? m.mx : 0;
-  R.peak_allocated = uint64_t(mx) << P.unit_shift;
-  R.peak_allocated_idx = m.mx > 0 ? uint32_t(m.arg - o) : 0u;
+  R.peak_allocated = mx > 0 ? uint64_t(mx) << P.unit_shift : 0ull;
+  R.peak_allocated_idx = mx > 0 ? uint32_t(arg_flat - o) : 0u;
   R.events_done = uint32_t(P.off[t + 1] - o);
   R.status = XM_T_OK;
   P.out[t] = R;
 }
 
-// K1z: tile c's first event (c*kTile) lies in trace t iff off[t] <= c*kTile < off[t+1]
-__global__ void k_tile_map(SParams P) {
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= P.n_traces) return;
-  const int64_t a = P.off[t], b = P.off[t + 1];
-  if (b <= a) return;
-  for (int64_t c = (a + kTile - 1) / kTile; c * kTile < b; ++c) P.tile_trace[c] = uint32_t(t);
-}
-
-__device__ __forceinline__ Mono shfl_up_mono(const Mono& m, int o) {
-  return Mono{__shfl_up_sync(kFull, m.sum, o), __shfl_up_sync(kFull, m.mx, o),
-              __shfl_up_sync(kFull, m.arg, o)};
+__device__ __forceinline__ MonoR shfl_up_mono(const MonoR& m, int o) {
+  return MonoR{__shfl_up_sync(kFull, m.sum, o), __shfl_up_sync(kFull, m.mx, o),
+               __shfl_up_sync(kFull, m.arg, o), __shfl_up_sync(kFull, m.tr, o)};
 }
 
 // segmented op: (fa, A) (+) (fb, B) = (fa | fb, fb ? B : A.B)
-__device__ __forceinline__ void seg_combine(bool& fa, Mono& a, bool fb, const Mono& b) {
+__device__ __forceinline__ void seg_combine(bool& fa, MonoR& a, bool fb, const MonoR& b) {
   a = fb ? b : combine(a, b);
   fa = fa || fb;
 }
 
-__global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
-  __shared__ int32_t head_pos[kTile];       // tile-relative positions of heads (sorted)
-  __shared__ uint32_t head_trace[kTile];
-  __shared__ int n_heads_s;
-  __shared__ bool wflag[kWarps];
-  __shared__ Mono wagg[kWarps];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t c = blockIdx.x;
+// K1z: row_trace[r] = trace owning event r*kPer (one warp per trace, lanes stride
+// over its rows, so a long trace does not serialise)
+__global__ void k_row_map(SParams P) {
+  const int64_t t = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= P.n_traces) return;
+  const int64_t a = P.off[t], b = P.off[t + 1];
+  if (b <= a) return;
+  for (int64_t r = (a + kPer - 1) / kPer + lane; r * kPer < b; r += 32) P.row_trace[r] = uint32_t(t);
+}
+
+__device__ __forceinline__ void stage_tile(const SParams& P, unsigned char* buf, int64_t c) {
+  const int tid = threadIdx.x;
   const int64_t t0e = c * kTile;
   const int64_t t1e = min(t0e + kTile, P.n_events);
-  const uint32_t tf = P.tile_trace[c];
-
-  // ---- load this thread's 8 contiguous events first (latency overlaps the head search) ----
-  const int64_t g0 = t0e + int64_t(tid) * kPer;
-  int64_t d[kPer];
+  const int nchunks = int((t1e - t0e + 1) / 2);                   // 16 B = 2 events
+  const uint32_t sbase = uint32_t(__cvta_generic_to_shared(buf));
   const long long* by = reinterpret_cast<const long long*>(P.bytes);
-  if (g0 + kPer <= t1e) {
-    const longlong2* v = reinterpret_cast<const longlong2*>(by + g0);
 #pragma unroll
-    for (int i = 0; i < kPer / 2; ++i) {
-      const longlong2 x = __ldcs(v + i);
-      d[2 * i] = x.x;                       // raw bytes; rounded in the local pass
-      d[2 * i + 1] = x.y;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < kPer; ++i)
-      d[i] = (g0 + i < t1e) ? __ldcs(by + g0 + i) : 0;
-  }
-  // ---- heads: starts of non-empty traces inside [t0e, t1e) ----
-  if (tid == 0) n_heads_s = 0;
-  __syncthreads();
-  {
-    const bool first_is_head = P.off[tf] == t0e;
-    int64_t tb = first_is_head ? tf : int64_t(tf) + 1;
-    for (;;) {
-      const int64_t t = tb + tid;
-      bool head = false;
-      bool past = true;
-      int64_t a = 0;
-      if (t < P.n_traces) {
-        a = P.off[t];
-        past = a >= t1e;
-        head = !past && P.off[t + 1] > a;
+  for (int r = 0; r < kTile / 2 / kThreads; ++r) {
+    const int ch = tid + r * kThreads;
+    if (ch < nchunks) {
+      const uint32_t dst = sbase + uint32_t(ch * 16 + (ch >> 3) * 16);
+      const long long* src = by + t0e + 2 * ch;
+      if (t0e + 2 * ch + 1 < t1e) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+      } else {                                                    // odd tail: one event
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
       }
-      const unsigned hm = __ballot_sync(kFull, head);
-      int base = 0;
-      if (lane == 0 && hm) base = atomicAdd(&n_heads_s, __popc(hm));
-      base = __shfl_sync(kFull, base, 0);
-      if (head) {
-        const int k = base + __popc(hm & ((1u << lane) - 1u));
-        head_pos[k] = int32_t(a - t0e);
-        head_trace[k] = uint32_t(t);
-      }
-      // more traces may start in this tile iff the chunk's last one did not pass it
-      const int any_more = __syncthreads_or(tid == kThreads - 1 && !past);
-      if (!any_more) break;
-      tb += kThreads;
     }
   }
-  __syncthreads();
-  const int nh = n_heads_s;
-  // warps appended in arbitrary order: sort heads by position (few; insertion
-  // sort by one thread is fine when nh is small, else a simple parallel rank)
-  if (nh > 1) {
-    __shared__ int32_t tmp_pos[kTile];
-    __shared__ uint32_t tmp_tr[kTile];
-    for (int k = tid; k < nh; k += kThreads) { tmp_pos[k] = head_pos[k]; tmp_tr[k] = head_trace[k]; }
+}
+
+// K1a: persistent; tiles are staged in shared memory with coalesced cp.async
+// (16 B per thread per round), padded by 16 B every 128 B so that each
+// thread's 16-event (128 B) row reads back without bank conflicts; the next
+// tile is in flight while the current one is scanned (double buffer).
+__global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ bool wflag[kWarps];
+  __shared__ MonoR wagg[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kStage = kTile * 8 + kTile / 16 * 16;           // 36 KB per stage
+
+  int64_t c = blockIdx.x;
+  if (c < P.n_tiles) stage_tile(P, dsm, c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int k = 0; c < P.n_tiles; ++k, c += gridDim.x) {
+    unsigned char* cur_buf = dsm + (k & 1) * kStage;
+    const int64_t cn = c + gridDim.x;
+    if (cn < P.n_tiles) stage_tile(P, dsm + ((k + 1) & 1) * kStage, cn);
+    asm volatile("cp.async.commit_group;\n" ::);
+
+    const int64_t t0e = c * kTile;
+    const int64_t t1e = min(t0e + kTile, P.n_events);
+    const int rel0 = tid * kPer;
+    const int64_t g0 = t0e + rel0;
+    const int64_t left = t1e - g0;
+    const int nvalid = left <= 0 ? 0 : (left >= kPer ? kPer : int(left));
+    // which trace owns this thread's first event, and does a trace start in its row?
+    uint32_t tcur = 0;
+    int64_t end_cur = INT64_MAX;
+    bool head0 = false;
+    if (nvalid > 0) {
+      tcur = P.row_trace[c * kThreads + tid];
+      end_cur = P.off[tcur + 1];
+      head0 = P.off[tcur] == g0;
+    }
+    const bool any_head = __syncthreads_or(head0 || (nvalid > 0 && end_cur < g0 + nvalid));
+
+    asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
-    for (int k = tid; k < nh; k += kThreads) {
-      const int32_t p = tmp_pos[k];
-      int r = 0;
-      for (int q = 0; q < nh; ++q) r += tmp_pos[q] < p;   // positions are distinct
-      head_pos[r] = p;
-      head_trace[r] = tmp_tr[k];
-    }
-    __syncthreads();
-  }
-
-  // heads inside [rel0, rel0 + kPer)
-  const int rel0 = tid * kPer;
-  int h0 = 0;                               // first head index with pos >= rel0
-  {
-    int lo = 0, hi = nh;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (head_pos[mid] < rel0) lo = mid + 1; else hi = mid;
-    }
-    h0 = lo;
-  }
-  unsigned hb = 0;
-  for (int k = h0; k < nh && head_pos[k] < rel0 + kPer; ++k) hb |= 1u << (head_pos[k] - rel0);
-
-  // ---- thread-local segmented pass ----
-  Mono cur = mono_id(), first_piece = mono_id();
-  bool seen = false;
-  int hk = h0;                              // index of the next head in this thread
+    int64_t d[kPer];
+    {
+      const longlong2* row = reinterpret_cast<const longlong2*>(cur_buf + tid * 144);
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    if ((hb >> i) & 1u) {
-      if (!seen) {
-        first_piece = cur;
-        seen = true;
-      } else {
-        write_result(P, head_trace[hk - 1], cur);  // trace wholly inside this thread
+      for (int i = 0; i < kPer / 2; ++i) {
+        const longlong2 x = row[i];
+        d[2 * i] = x.x;
+        d[2 * i + 1] = x.y;
       }
-      ++hk;
-      cur = mono_id();
     }
-    if (g0 + i < t1e) {
-      const int64_t x = rounded_delta(d[i], P.unit_shift);
-      cur = combine(cur, Mono{x, x, g0 + i});
-    }
-  }
-  // ---- CTA exclusive segmented scan of (seen, cur) ----
-  bool f = seen;
-  Mono a = cur;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const Mono b = shfl_up_mono(a, o);
-    const bool fb = __shfl_up_sync(kFull, f, o);
-    if (lane >= o) {            // (fb, b) precedes (f, a)
-      Mono x = b;
-      bool fx = fb;
-      seg_combine(fx, x, f, a);
-      a = x;
-      f = fx;
-    }
-  }
-  if (lane == 31) { wflag[warp] = f; wagg[warp] = a; }
-  __syncthreads();
-  // carry into this warp: fold of warps before it
-  bool cf = false;
-  Mono cw = mono_id();
-  for (int w = 0; w < warp; ++w) seg_combine(cf, cw, wflag[w], wagg[w]);
-  // exclusive within warp
-  Mono ex = Mono{__shfl_up_sync(kFull, a.sum, 1), __shfl_up_sync(kFull, a.mx, 1),
-                 __shfl_up_sync(kFull, a.arg, 1)};
-  bool exf = __shfl_up_sync(kFull, f, 1);
-  if (lane == 0) { ex = mono_id(); exf = false; }
-  bool carry_f = cf;
-  Mono carry = cw;
-  seg_combine(carry_f, carry, exf, ex);     // carry = everything before this thread
+    __syncthreads();                          // the buffer is refilled next iteration
 
-  if (seen) {
-    const Mono done = combine(carry, first_piece);
-    if (carry_f) {
-      // the piece ending at this thread's first head started at a head in this tile
-      if (h0 > 0) write_result(P, head_trace[h0 - 1], done);
-    } else {
-      P.tile_first[c] = done;               // tile prefix piece (trace crossed in)
+    if (!any_head) {
+      // ===== fast path: the whole tile is one piece of one trace =====
+      int64_t run = 0, mx = kNeg;
+      int32_t arg = -1;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        if (i < nvalid) {
+          run += rounded_delta(d[i], P.unit_shift);
+          if (run > mx) { mx = run; arg = rel0 + i; }
+        }
+      }
+      int64_t incl = run;                     // warp exclusive prefix of run
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int64_t excl = incl - run;
+      int64_t v = mx == kNeg ? kNeg : excl + mx;
+      int32_t va = arg;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {          // argmax, earlier index on ties
+        const int64_t w = __shfl_xor_sync(kFull, v, o);
+        const int32_t wa = __shfl_xor_sync(kFull, va, o);
+        if (w > v || (w == v && wa < va && w != kNeg)) { v = w; va = wa; }
+      }
+      if (lane == 31) wagg[warp] = MonoR{incl, v, va, 0};
+      __syncthreads();
+      if (tid == 0) {
+        MonoR m = wagg[0];
+        for (int w = 1; w < kWarps; ++w) m = combine(m, wagg[w]);
+        const Mono g = to_global(m, t0e);
+        P.tile_first[c] = g;
+        P.tile_last[c] = g;
+      }
+      __syncthreads();
+      continue;
     }
-  }
-  // last thread with events owns the tile's tail piece
-  const int last_tid = int((t1e - t0e - 1) / kPer);
-  if (tid == last_tid) {
-    bool lf = carry_f;
-    Mono lm = carry;
-    seg_combine(lf, lm, seen, cur);
-    if (nh == 0) {
-      P.tile_first[c] = lm;                 // no head: the whole tile is one piece
-      P.tile_last[c] = lm;
-    } else {
-      const uint32_t tl = head_trace[nh - 1];
-      if (P.off[tl + 1] <= t1e) write_result(P, tl, lm);   // last trace ends in tile
-      else P.tile_last[c] = lm;
+
+    // ===== general path: segmented scan; pieces carry the trace of their head =====
+    MonoR cur = mono_id(), first_piece = mono_id();
+    bool seen = false;
+    int64_t run = 0;
+    int hnext = int(min(end_cur - g0, int64_t(kPer)));     // row offset of the next head
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (i < nvalid) {
+        const bool head = (i == 0) ? head0 : (i == hnext);
+        if (head) {
+          if (i > 0) {                        // step to the trace starting here (skip empties)
+            const int64_t pos = g0 + i;
+            ++tcur;
+            while (P.off[tcur + 1] == pos) ++tcur;
+            end_cur = P.off[tcur + 1];
+            hnext = int(min(end_cur - g0, int64_t(kPer)));
+          }
+          if (!seen) {
+            first_piece = cur;
+            seen = true;
+          } else {
+            write_result(P, cur.tr, cur.mx, t0e + cur.arg);   // trace wholly inside this row
+          }
+          cur = mono_id();
+          cur.tr = tcur;
+          run = 0;
+        }
+        run += rounded_delta(d[i], P.unit_shift);
+        cur.sum = run;
+        if (run > cur.mx) { cur.mx = run; cur.arg = rel0 + i; }
+      }
     }
+    // ---- CTA exclusive segmented scan of (seen, cur) ----
+    bool f = seen;
+    MonoR a = cur;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const MonoR b = shfl_up_mono(a, o);
+      const bool fb = __shfl_up_sync(kFull, f, o);
+      if (lane >= o) {          // (fb, b) precedes (f, a)
+        MonoR x = b;
+        bool fx = fb;
+        seg_combine(fx, x, f, a);
+        a = x;
+        f = fx;
+      }
+    }
+    if (lane == 31) { wflag[warp] = f; wagg[warp] = a; }
+    __syncthreads();
+    bool cf = false;
+    MonoR cw = mono_id();
+    for (int w = 0; w < warp; ++w) seg_combine(cf, cw, wflag[w], wagg[w]);
+    MonoR ex = shfl_up_mono(a, 1);
+    bool exf = __shfl_up_sync(kFull, f, 1);
+    if (lane == 0) { ex = mono_id(); exf = false; }
+    bool carry_f = cf;
+    MonoR carry = cw;
+    seg_combine(carry_f, carry, exf, ex);   // everything before this thread
+
+    if (seen) {
+      const MonoR done = combine(carry, first_piece);
+      if (carry_f) write_result(P, carry.tr, done.mx, t0e + done.arg);   // started at a head here
+      else P.tile_first[c] = to_global(done, t0e);   // prefix piece of a trace that crossed in
+    }
+    const int last_tid = int((t1e - t0e - 1) / kPer);   // owns the tile's tail piece
+    if (tid == last_tid) {
+      bool lf = carry_f;
+      MonoR lm = carry;
+      seg_combine(lf, lm, seen, cur);
+      if (P.off[lm.tr + 1] <= t1e) write_result(P, lm.tr, lm.mx, t0e + lm.arg);  // ends in tile
+      else P.tile_last[c] = to_global(lm, t0e);
+    }
+    __syncthreads();                          // wflag/wagg reused next tile
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 // K1b: fold pieces of traces that cross tile boundaries; empty traces -> zeros
@@ -284,8 +329,8 @@ __global__ void k_scan_combine(SParams P) {
   const int64_t ca = a / kTile, cb = (b - 1) / kTile;
   if (ca == cb) return;                     // finished by k_scan_tiles
   Mono m = P.tile_last[ca];
-  for (int64_t c = ca + 1; c <= cb; ++c) m = combine(m, P.tile_first[c]);
-  write_result(P, uint32_t(t), m);
+  for (int64_t c = ca + 1; c <= cb; ++c) m = combine_g(m, P.tile_first[c]);
+  write_result(P, uint32_t(t), m.mx, m.arg);
 }
 
 }  // namespace
@@ -296,7 +341,7 @@ static int64_t n_tiles_of(const xm_batch* b) { return (b->n_events + kTile - 1) 
 
 size_t scan_scratch_bytes(const xm_batch* b) {
   const int64_t nt = n_tiles_of(b);
-  return 256 + size_t(nt) * (4 + 2 * sizeof(Mono)) + 256;
+  return 256 + size_t(nt) * (2 * sizeof(Mono) + 4 * kThreads) + 256;
 }
 
 int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
@@ -314,13 +359,20 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
   s += size_t(P.n_tiles) * sizeof(Mono);
   P.tile_last = reinterpret_cast<Mono*>(s);
   s += size_t(P.n_tiles) * sizeof(Mono);
-  P.tile_trace = reinterpret_cast<uint32_t*>(s);
+  P.row_trace = reinterpret_cast<uint32_t*>(s);
   P.out = d_out;
   const int tb = 256;
   const int gt = int((b->n_traces + tb - 1) / tb);
   if (P.n_tiles > 0) {
-    k_tile_map<<<gt, tb, 0, st>>>(P);
-    k_scan_tiles<<<unsigned(P.n_tiles), kThreads, 0, st>>>(P);
+    const int dsm = 2 * (kTile * 8 + kTile / 16 * 16);       // two staged tiles, 72 KB
+    cudaError_t e = cudaFuncSetAttribute(k_scan_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+    if (e != cudaSuccess) return int(e);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(P.n_tiles, int64_t(sms) * 3);   // 3 CTAs/SM fit
+    k_row_map<<<int((b->n_traces * 32 + tb - 1) / tb), tb, 0, st>>>(P);
+    k_scan_tiles<<<unsigned(grid), kThreads, dsm, st>>>(P);
     *n_launches += 2;
   }
   k_scan_combine<<<gt > 0 ? gt : 1, tb, 0, st>>>(P);
