@@ -53,7 +53,9 @@ class Seg:
             yield (a, self.base + self.size - a)
 
 
-def simulate(bytes_, tag, capacity=UNLIMITED, strict=True):
+def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None):
+    """bases: optional segment base addresses in creation order (e.g. the real
+    cudaMalloc addresses torch got); default = bump addresses (reading Q4)."""
     segs = []
     where = {}     # id -> (seg, start, end, s, request)
     nxt = 0
@@ -91,7 +93,10 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True):
                     if reserved + need > capacity:
                         out["status"] = 1
                         break
-                g = Seg(nxt, need, st, small)
+                if bases is not None and out["n_seg_alloc"] < len(bases):
+                    g = Seg(bases[out["n_seg_alloc"]], need, st, small)
+                else:
+                    g = Seg(nxt, need, st, small)
                 nxt += need
                 segs.append(g)
                 reserved += need

@@ -1,0 +1,147 @@
+"""External pin (GPU box only): the oracle -- and the CUDA path through the
+C-ABI -- against the real PyTorch CUDACachingAllocator that the paper's
+Simulator follows (PAPER.md:257 footnote).
+
+Each trace is replayed in a fresh subprocess (clean allocator, no
+PYTORCH_CUDA_ALLOC_CONF) by tests/torch_replay.py. Compared: peak reserved
+bytes (the paper's M_peak), peak allocated block bytes (torch
+allocated_bytes.all.peak, reading Q2), segment counters, and the failing event
+under a finite capacity. This settles readings Q1 (strict large split), Q3
+(release all cached segments), Q5 (per-stream pools) against real torch.
+Real cudaMalloc addresses decide best-fit ties; the traces here are built so
+that the bump-address order used by the model is the real address order
+(segments are only created, never returned, except in the OOM cases).
+"""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle
+import paper_2510_21048_b200 as xm
+from workloads import concat, fuzz, hand, suites
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+MiB = 1 << 20
+
+
+def torch_replay_batch(batch, full=False):
+    """All traces of a workloads.Batch in one fresh process (cache emptied between).
+    Returns per-trace stats (and, if full, the per-event curve and pointers)."""
+    with tempfile.TemporaryDirectory() as d:
+        p, q = os.path.join(d, "t.npz"), os.path.join(d, "o.npz")
+        np.savez(p, bytes=batch.bytes, tag=batch.tag, off=batch.off, capacity=batch.capacity)
+        r = subprocess.run([sys.executable, os.path.join(HERE, "torch_replay.py"), p, q],
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        o = np.load(q)
+        stats = json.loads(str(o["stats"]))
+        return (stats, o["curve"], o["ptr"]) if full else stats
+
+
+def torch_replay(by, tg, cap=oracle.UNLIMITED):
+    from workloads.trace import from_arrays
+    return torch_replay_batch(from_arrays(by, tg, cap))[0]
+
+
+def _gpu(batch):
+    tr = xm.load_traces(batch.bytes, batch.tag, batch.off)
+    cap = batch.capacity if (batch.capacity != oracle.UNLIMITED).any() else None
+    h, _ = xm.peaks(xm.simulate_batch(tr.to_device(capacity=cap)))
+    return h
+
+
+FIELDS = ["peak_reserved", "peak_allocated_blk", "n_seg_alloc", "max_live_segments"]
+
+HAND = ["H1a", "H1b", "H1d", "H2a", "H2b", "H3-early", "H3-late", "H4-early", "H4-late",
+        "H5-one", "H5-two", "H6", "S251", "S252", "S260", "S261", "S262", "P169", "P654",
+        "P654-10MiB"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+
+
+def test_hand_traces_match_real_torch():
+    named = hand.all_named()
+    b = concat([named[k] for k in HAND])
+    reals = torch_replay_batch(b)
+    o = oracle.simulate_batch(b)
+    g = _gpu(b)
+    for t, name in enumerate(HAND):
+        for f in FIELDS:
+            assert int(o[f][t]) == reals[t][f], (name, f, int(o[f][t]), reals[t][f])
+            assert int(g[f][t]) == reals[t][f], (name, f)
+
+
+def test_capacity_reclaim_oom_matches_real_torch():
+    """SPEC.md:253 / H7 scaled to a real device (a 2 MiB capacity is below what
+    a CUDA context needs): six 1 MiB tensors fill three 2 MiB small segments,
+    all are freed (cached), then a 30 GiB request under a 20 GiB capacity makes
+    the device level refuse; both levels release all three cached segments
+    (reading Q3) and report OOM at event 12 (PAPER.md:260 (v))."""
+    from workloads.trace import TraceBuilder
+    G = 1 << 30
+    tb = TraceBuilder()
+    for i in range(6):
+        tb.alloc(i, MiB)            # two per 2 MiB small segment
+    for i in range(6):
+        tb.free(i)
+    tb.alloc(100, 30 * G)           # needs a 30 GiB segment: reclaim, then OOM
+    tb.end_trace(capacity=20 * G)
+    b = tb.build()
+    real = torch_replay(b.bytes, b.tag, 20 * G)
+    o, _ = oracle.simulate_trace(b.bytes, b.tag, 20 * G)
+    assert real["fail_idx"] == o["events_done"] == 12
+    assert o["status"] == 1 and real["num_ooms"] >= 1
+    assert o["n_seg_release"] == real["n_seg_release"] == 3
+    assert o["peak_reserved"] == real["peak_reserved"]
+
+
+def test_training_traces_match_real_torch_given_its_addresses():
+    """Realistic training-iteration traces (configs[0..2]). Real cudaMalloc
+    returns segment addresses in no fixed order, and torch breaks best-fit ties
+    between equal free blocks by address; the model's reading Q4 uses creation
+    order (SPEC D2). So: (a) injecting torch's own segment addresses into the
+    independent gap model (tests/bruteforce.py) must reproduce torch's
+    per-event reserved AND allocated curves exactly -- this pins every rule of
+    the model against the real allocator; (b) with bump addresses the gap model,
+    the oracle and the CUDA path agree exactly (pinned elsewhere), and the
+    peak differs from torch only through ties (reported, not asserted)."""
+    import bruteforce
+    b = concat([suites.config1(), suites.config2().subset([0, 15, 31]),
+                suites.config3().subset([0, 21, 43])])
+    stats, curve, ptr = torch_replay_batch(b, full=True)
+    for t in range(b.n_traces):
+        a, z = int(b.off[t]), int(b.off[t + 1])
+        by, tg = b.bytes[a:z], b.tag[a:z]
+        res = curve[a:z, 1]
+        grew = np.flatnonzero(res > np.concatenate([[0], res[:-1]]))
+        bases = [int(ptr[a + i]) for i in grew]          # segment bases, creation order
+        _, bc = bruteforce.simulate(by, tg, bases=bases)
+        bc = np.asarray(bc, np.int64)
+        assert (bc[:, 2] == res).all(), (b.names[t], "reserved curve")
+        assert (bc[:, 1] == curve[a:z, 0]).all(), (b.names[t], "allocated curve")
+        assert int(bc[:, 2].max()) == stats[t]["peak_reserved"]
+
+
+def test_fuzz_traces_match_real_torch():
+    """Random sequences (SPEC.md:508 shape, smaller). Ties between equal free
+    blocks are decided by real addresses in torch; report agreement, require it
+    on peak_reserved for the large majority."""
+    c = fuzz.spec1_corpus(40, 300, salt=77)
+    reals = torch_replay_batch(c)
+    o = oracle.simulate_batch(c)
+    agree = 0
+    for t in range(c.n_traces):
+        agree += all(int(o[f][t]) == reals[t][f] for f in FIELDS)
+    assert agree >= int(0.9 * c.n_traces), f"{agree}/{c.n_traces} traces agree with real torch"
