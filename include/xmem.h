@@ -80,9 +80,10 @@ typedef struct {
   uint32_t large_split_strict; /* 1 (default): large split iff remainder >     */
                                /* small_size (torch); 0: >=       */
   uint32_t mode;               /* XM_FULL (default) or XM_ALLOCATED_ONLY        */
-  uint32_t smem_per_warp;      /* shared-memory state budget per warp in bytes; */
-                               /* 0 = choose automatically                      */
-  uint32_t warps_per_cta;      /* 0 = default (4)                               */
+  uint32_t smem_per_warp;      /* caps the per-CTA shared-memory heap at        */
+                               /* smem_per_warp * warps_per_cta bytes (tests);  */
+                               /* 0 = the whole 227 KB                          */
+  uint32_t warps_per_cta;      /* 0 = default (12)                              */
 } xm_config;
 
 /*
@@ -143,6 +144,13 @@ typedef struct {
   int64_t n_events;
   uint32_t max_ids;         /* max over n_ids                                        */
   uint32_t max_events;      /* max trace length                                      */
+  uint64_t* curve;          /* optional DEVICE output [n_events][3] or NULL: the     */
+                            /* memory-usage curve ("the full series can */
+                            /* optionally be output"): after event i,   */
+                            /* {allocated (sum of rounded requests), allocated block */
+                            /* bytes, reserved bytes}. Rows of events a trace did not*/
+                            /* process (after a simulated OOM) are left untouched.   */
+                            /* XM_FULL mode only.                                    */
 } xm_batch;
 
 /* Fill *cfg with the defaults above. */

@@ -58,7 +58,7 @@ class _Batch(ctypes.Structure):
                 ("n_ids", ctypes.c_void_p), ("order", ctypes.c_void_p),
                 ("capacity", ctypes.c_void_p), ("n_traces", ctypes.c_int64),
                 ("n_events", ctypes.c_int64), ("max_ids", ctypes.c_uint32),
-                ("max_events", ctypes.c_uint32)]
+                ("max_events", ctypes.c_uint32), ("curve", ctypes.c_void_p)]
 
 
 class _Summary(ctypes.Structure):
@@ -193,12 +193,12 @@ class DeviceBatch:
     max_events: int
     _scratch: Dict = field(default_factory=dict)
 
-    def c(self) -> _Batch:
+    def c(self, curve=None) -> _Batch:
         def p(x):
             return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
         return _Batch(p(self.bytes), p(self.tag), p(self.off), p(self.n_ids), p(self.order),
                       p(self.capacity), self.n_traces, self.n_events, self.max_ids,
-                      self.max_events)
+                      self.max_events, p(curve))
 
 
 def load_traces(bytes_: np.ndarray, tag: np.ndarray, off: np.ndarray) -> Traces:
@@ -229,11 +229,15 @@ def scratch_bytes(dev: DeviceBatch, cfg: Config = Config()) -> int:
     return int(lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(c)))
 
 
-def simulate_batch(dev: DeviceBatch, cfg: Config = Config(), stream=None, out=None):
+def simulate_batch(dev: DeviceBatch, cfg: Config = Config(), stream=None, out=None, curve=None):
     """xm_simulate_batch on the current (or given) torch stream.
-    Returns a uint8 device tensor [n_traces, 64] holding xm_result records."""
+    Returns a uint8 device tensor [n_traces, 64] holding xm_result records.
+    curve: optional int64 device tensor [n_events, 3] receiving the memory-usage
+    curve (allocated, allocated blocks, reserved bytes after each event)."""
     import torch
-    b, c = dev.c(), cfg.c()
+    if curve is not None:
+        assert curve.dtype == torch.int64 and curve.shape == (dev.n_events, 3) and curve.is_contiguous()
+    b, c = dev.c(curve), cfg.c()
     need = int(lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(c)))
     key = (cfg.mode, cfg.smem_per_warp, cfg.warps_per_cta)
     scr = dev._scratch.get(key)

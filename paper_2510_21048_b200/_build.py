@@ -9,7 +9,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 DEBUG = bool(os.environ.get("XM_DEBUG"))
-LIB = os.path.join(PKG, "libxmem_debug.so" if DEBUG else "libxmem.so")
+TIMING = bool(os.environ.get("XM_TIMING"))
+LIB = os.path.join(PKG, "libxmem_debug.so" if DEBUG else ("libxmem_timing.so" if TIMING else "libxmem.so"))
 SOURCES = ["loader.cpp", "capi.cu", "replay.cu", "scan.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -30,8 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     bdir = os.path.join(PKG, "build")
     os.makedirs(bdir, exist_ok=True)
     for src in SOURCES:
-        obj = os.path.join(bdir, src + (".dbg.o" if DEBUG else ".o"))
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), "-std=c++17", "-Xcompiler", "-fPIC",
+        obj = os.path.join(bdir, src + (".dbg.o" if DEBUG else (".tim.o" if TIMING else ".o")))
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), *(["-DXM_TIMING"] if TIMING else []), "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src),
                "-o", obj]
         if src.endswith(".cu"):

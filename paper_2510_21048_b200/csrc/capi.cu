@@ -116,6 +116,7 @@ extern "C" int xm_simulate_batch(const xm_batch* b, const xm_config* cfg, void* 
   if (cfg->mode == XM_ALLOCATED_ONLY) {
     if (cfg->capacity != XM_UNLIMITED || b->capacity)
       return set_error(XM_EINVAL, "XM_ALLOCATED_ONLY requires unlimited capacity");
+    if (b->curve) return set_error(XM_EINVAL, "the memory curve needs XM_FULL");
     if (scratch_bytes < scan_scratch_bytes(b)) return set_error(XM_ENOMEM, "scratch too small");
     e = launch_scan(b, u, d_scratch, scratch_bytes, d_out, stream, &launch_counter());
   } else {

@@ -144,3 +144,25 @@ def test_summary_eq1():
     r2 = xm.simulate_batch(tr2.to_device())
     assert xm.peaks(r2, capacity_for_eq1=196 << 20)[1]["n_predicted_oom"] == 0
     assert xm.peaks(r2, capacity_for_eq1=(196 << 20) - 1)[1]["n_predicted_oom"] == 1
+
+
+def test_memory_curve_output():
+    """per-event (allocated, allocated blocks, reserved) rows
+    (PAPER.md:263 "the full series can optionally be output"; SPEC.md:223)
+    equal the oracle's curve for every processed event."""
+    b = concat([fuzz.spec1_corpus(60, 600, salt=41), fuzz.capacity_corpus(40, 500, salt=42),
+                suites.config1(), hand.h7(), fuzz.fragmentation_stress()])
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    dev = tr.to_device(capacity=b.capacity)
+    curve = torch.zeros((b.n_events, 3), dtype=torch.int64, device="cuda")
+    res = xm.simulate_batch(dev, xm.Config(), curve=curve)
+    h, _ = xm.peaks(res)
+    cv = curve.cpu().numpy().view(np.uint64)
+    for t in range(b.n_traces):
+        by, tg = b.trace(t)
+        o, oc = oracle.simulate_trace(by, tg, int(b.capacity[t]), curve=True)
+        n = o["events_done"]
+        a = int(b.off[t])
+        assert int(h["events_done"][t]) == n
+        assert (cv[a:a + n] == oc[:n]).all(), (b.names[t], np.flatnonzero((cv[a:a + n] != oc[:n]).any(1))[:3])
+        assert (cv[a + n:int(b.off[t + 1])] == 0).all()      # unprocessed rows untouched

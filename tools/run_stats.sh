@@ -1,1 +1,1 @@
-python tools/k2_stats.py cfg4 8,10,12,16 2>&1 | tail -4
+python tools/k2_stats.py cfg4 8,12,16 2>&1 | tail -3
