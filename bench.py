@@ -310,7 +310,7 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            _, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
+            h_e2e, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
         dt = (time.perf_counter() - t0) / args.steps
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
@@ -320,7 +320,9 @@ def main():
             + 8 * batch.n_traces + (8 * batch.n_traces if has_cap else 0)
         e2e = {"value": done / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(64 * batch.n_traces), "ms_per_step": dt * 1e3,
-               "api": "xm_simulate_host (pinned host traces -> device -> host results)"}
+               "api": "xm_simulate_host (pinned host traces -> device -> host results; "
+                      "upload streamed in longest-first chunks overlapping the replay)",
+               "results_equal_device_path": bool((h_e2e == h).all())}
     clocks = sampler.stop() if sampler else None
 
     # ---- roofline of the dominant kernel (k_replay): algorithmic bytes / launch time

@@ -132,25 +132,30 @@ typedef struct xm_traces xm_traces;
 
 /* Device view of a batch, as passed to xm_simulate_batch. All pointers are   */
 /* DEVICE memory owned by the caller, laid out exactly as xm_traces_views    */
-/* returns them (normally copied there by the caller).                        */
+/* returns them (normally copied there by the caller). Traces are STORED in   */
+/* processing order: the kernel starts stored trace 0 first, then 1, ...;     */
+/* xm_load_traces stores them longest-first (LPT). Results stay in the        */
+/* caller's order through `order`.                                            */
 typedef struct {
   const int64_t* bytes;     /* [n_events] signed request bytes: +req alloc, -req free */
   const uint32_t* tag;      /* [n_events] dense id (bits 0-26) | stream << 28         */
-  const int64_t* off;       /* [n_traces+1] trace t = events [off[t], off[t+1])      */
-  const uint32_t* n_ids;    /* [n_traces] dense id space of each trace (= max live)  */
-  const uint32_t* order;    /* [n_traces] processing order, longest first (LPT)      */
-  const uint64_t* capacity; /* [n_traces] per-trace capacity or NULL (cfg->capacity) */
+  const int64_t* off;       /* [n_traces+1] stored trace i = events [off[i], off[i+1])*/
+  const uint32_t* n_ids;    /* [n_traces] dense id space of stored trace i (max live) */
+  const uint32_t* order;    /* [n_traces] caller index of stored trace i (a          */
+                            /* permutation): its result goes to d_out[order[i]]      */
+  const uint64_t* capacity; /* [n_traces] per-trace capacity in CALLER order, or NULL*/
+                            /* (cfg->capacity for all)                               */
   int64_t n_traces;
   int64_t n_events;
   uint32_t max_ids;         /* max over n_ids                                        */
   uint32_t max_events;      /* max trace length                                      */
   uint64_t* curve;          /* optional DEVICE output [n_events][3] or NULL: the     */
                             /* memory-usage curve ("the full series can */
-                            /* optionally be output"): after event i,   */
-                            /* {allocated (sum of rounded requests), allocated block */
-                            /* bytes, reserved bytes}. Rows of events a trace did not*/
-                            /* process (after a simulated OOM) are left untouched.   */
-                            /* XM_FULL mode only.                                    */
+                            /* optionally be output"): after stored     */
+                            /* event e, {allocated (sum of rounded requests),        */
+                            /* allocated block bytes, reserved bytes}. Rows of events*/
+                            /* a trace did not process (after a simulated OOM) are   */
+                            /* left untouched. XM_FULL mode only.                    */
 } xm_batch;
 
 /* Fill *cfg with the defaults above. */
@@ -160,9 +165,11 @@ void xm_config_default(xm_config* cfg);
  * Validate and pack a batch of host traces (SPEC.md:156-163 ordered sequence;
  * signed-bytes convention SPEC.md:27).
  *   bytes[n_events], tag[n_events], off[n_traces+1]: HOST, caller-owned, read only.
- *   Array order is replay order (reading Q6). Block ids may be any 28-bit values;
- *   they are renumbered densely (an id is reused after its free) so each trace's
- *   id space is its maximum number of live blocks.
+ *   Array order within a trace is replay order (reading Q6). Block ids may be
+ *   any 28-bit values; they are renumbered densely (an id is reused after its
+ *   free) so each trace's id space is its maximum number of live blocks.
+ *   The packed copy stores the traces longest-first (ties in caller order);
+ *   see xm_batch for how stored and caller indices relate.
  * Rejects (XM_EINVAL, *bad_trace = first offending trace): off not monotone or
  *   off[0] != 0; a zero-byte event (reading Q8); |bytes| >=
  *   XM_MAX_REQUEST (XM_ERANGE); an alloc of a live id; a free of a
@@ -216,8 +223,12 @@ int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_summary* h_
 /*
  * End-to-end entry point with HOST buffers: copies the packed batch to the
  * DEVICE workspace d_ws (>= xm_host_ws_bytes()), replays it, copies the
- * results to h_out[n_traces] (HOST) and synchronises `stream`.
- *   capacity: HOST [n_traces] per-trace capacities or NULL.
+ * results to h_out[n_traces] (HOST, caller order) and synchronises `stream`.
+ *   capacity: HOST [n_traces] per-trace capacities (caller order) or NULL.
+ * In XM_FULL mode the event upload is streamed: chunks of whole traces, in
+ * stored (longest-first) order, go over a library-owned copy stream while the
+ * replay kernel already runs on `stream`, each trace starting once its chunk
+ * is resident (env XM_NO_STREAM=1 copies everything first, for comparison).
  */
 size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg);
 int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_config* cfg,

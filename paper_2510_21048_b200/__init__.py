@@ -132,7 +132,8 @@ def _np_ptr(a: np.ndarray):
 
 
 class Traces:
-    """A validated, renumbered, packed host batch (xm_traces, page-locked)."""
+    """A validated, renumbered, packed host batch (xm_traces, page-locked),
+    stored in processing (longest-first) order; results stay in caller order."""
 
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
@@ -156,6 +157,16 @@ class Traces:
         self.off = view(ptrs[2], np.int64, self.n_traces + 1)
         self.n_ids = view(ptrs[3], np.uint32, self.n_traces)
         self.order = view(ptrs[4], np.uint32, self.n_traces)
+        # the batch is STORED longest-first: stored trace i is the caller's
+        # trace order[i], its events are [off[i], off[i+1]); pos[t] = i
+        self.pos = np.empty(self.n_traces, np.int64)
+        self.pos[self.order.astype(np.int64)] = np.arange(self.n_traces)
+
+    def span(self, t: int):
+        """Event range [a, b) of the caller's trace t in the stored arrays
+        (and in a memory-curve output)."""
+        i = int(self.pos[t])
+        return int(self.off[i]), int(self.off[i + 1])
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -233,7 +244,8 @@ def simulate_batch(dev: DeviceBatch, cfg: Config = Config(), stream=None, out=No
     """xm_simulate_batch on the current (or given) torch stream.
     Returns a uint8 device tensor [n_traces, 64] holding xm_result records.
     curve: optional int64 device tensor [n_events, 3] receiving the memory-usage
-    curve (allocated, allocated blocks, reserved bytes after each event)."""
+    curve (allocated, allocated blocks, reserved bytes after each event), rows
+    in stored event order (Traces.span(t) gives trace t's rows)."""
     import torch
     if curve is not None:
         assert curve.dtype == torch.int64 and curve.shape == (dev.n_events, 3) and curve.is_contiguous()

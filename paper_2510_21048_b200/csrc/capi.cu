@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -101,8 +102,9 @@ extern "C" size_t xm_scratch_bytes(const xm_batch* b, const xm_config* cfg) {
   return plan_replay(b, cfg).scratch_bytes;
 }
 
-extern "C" int xm_simulate_batch(const xm_batch* b, const xm_config* cfg, void* d_scratch,
-                                 size_t scratch_bytes, xm_result* d_out, void* stream) {
+// ready: streamed-input counter (xm_simulate_host) or null
+static int simulate(const xm_batch* b, const xm_config* cfg, void* d_scratch, size_t scratch_bytes,
+                    xm_result* d_out, void* stream, const uint32_t* ready) {
   launch_counter() = 0;
   if (!cfg) return set_error(XM_EINVAL, "null config");
   int rc = check_batch(b);
@@ -117,18 +119,24 @@ extern "C" int xm_simulate_batch(const xm_batch* b, const xm_config* cfg, void* 
     if (cfg->capacity != XM_UNLIMITED || b->capacity)
       return set_error(XM_EINVAL, "XM_ALLOCATED_ONLY requires unlimited capacity");
     if (b->curve) return set_error(XM_EINVAL, "the memory curve needs XM_FULL");
+    if (ready) return set_error(XM_EINVAL, "streamed input needs XM_FULL");
     if (scratch_bytes < scan_scratch_bytes(b)) return set_error(XM_ENOMEM, "scratch too small");
     e = launch_scan(b, u, d_scratch, scratch_bytes, d_out, stream, &launch_counter());
   } else {
     ReplayPlan plan = plan_replay(b, cfg);
     if (scratch_bytes < plan.scratch_bytes)
       return set_error(XM_ENOMEM, "scratch smaller than xm_scratch_bytes()");
-    e = launch_replay(b, cfg, u, plan, d_scratch, d_out, stream, &launch_counter());
+    e = launch_replay(b, cfg, u, plan, d_scratch, d_out, stream, &launch_counter(), ready);
   }
   if (e != 0)
     return set_error(XM_ECUDA, std::string("launch failed: ") + cudaGetErrorString(cudaError_t(e)));
   clear_error();
   return XM_OK;
+}
+
+extern "C" int xm_simulate_batch(const xm_batch* b, const xm_config* cfg, void* d_scratch,
+                                 size_t scratch_bytes, xm_result* d_out, void* stream) {
+  return simulate(b, cfg, d_scratch, scratch_bytes, d_out, stream, nullptr);
 }
 
 extern "C" int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_summary* h_sum,
@@ -172,7 +180,7 @@ extern "C" int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_
 
 namespace {
 struct HostLayout {
-  size_t bytes, tag, off, n_ids, order, cap, out, scratch, total;
+  size_t bytes, tag, off, n_ids, order, cap, out, ready, scratch, total;
 };
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -186,6 +194,7 @@ HostLayout host_layout(const xm_traces_info& I, const xm_config* cfg, bool with_
   L.order = p; p += al(sizeof(uint32_t) * I.n_traces);
   L.cap = p; p += with_cap ? al(sizeof(uint64_t) * I.n_traces) : 0;
   L.out = p; p += al(sizeof(xm_result) * I.n_traces);
+  L.ready = p; p += 256;
   L.scratch = p;
   xm_batch b{};
   b.n_traces = I.n_traces;
@@ -196,6 +205,49 @@ HostLayout host_layout(const xm_traces_info& I, const xm_config* cfg, bool with_
   L.total = p;
   return L;
 }
+
+// Per-thread copy stream + events of the streamed host entry point (created
+// on first use per device and kept for the thread's lifetime).
+struct Pipe {
+  int dev = -1;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t start = nullptr, copied = nullptr;
+};
+thread_local Pipe g_pipe;
+
+cudaError_t get_pipe(Pipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  Pipe& p = g_pipe;
+  if (p.dev != dev) {
+    Pipe q;
+    q.dev = dev;
+    if ((e = cudaStreamCreateWithFlags(&q.cs, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&q.start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&q.copied, cudaEventDisableTiming)) != cudaSuccess) return e;
+    p = q;   // a previous device's objects are leaked, not destroyed under another context
+  }
+  *out = &p;
+  return cudaSuccess;
+}
+
+// cuStreamWriteValue32 (driver API, a stream-ordered 4-byte write with
+// memory-barrier semantics: the writes of earlier copies in the stream are
+// visible before it), resolved at run time so that libxmem needs no -lcuda.
+typedef int (*WriteValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<WriteValue32Fn>(f);
+  }();
+  return fn;
+}
 }  // namespace
 
 extern "C" size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg) {
@@ -203,6 +255,15 @@ extern "C" size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg) {
   return host_layout(traces_info(tr), cfg, true).total;
 }
 
+// Streamed end-to-end replay. The packed batch is stored longest-first
+// (xm_load_traces), so the upload is cut into chunks of whole traces in that
+// order: the metadata goes first on `stream`, the event chunks follow on a
+// second (copy) stream, each chunk followed by a stream-ordered write of the
+// number of stored traces now resident, and the replay kernel, launched on
+// `stream` without waiting for the copies, starts each trace as soon as its
+// chunk has landed (wait_ready in replay.cu). The H2D transfer thereby
+// overlaps the replay instead of preceding it. XM_ALLOCATED_ONLY (K1 reads the
+// batch as one flat array) copies everything first.
 extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
                                 const xm_config* cfg, void* d_ws, size_t ws_bytes,
                                 xm_result* h_out, void* stream) {
@@ -210,18 +271,55 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   const xm_traces_info I = traces_info(tr);
   const HostLayout L = host_layout(I, cfg, true);
   if (ws_bytes < L.total) return set_error(XM_ENOMEM, "xm_simulate_host: workspace too small");
+  if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(d_ws);
   cudaError_t e = cudaSuccess;
-  auto cp = [&](size_t o, const void* src, size_t n) {
-    if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, st);
+  auto cp = [&](size_t o, const void* src, size_t n, cudaStream_t s) {
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, s);
   };
-  cp(L.bytes, I.bytes, sizeof(int64_t) * I.n_events);
-  cp(L.tag, I.tag, sizeof(uint32_t) * I.n_events);
-  cp(L.off, I.off, sizeof(int64_t) * (I.n_traces + 1));
-  cp(L.n_ids, I.n_ids, sizeof(uint32_t) * I.n_traces);
-  cp(L.order, I.order, sizeof(uint32_t) * I.n_traces);
-  if (capacity) cp(L.cap, capacity, sizeof(uint64_t) * I.n_traces);
+  const bool streamed = cfg->mode == XM_FULL && I.n_chunks > 0 && !std::getenv("XM_NO_STREAM");
+  cp(L.off, I.off, sizeof(int64_t) * (I.n_traces + 1), st);
+  cp(L.n_ids, I.n_ids, sizeof(uint32_t) * I.n_traces, st);
+  cp(L.order, I.order, sizeof(uint32_t) * I.n_traces, st);
+  if (capacity) cp(L.cap, capacity, sizeof(uint64_t) * I.n_traces, st);
+  uint32_t* ready = reinterpret_cast<uint32_t*>(w + L.ready);
+  if (!streamed) {
+    cp(L.bytes, I.bytes, sizeof(int64_t) * I.n_events, st);
+    cp(L.tag, I.tag, sizeof(uint32_t) * I.n_events, st);
+  } else {
+    Pipe* pp = nullptr;
+    if (e == cudaSuccess) e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = get_pipe(&pp);
+    // the copy stream starts after everything already queued on `stream`
+    // (earlier users of this workspace, the counter reset)
+    if (e == cudaSuccess) e = cudaEventRecord(pp->start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, pp->start, 0);
+    const WriteValue32Fn wv = write_value32();
+    int64_t ev0 = 0;
+    for (int c = 0; c < I.n_chunks && e == cudaSuccess; ++c) {
+      // chunk ends are rounded up to 32 events (>= 128 B of each array) so no
+      // cache sector holds events of two chunks
+      int64_t ev1 = I.off[I.chunk_end[c]];
+      if (c + 1 < I.n_chunks) ev1 = std::min<int64_t>(I.n_events, (ev1 + 31) & ~int64_t(31));
+      else ev1 = I.n_events;
+      if (ev1 > ev0) {
+        cp(L.bytes + sizeof(int64_t) * ev0, I.bytes + ev0, sizeof(int64_t) * (ev1 - ev0), pp->cs);
+        cp(L.tag + sizeof(uint32_t) * ev0, I.tag + ev0, sizeof(uint32_t) * (ev1 - ev0), pp->cs);
+        ev0 = ev1;
+      }
+      if (e != cudaSuccess) break;
+      if (wv) {
+        if (wv(pp->cs, reinterpret_cast<unsigned long long>(ready), I.chunk_end[c], 0) != 0)
+          e = cudaErrorUnknown;
+      } else {
+        cp(L.ready, I.chunk_end + c, sizeof(uint32_t), pp->cs);
+      }
+    }
+    // every copy and counter write is queued before the kernel that waits on
+    // them is launched
+    if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
+  }
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
   xm_batch b{};
   b.bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
@@ -235,7 +333,15 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   b.max_ids = I.max_ids;
   b.max_events = I.max_events;
   xm_result* d_out = reinterpret_cast<xm_result*>(w + L.out);
-  int rc = xm_simulate_batch(&b, cfg, w + L.scratch, L.total - L.scratch, d_out, stream);
+  int rc = simulate(&b, cfg, w + L.scratch, L.total - L.scratch, d_out, stream,
+                    streamed ? ready : nullptr);
+  // `stream` resumes (result download, the caller's later work) only after
+  // the copies too, also when the launch failed
+  if (streamed) {
+    const cudaError_t e2 = cudaStreamWaitEvent(st, g_pipe.copied, 0);
+    if (!rc && e2 != cudaSuccess)
+      return set_error(XM_ECUDA, std::string("stream wait: ") + cudaGetErrorString(e2));
+  }
   if (rc) return rc;
   return xm_peaks(d_out, I.n_traces, h_out, nullptr, XM_UNLIMITED, stream);
 }

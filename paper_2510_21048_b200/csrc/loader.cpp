@@ -5,8 +5,8 @@
 // of a non-live id or of the wrong size S:258), renumbers block ids densely so a
 // trace's id space equals its maximum number of live blocks (the device keeps
 // one state record per id), and computes the longest-first processing order
-// the persistent replay kernel pulls work from. Traces are processed in
-// parallel on host threads. None of the allocator arithmetic lives here.
+// the persistent replay kernel pulls work from, storing the traces in that
+// order. Traces are processed in parallel on host threads. None of the allocator arithmetic lives here.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -30,6 +30,8 @@ struct xm_traces {
   uint32_t* n_ids = nullptr;
   uint32_t* order = nullptr;
   uint32_t max_ids = 0, max_events = 0;
+  uint32_t* chunk_end = nullptr;   // [kUploadChunks] pinned, see xm_simulate_host
+  int n_chunks = 0;
   std::vector<void*> blocks;
   std::vector<bool> pinned;
 };
@@ -147,39 +149,54 @@ extern "C" int xm_load_traces(const int64_t* bytes, const uint32_t* tag, const i
   tr->off = (int64_t*)host_alloc(tr, sizeof(int64_t) * (n_traces + 1));
   tr->n_ids = (uint32_t*)host_alloc(tr, sizeof(uint32_t) * n_traces);
   tr->order = (uint32_t*)host_alloc(tr, sizeof(uint32_t) * n_traces);
-  if (!tr->bytes || !tr->tag || !tr->off || !tr->n_ids || !tr->order) {
+  tr->chunk_end = (uint32_t*)host_alloc(tr, sizeof(uint32_t) * xm_internal::kUploadChunks);
+  if (!tr->bytes || !tr->tag || !tr->off || !tr->n_ids || !tr->order || !tr->chunk_end) {
     xm_free_traces(tr);
     return set_error(XM_ENOMEM, "xm_load_traces: out of host memory");
   }
-  std::memcpy(tr->off, off, sizeof(int64_t) * (n_traces + 1));
+  // storage order = processing order: longest first (LPT), stable (ties keep
+  // caller order). order[i] = caller index of stored trace i; off is the
+  // storage prefix sum. Storing the longest traces first lets the host entry
+  // point stream the batch to the device in chunks the kernel starts on as
+  // they land (xm_simulate_host).
+  for (int64_t i = 0; i < n_traces; ++i) tr->order[i] = uint32_t(i);
+  std::stable_sort(tr->order, tr->order + n_traces, [&](uint32_t a, uint32_t b) {
+    return off[a + 1] - off[a] > off[b + 1] - off[b];
+  });
+  tr->off[0] = 0;
+  for (int64_t i = 0; i < n_traces; ++i) {
+    const uint32_t t = tr->order[i];
+    tr->off[i + 1] = tr->off[i] + (off[t + 1] - off[t]);
+  }
+  const int64_t* soff = tr->off;
 
-  // parallel over traces: contiguous chunks of roughly equal event counts
+  // parallel over stored traces: contiguous ranges of roughly equal event counts
   unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   int nth = int(std::min<int64_t>(hw, std::max<int64_t>(1, E / 65536)));
   nth = std::max(1, std::min<int>(nth, int(std::max<int64_t>(1, n_traces))));
+  // first_bad = the smallest CALLER index of an invalid trace
   std::atomic<int64_t> first_bad{INT64_MAX};
   std::vector<int> codes(nth, XM_OK);
   std::vector<const char*> msgs(nth, nullptr);
-  std::vector<int64_t> bads(nth, -1);
-  // chunk boundaries must be disjoint: compute them once
+  std::vector<int64_t> bads(nth, INT64_MAX);
   std::vector<int64_t> bounds(nth + 1);
   bounds[0] = 0;
   for (int k = 1; k < nth; ++k)
-    bounds[k] = std::max(bounds[k - 1], int64_t(std::lower_bound(off, off + n_traces, E * k / nth) - off));
+    bounds[k] = std::max(bounds[k - 1], int64_t(std::lower_bound(soff, soff + n_traces, E * k / nth) - soff));
   bounds[nth] = n_traces;
   auto work2 = [&](int k) {
     Renumberer R;
-    for (int64_t t = bounds[k]; t < bounds[k + 1]; ++t) {
-      if (t >= first_bad.load(std::memory_order_relaxed)) return;
-      int64_t a = off[t], n = off[t + 1] - a;
-      std::memcpy(tr->bytes + a, bytes + a, sizeof(int64_t) * n);
+    for (int64_t i = bounds[k]; i < bounds[k + 1]; ++i) {
+      const int64_t t = tr->order[i];
+      if (t >= first_bad.load(std::memory_order_relaxed)) continue;
+      const int64_t a = off[t], n = off[t + 1] - a, d = soff[i];
+      std::memcpy(tr->bytes + d, bytes + a, sizeof(int64_t) * n);
       const char* m = nullptr;
-      int rc = R.run(bytes + a, tag + a, n, tr->tag + a, tr->n_ids + t, &m);
+      int rc = R.run(bytes + a, tag + a, n, tr->tag + d, tr->n_ids + i, &m);
       if (rc) {
-        codes[k] = rc; msgs[k] = m; bads[k] = t;
+        if (t < bads[k]) { codes[k] = rc; msgs[k] = m; bads[k] = t; }
         int64_t cur = first_bad.load();
         while (t < cur && !first_bad.compare_exchange_weak(cur, t)) {}
-        return;
       }
     }
   };
@@ -200,18 +217,24 @@ extern "C" int xm_load_traces(const int64_t* bytes, const uint32_t* tag, const i
     xm_free_traces(tr);
     return set_error(rc, std::string("xm_load_traces: trace ") + std::to_string(fb) + ": " + m);
   }
-  uint32_t mi = 0, me = 0;
-  for (int64_t t = 0; t < n_traces; ++t) {
-    mi = std::max(mi, tr->n_ids[t]);
-    me = std::max<uint32_t>(me, uint32_t(off[t + 1] - off[t]));
-    tr->order[t] = uint32_t(t);
-  }
+  uint32_t mi = 0;
+  for (int64_t i = 0; i < n_traces; ++i) mi = std::max(mi, tr->n_ids[i]);
   tr->max_ids = mi;
-  tr->max_events = me;
-  // longest-processing-time-first order (stable: ties keep trace order)
-  std::stable_sort(tr->order, tr->order + n_traces, [&](uint32_t a, uint32_t b) {
-    return off[a + 1] - off[a] > off[b + 1] - off[b];
-  });
+  tr->max_events = n_traces ? uint32_t(soff[1] - soff[0]) : 0u;
+  // upload chunks for the streamed host entry point: chunk c = stored traces
+  // [chunk_end[c-1], chunk_end[c]), cut at trace boundaries near equal event
+  // counts (the first chunks hold the longest traces, which start first)
+  tr->n_chunks = 0;
+  if (tr->chunk_end) {
+    int64_t prev = 0;
+    for (int c = 1; c <= xm_internal::kUploadChunks && prev < n_traces; ++c) {
+      int64_t e = int64_t(std::lower_bound(soff, soff + n_traces + 1, E * c / xm_internal::kUploadChunks) - soff);
+      if (c == xm_internal::kUploadChunks) e = n_traces;
+      if (e <= prev) continue;
+      tr->chunk_end[tr->n_chunks++] = uint32_t(e);
+      prev = e;
+    }
+  }
   *out = tr;
   xm_internal::clear_error();
   return XM_OK;
@@ -246,7 +269,8 @@ extern "C" void xm_free_traces(xm_traces* tr) {
 // ---- helpers for the host entry point (capi.cu) ----
 namespace xm_internal {
 const xm_traces_info traces_info(const xm_traces* tr) {
-  return xm_traces_info{tr->bytes, tr->tag, tr->off, tr->n_ids, tr->order, tr->n_traces,
-                        tr->n_events, tr->max_ids, tr->max_events};
+  return xm_traces_info{tr->bytes,   tr->tag,      tr->off,      tr->n_ids,    tr->order,
+                        tr->n_traces, tr->n_events, tr->max_ids, tr->max_events,
+                        tr->chunk_end, tr->n_chunks};
 }
 }  // namespace xm_internal

@@ -98,6 +98,7 @@ struct KParams {
   uint32_t arena_ids, arena_free;
   xm_result* out;
   uint64_t* curve;              // optional [n_events][3] memory-usage curve (NEXT-1)
+  const uint32_t* ready;        // streamed input: stored traces resident so far, or null
   unsigned long long* timing;   // XM_TIMING builds: [T][2] globaltimer start/end
 };
 
@@ -540,12 +541,12 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
 
   int64_t b_nx = 0;
   uint32_t t_nx = 0;
-  if (lane < n) { b_nx = __ldcs(by + lane); t_nx = __ldcs(tg + lane); }
+  if (lane < n) { b_nx = __ldcg(by + lane); t_nx = __ldcg(tg + lane); }
   for (uint32_t base = 0; base < n; base += 32) {
     const int64_t bc = b_nx;
     const uint32_t tc = t_nx;
     const uint32_t cnt = min(32u, n - base);
-    if (base + 32 + lane < n) { b_nx = __ldcs(by + base + 32 + lane); t_nx = __ldcs(tg + base + 32 + lane); }
+    if (base + 32 + lane < n) { b_nx = __ldcg(by + base + 32 + lane); t_nx = __ldcg(tg + base + 32 + lane); }
     __syncwarp();
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;
@@ -836,6 +837,22 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   return status;
 }
 
+// Streamed input (xm_simulate_host): the copy engine publishes, after each
+// upload chunk, the number of stored traces whose events are resident. The
+// warp sleeps until trace k is among them; the acquire load orders the event
+// loads after the copy that the counter update follows in stream order.
+__device__ void wait_ready(const uint32_t* ready, uint32_t k) {
+  uint32_t nap = 512;
+  for (;;) {
+    uint32_t r;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(ready) : "memory");
+    if (__shfl_sync(kFull, r, 0) > k) break;
+    __nanosleep(nap);
+    nap = min(nap * 2, 8192u);
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   HeapHdr* hdr = reinterpret_cast<HeapHdr*>(smem);
@@ -862,11 +879,13 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       ticket_release(hdr);
       break;
     }
+    // stored trace k (events [off[k], off[k+1])) is the caller's trace order[k]
     const uint32_t t = P.order[k];
-    const int64_t e0 = P.off[t];
-    const uint32_t n = uint32_t(P.off[t + 1] - e0);
-    const uint32_t na = P.n_ids[t];
+    const int64_t e0 = P.off[k];
+    const uint32_t n = uint32_t(P.off[k + 1] - e0);
+    const uint32_t na = P.n_ids[k];
     const uint64_t cap = P.capacity ? P.capacity[t] : P.cap_default;
+    if (P.ready) wait_ready(P.ready, k);
     const uint64_t cap_u = cap >> P.u.unit_shift;
     xm_result R;
 #ifdef XM_TIMING
@@ -959,9 +978,10 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
 
 int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
                   const ReplayPlan& plan, void* d_scratch, xm_result* d_out, void* stream,
-                  int* n_launches) {
+                  int* n_launches, const uint32_t* ready) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   KParams P{};
+  P.ready = ready;
   P.bytes = b->bytes;
   P.tag = b->tag;
   P.off = b->off;

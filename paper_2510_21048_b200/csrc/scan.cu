@@ -81,6 +81,7 @@ __device__ __forceinline__ int64_t rounded_delta(int64_t b, uint32_t sh) {
 struct SParams {
   const int64_t* __restrict__ bytes;
   const int64_t* __restrict__ off;
+  const uint32_t* __restrict__ order;   // caller index of each stored trace
   int64_t n_traces, n_events;
   uint32_t unit_shift;
   int64_t n_tiles;
@@ -102,7 +103,7 @@ __device__ __forceinline__ void write_result(const SParams& P, uint32_t t, int64
   R.peak_allocated_idx = mx > 0 ? uint32_t(arg_flat - o) : 0u;
   R.events_done = uint32_t(P.off[t + 1] - o);
   R.status = XM_T_OK;
-  P.out[t] = R;
+  P.out[P.order[t]] = R;
 }
 
 __device__ __forceinline__ MonoR shfl_up_mono(const MonoR& m, int o) {
@@ -323,7 +324,7 @@ __global__ void k_scan_combine(SParams P) {
   const int64_t a = P.off[t], b = P.off[t + 1];
   if (b <= a) {
     xm_result R{};
-    P.out[t] = R;
+    P.out[P.order[t]] = R;
     return;
   }
   const int64_t ca = a / kTile, cb = (b - 1) / kTile;
@@ -350,6 +351,7 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
   SParams P{};
   P.bytes = b->bytes;
   P.off = b->off;
+  P.order = b->order;
   P.n_traces = b->n_traces;
   P.n_events = b->n_events;
   P.unit_shift = u.unit_shift;

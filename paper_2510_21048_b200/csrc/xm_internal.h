@@ -21,7 +21,11 @@ struct xm_traces_info {
   const uint32_t* order;
   int64_t n_traces, n_events;
   uint32_t max_ids, max_events;
+  const uint32_t* chunk_end;   // pinned [n_chunks]: stored-trace end of each upload chunk
+  int n_chunks;
 };
+// upload chunks of the streamed host entry point (xm_simulate_host)
+constexpr int kUploadChunks = 24;
 const xm_traces_info traces_info(const xm_traces* tr);
 
 // Allocator constants in units of min_block.
@@ -52,7 +56,7 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg);
 // Kernel launchers (replay.cu / scan.cu). Return cudaError_t as int.
 int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
                   const ReplayPlan& plan, void* d_scratch, xm_result* d_out, void* stream,
-                  int* n_launches);
+                  int* n_launches, const uint32_t* ready = nullptr);
 int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t scratch_bytes,
                 xm_result* d_out, void* stream, int* n_launches);
 size_t scan_scratch_bytes(const xm_batch* b);

@@ -55,33 +55,59 @@ def test_loader_renumbers_densely():
     c = fuzz.spec1_corpus(50, 500, salt=31)
     tr = xm.load_traces(c.bytes, c.tag, c.off)
     assert tr.n_traces == 50 and tr.n_events == c.n_events
-    assert (tr.bytes == c.bytes).all() and (tr.off == c.off).all()
-    assert (tr.tag >> 28 == c.tag >> 28).all()                  # streams preserved
     for t in range(c.n_traces):
         a, b = c.off[t], c.off[t + 1]
+        sa, sb = tr.span(t)                                     # stored copy of trace t
+        assert sb - sa == b - a
         by = c.bytes[a:b]
-        dense = tr.tag[a:b] & ((1 << 28) - 1)
+        assert (tr.bytes[sa:sb] == by).all()
+        assert (tr.tag[sa:sb] >> 28 == c.tag[a:b] >> 28).all()  # streams preserved
+        dense = tr.tag[sa:sb] & ((1 << 28) - 1)
         raw = c.tag[a:b] & ((1 << 28) - 1)
-        assert tr.n_ids[t] == _max_live(by)
-        assert dense.max() < tr.n_ids[t]
+        i = int(tr.pos[t])
+        assert tr.n_ids[i] == _max_live(by)
+        assert dense.max() < tr.n_ids[i]
         # the renaming is a bijection between live raw ids and live dense ids
         live = {}
-        for i in range(len(by)):
-            if by[i] > 0:
-                assert dense[i] not in live.values()
-                live[raw[i]] = dense[i]
+        for k in range(len(by)):
+            if by[k] > 0:
+                assert dense[k] not in live.values()
+                live[raw[k]] = dense[k]
             else:
-                assert live.pop(raw[i]) == dense[i]
+                assert live.pop(raw[k]) == dense[k]
     assert tr.max_ids == tr.n_ids.max()
     assert tr.max_events == np.diff(c.off).max()
 
 
 def test_loader_lpt_order():
+    """Stored order = processing order: longest first, ties in caller order;
+    the stored arrays are the caller's traces permuted by order."""
     c = fuzz.spec1_corpus(40, 700, salt=32)
     tr = xm.load_traces(c.bytes, c.tag, c.off)
     L = np.diff(c.off)
     assert sorted(tr.order.tolist()) == list(range(40))
     assert (np.diff(L[tr.order]) <= 0).all()
+    assert (np.diff(tr.off) == L[tr.order]).all() and tr.off[0] == 0
+    for i in range(39):                                         # stable
+        if L[tr.order[i]] == L[tr.order[i + 1]]:
+            assert tr.order[i] < tr.order[i + 1]
+    perm = np.concatenate([np.arange(c.off[t], c.off[t + 1]) for t in tr.order])
+    assert (tr.bytes == c.bytes[perm]).all()
+
+
+def test_loader_reports_first_bad_caller_trace():
+    """With several invalid traces the smallest CALLER index is reported, even
+    though traces are validated in (longest-first) storage order."""
+    by = np.array([512, -512,            # 0 ok
+                   512, -1024,           # 1 bad (short): free size mismatch
+                   512, 512, 512, 512, 512], np.int64)   # 2 bad (long): alloc of a live id
+    tg = np.array([1, 1, 1, 1, 1, 1, 1, 1, 1], np.uint32)
+
+    class bt:
+        bytes, tag, off = by, tg, np.array([0, 2, 4, 9], np.int64)
+    with pytest.raises(xm.XMemError) as e:
+        xm.load_traces(bt.bytes, bt.tag, bt.off)
+    assert e.value.trace == 1
 
 
 @pytest.mark.parametrize("events,code", [
@@ -108,8 +134,9 @@ def test_loader_accepts_id_reuse_and_empty_traces():
     b.alloc(1 << 27, 5, stream=3).free(1 << 27, stream=3).end_trace()
     bt = b.build()
     tr = xm.load_traces(bt.bytes, bt.tag, bt.off)
-    assert tr.n_ids.tolist() == [1, 0, 1]
-    assert (tr.tag[-2:] >> 28 == 3).all()
+    assert tr.n_ids[tr.pos].tolist() == [1, 0, 1]
+    a, b = tr.span(2)
+    assert (tr.tag[a:b] >> 28 == 3).all()
 
 
 def test_loader_bad_offsets():

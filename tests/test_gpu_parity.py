@@ -162,7 +162,7 @@ def test_memory_curve_output():
         by, tg = b.trace(t)
         o, oc = oracle.simulate_trace(by, tg, int(b.capacity[t]), curve=True)
         n = o["events_done"]
-        a = int(b.off[t])
+        a, z = tr.span(t)                                  # rows in stored order
         assert int(h["events_done"][t]) == n
         assert (cv[a:a + n] == oc[:n]).all(), (b.names[t], np.flatnonzero((cv[a:a + n] != oc[:n]).any(1))[:3])
-        assert (cv[a + n:int(b.off[t + 1])] == 0).all()      # unprocessed rows untouched
+        assert (cv[a + n:z] == 0).all()                    # unprocessed rows untouched
