@@ -138,7 +138,9 @@ typedef struct xm_traces xm_traces;
 /* caller's order through `order`.                                            */
 typedef struct {
   const int64_t* bytes;     /* [n_events] signed request bytes: +req alloc, -req free */
-  const uint32_t* tag;      /* [n_events] dense id (bits 0-26) | stream << 28         */
+  const uint32_t* tag;      /* [n_events] dense id (bits 0-26) | stream << 28; a free */
+                            /* carries its block's alloc stream (as xm_load_traces   */
+                            /* writes it)                                            */
   const int64_t* off;       /* [n_traces+1] stored trace i = events [off[i], off[i+1])*/
   const uint32_t* n_ids;    /* [n_traces] dense id space of stored trace i (max live) */
   const uint32_t* order;    /* [n_traces] caller index of stored trace i (a          */

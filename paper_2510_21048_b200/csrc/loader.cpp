@@ -60,6 +60,7 @@ struct Slot {
   uint32_t dense;  // kNone when not live
   int64_t req;
   uint32_t used;
+  uint32_t stream;  // of the live block's alloc
 };
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -84,14 +85,14 @@ struct Renumberer {
     for (int64_t i = 0; i < n; ++i) nalloc += bytes[i] > 0;
     uint64_t cap = 16;
     while (cap < uint64_t(2 * nalloc + 2)) cap <<= 1;
-    table.assign(cap, Slot{0, kNone, 0, 0});
+    table.assign(cap, Slot{0, kNone, 0, 0, 0});
     mask = cap - 1;
     free_ids.clear();
     uint32_t next = 0;
     for (int64_t i = 0; i < n; ++i) {
       int64_t b = bytes[i];
       uint32_t raw = tag[i] & ((1u << XM_ID_BITS) - 1);
-      uint32_t stream = tag[i] >> XM_STREAM_SHIFT;
+      const uint32_t stream = tag[i] >> XM_STREAM_SHIFT;
       if (b == 0) { *msg = "zero-byte event (SPEC.md:231)"; return XM_EINVAL; }
       uint64_t mag = b > 0 ? uint64_t(b) : uint64_t(-(b + 1)) + 1;
       if (mag >= XM_MAX_REQUEST) { *msg = "request >= 2^40 bytes"; return XM_ERANGE; }
@@ -104,12 +105,14 @@ struct Renumberer {
           d = next++;
           if (next > (1u << 27)) { *msg = "more than 2^27 live blocks"; return XM_ERANGE; }
         }
-        s->used = 1; s->key = raw; s->dense = d; s->req = b;
+        s->used = 1; s->key = raw; s->dense = d; s->req = b; s->stream = stream;
         out_tag[i] = d | (stream << XM_STREAM_SHIFT);
       } else {
         if (!s->used || s->dense == kNone) { *msg = "free of a non-live id (SPEC.md:258)"; return XM_EINVAL; }
         if (s->req != -b) { *msg = "free size differs from the alloc's request (SPEC.md:258)"; return XM_EINVAL; }
-        out_tag[i] = s->dense | (stream << XM_STREAM_SHIFT);
+        // a block returns to its own pool (PAPER.md:259 (iv)): the free carries
+        // the stream of the block's alloc, whatever stream the trace records
+        out_tag[i] = s->dense | (s->stream << XM_STREAM_SHIFT);
         free_ids.push_back(s->dense);
         s->dense = kNone;
       }

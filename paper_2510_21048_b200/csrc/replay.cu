@@ -102,11 +102,13 @@ struct KParams {
   unsigned long long* timing;   // XM_TIMING builds: [T][2] globaltimer start/end
 };
 
+#ifdef XM_TIMING
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#endif
 
 // ---- the two state layouts ---------------------------------------------------
 struct Narrow {                       // shared memory
@@ -116,8 +118,11 @@ struct Narrow {                       // shared memory
   static constexpr uint32_t kF = 0x8000u;
   static constexpr uint32_t kMaxIdx = 0x7FFFu;          // ids and free entries < 32767
   static constexpr uint64_t kMaxAddr = 0xFFFFFFFFull;   // bump addresses < 2^32 units
-  static constexpr size_t kABytes = 4 + 4 + 2 + 2 + 1;  // 13
-  static constexpr size_t kFBytes = 8 + 4 + 2 + 2;      // 16: (key<<32 | addr) packed
+  static constexpr uint32_t kMaxSeg = kKeyMax - 1;      // segments < 2^27-1 units, so a
+                                                        // key never saturates: its low
+                                                        // bits ARE the size
+  static constexpr size_t kABytes = 8 + 4;  // (size << 32 | addr), (next << 16 | prev)
+  static constexpr size_t kFBytes = 8 + 4;  // (key << 32 | addr),  (next << 16 | prev)
   static constexpr bool kPacked = true;
 };
 struct Wide {                         // global-memory arena
@@ -127,24 +132,25 @@ struct Wide {                         // global-memory arena
   static constexpr uint32_t kF = 0x80000000u;
   static constexpr uint32_t kMaxIdx = 0x7FFFFFFFu;
   static constexpr uint64_t kMaxAddr = ~0ull;
-  static constexpr size_t kABytes = 8 + 4 + 4 + 4 + 1;  // 21
-  static constexpr size_t kFBytes = 8 + 4 + 4 + 4 + 4;  // 24
+  static constexpr uint32_t kMaxSeg = 0xFFFFFFFFu;
+  static constexpr size_t kABytes = 8 + 4 + 8;          // addr, size, (prev, next)
+  static constexpr size_t kFBytes = 8 + 8 + 4 + 4;      // addr, (prev, next), key, size
   static constexpr bool kPacked = false;
 };
 
+// Links are stored in pairs: lk[2i] = prev, lk[2i+1] = next of record i, so one
+// 32-bit (narrow) or 64-bit (wide) load fetches both.
 template <class L>
 struct State {
-  typename L::Addr* A_pos;
-  uint32_t* A_size;
-  typename L::Link* A_prev;
-  typename L::Link* A_next;
-  uint8_t* A_cls;
+  uint64_t* A_ps;            // Narrow: size << 32 | addr
+  uint64_t* A_pos;           // Wide: addr
+  uint32_t* A_size;          // Wide: size
+  typename L::Link* A_lk;    // [2 * na]
   uint64_t* F_kp;            // Narrow: key << 32 | addr (one load per scanned entry)
-  typename L::Addr* F_pos;   // Wide: addr
+  uint64_t* F_pos;           // Wide: addr
   uint32_t* F_key;           // Wide: key
-  uint32_t* F_size;
-  typename L::Link* F_prev;
-  typename L::Link* F_next;
+  uint32_t* F_size;          // Wide: size (narrow: the key's low 27 bits)
+  typename L::Link* F_lk;    // [2 * nf]
   uint32_t cap_f;
 };
 
@@ -158,28 +164,28 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 // arrays ordered by element size so every array stays naturally aligned
 template <class L>
 __device__ __forceinline__ void carve_a(State<L>& S, unsigned char* p, uint32_t na) {
-  using A = typename L::Addr;
   using K = typename L::Link;
-  S.A_pos = reinterpret_cast<A*>(p); p += align16(size_t(na) * sizeof(A));
-  S.A_size = reinterpret_cast<uint32_t*>(p); p += align16(size_t(na) * 4);
-  S.A_prev = reinterpret_cast<K*>(p); p += size_t(na) * sizeof(K);
-  S.A_next = reinterpret_cast<K*>(p); p += size_t(na) * sizeof(K);
-  S.A_cls = p;
+  if constexpr (L::kPacked) {
+    S.A_ps = reinterpret_cast<uint64_t*>(p); p += align16(size_t(na) * 8);
+  } else {
+    S.A_pos = reinterpret_cast<uint64_t*>(p); p += align16(size_t(na) * 8);
+    S.A_size = reinterpret_cast<uint32_t*>(p); p += align16(size_t(na) * 4);
+  }
+  S.A_lk = reinterpret_cast<K*>(p);
 }
 
 template <class L>
 __device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t nf) {
-  using A = typename L::Addr;
   using K = typename L::Link;
   if constexpr (L::kPacked) {
-    S.F_kp = reinterpret_cast<uint64_t*>(p); p += align16(size_t(nf) * 8);
+    S.F_kp = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
+    S.F_lk = reinterpret_cast<K*>(p);
   } else {
-    S.F_pos = reinterpret_cast<A*>(p); p += align16(size_t(nf) * sizeof(A));
+    S.F_pos = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
+    S.F_lk = reinterpret_cast<K*>(p); p += size_t(nf) * 8;
     S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
+    S.F_size = reinterpret_cast<uint32_t*>(p);
   }
-  S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-  S.F_prev = reinterpret_cast<K*>(p); p += size_t(nf) * sizeof(K);
-  S.F_next = reinterpret_cast<K*>(p);
   S.cap_f = nf;
 }
 
@@ -187,38 +193,91 @@ __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
   return (cls << kKeyBits) | (size < kKeyMax ? size : kKeyMax);
 }
 
-// free-entry key / address accessors (packed in one word for the narrow layout)
+// ---- record accessors ----
 template <class L>
-__device__ __forceinline__ uint32_t fkey(const State<L>& S, uint32_t f) {
-  if constexpr (L::kPacked) return uint32_t(S.F_kp[f] >> 32);
-  else return S.F_key[f];
+__device__ __forceinline__ void load_links(const typename L::Link* lk, uint32_t i, uint32_t& prev,
+                                           uint32_t& next) {
+  if constexpr (L::kPacked) {
+    const uint32_t v = reinterpret_cast<const uint32_t*>(lk)[i];
+    prev = v & 0xFFFFu;
+    next = v >> 16;
+  } else {
+    const uint2 v = reinterpret_cast<const uint2*>(lk)[i];
+    prev = v.x;
+    next = v.y;
+  }
 }
 template <class L>
-__device__ __forceinline__ uint64_t fpos(const State<L>& S, uint32_t f) {
-  if constexpr (L::kPacked) return uint32_t(S.F_kp[f]);
-  else return S.F_pos[f];
+__device__ __forceinline__ void store_links(typename L::Link* lk, uint32_t i, uint32_t prev,
+                                            uint32_t next) {
+  if constexpr (L::kPacked) reinterpret_cast<uint32_t*>(lk)[i] = (next << 16) | (prev & 0xFFFFu);
+  else reinterpret_cast<uint2*>(lk)[i] = make_uint2(prev, next);
+}
+
+// allocated block id: address, size, neighbours
+template <class L>
+__device__ __forceinline__ void a_load(const State<L>& S, uint32_t id, uint64_t& pos,
+                                       uint32_t& size, uint32_t& prev, uint32_t& next) {
+  if constexpr (L::kPacked) {
+    const uint64_t v = S.A_ps[id];
+    pos = uint32_t(v);
+    size = uint32_t(v >> 32);
+  } else {
+    pos = S.A_pos[id];
+    size = S.A_size[id];
+  }
+  load_links<L>(S.A_lk, id, prev, next);
 }
 template <class L>
-__device__ __forceinline__ void set_kp(const State<L>& S, uint32_t f, uint32_t key, uint64_t pos) {
+__device__ __forceinline__ void a_store(const State<L>& S, uint32_t id, uint64_t pos,
+                                        uint32_t size, uint32_t prev, uint32_t next) {
+  if constexpr (L::kPacked) {
+    S.A_ps[id] = (uint64_t(size) << 32) | uint32_t(pos);
+  } else {
+    S.A_pos[id] = pos;
+    S.A_size[id] = size;
+  }
+  store_links<L>(S.A_lk, id, prev, next);
+}
+
+// free entry f: key (class + size), address, size; links separately
+template <class L>
+__device__ __forceinline__ void f_load(const State<L>& S, uint32_t f, uint32_t& key,
+                                       uint64_t& pos, uint32_t& size) {
+  if constexpr (L::kPacked) {
+    const uint64_t v = S.F_kp[f];
+    key = uint32_t(v >> 32);
+    pos = uint32_t(v);
+    size = key & kKeyMax;
+  } else {
+    key = S.F_key[f];
+    pos = S.F_pos[f];
+    size = S.F_size[f];
+  }
+}
+template <class L>
+__device__ __forceinline__ void f_store(const State<L>& S, uint32_t f, uint32_t key,
+                                        uint64_t pos, uint32_t size) {
   if constexpr (L::kPacked) {
     S.F_kp[f] = (uint64_t(key) << 32) | uint32_t(pos);
   } else {
     S.F_key[f] = key;
     S.F_pos[f] = pos;
+    S.F_size[f] = size;
   }
 }
 
 template <class L>
 __device__ __forceinline__ void set_next(const State<L>& S, uint32_t ref, uint32_t v) {
   // branch-free: select the array, predicate the store
-  typename L::Link* p = (ref & L::kF) ? S.F_next + (ref & ~L::kF) : S.A_next + ref;
-  if (ref != L::kNone) *p = typename L::Link(v);
+  typename L::Link* p = (ref & L::kF) ? S.F_lk + 2 * (ref & ~L::kF) : S.A_lk + 2 * ref;
+  if (ref != L::kNone) p[1] = typename L::Link(v);
 }
 
 template <class L>
 __device__ __forceinline__ void set_prev(const State<L>& S, uint32_t ref, uint32_t v) {
-  typename L::Link* p = (ref & L::kF) ? S.F_prev + (ref & ~L::kF) : S.A_prev + ref;
-  if (ref != L::kNone) *p = typename L::Link(v);
+  typename L::Link* p = (ref & L::kF) ? S.F_lk + 2 * (ref & ~L::kF) : S.A_lk + 2 * ref;
+  if (ref != L::kNone) p[0] = typename L::Link(v);
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
@@ -417,13 +476,13 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   for (uint32_t f = lane; f < nf; f += 32) {
     if constexpr (L::kPacked) {
       T.F_kp[f] = S.F_kp[f];
+      reinterpret_cast<uint32_t*>(T.F_lk)[f] = reinterpret_cast<const uint32_t*>(S.F_lk)[f];
     } else {
       T.F_pos[f] = S.F_pos[f];
       T.F_key[f] = S.F_key[f];
+      T.F_size[f] = S.F_size[f];
+      reinterpret_cast<uint2*>(T.F_lk)[f] = reinterpret_cast<const uint2*>(S.F_lk)[f];
     }
-    T.F_size[f] = S.F_size[f];
-    T.F_prev[f] = S.F_prev[f];
-    T.F_next[f] = S.F_next[f];
   }
   __syncwarp();
   heap_free(G.h, G.fstart, G.fnp);
@@ -450,9 +509,10 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
     const uint32_t f = base + lane;
     const bool valid = f < nf;
     uint32_t k = 0, sz = 0, pv = L::kNone, nx = L::kNone;
-    typename L::Addr pos = 0;
+    uint64_t pos = 0;
     if (valid) {
-      k = fkey(S, f); sz = S.F_size[f]; pv = S.F_prev[f]; nx = S.F_next[f]; pos = fpos(S, f);
+      f_load(S, f, k, pos, sz);
+      load_links<L>(S.F_lk, f, pv, nx);
     }
     const bool whole = valid && pv == L::kNone && nx == L::kNone;
     const bool keep = valid && !whole;
@@ -462,8 +522,8 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
     const uint32_t dst = newn + __popc(km & ((1u << lane) - 1u));
     __syncwarp();
     if (keep && dst != f) {
-      set_kp(S, dst, k, pos); S.F_size[dst] = sz;
-      S.F_prev[dst] = typename L::Link(pv); S.F_next[dst] = typename L::Link(nx);
+      f_store(S, dst, k, pos, sz);
+      store_links<L>(S.F_lk, dst, pv, nx);
       set_next(S, pv, L::kF | dst);
       set_prev(S, nx, L::kF | dst);
     }
@@ -479,7 +539,7 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
 }
 
 // Exact best fit: min (size, addr) over entries of class cls with size >= s.
-// Used when the packed-key search cannot decide (sizes >= 2^27 units).
+// Used when the saturated key cannot decide (sizes >= 2^27 units; WIDE only).
 template <class L>
 __device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t nf, uint32_t cls,
                                                    uint32_t s) {
@@ -487,11 +547,10 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t n
   uint32_t bsz = kNone32, bf = kNone32;
   uint64_t bpos = ~0ull;
   for (uint32_t f = lane; f < nf; f += 32) {
-    const uint32_t k = fkey(S, f);
-    if ((k >> kKeyBits) != cls) continue;
-    const uint32_t sz = S.F_size[f];
-    if (sz < s) continue;
-    const uint64_t pos = fpos(S, f);
+    uint32_t k, sz;
+    uint64_t pos;
+    f_load(S, f, k, pos, sz);
+    if ((k >> kKeyBits) != cls || sz < s) continue;
     if (sz < bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
   }
   __syncwarp();
@@ -577,10 +636,12 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
         uint32_t fsel = kNone32;
+        uint32_t fkey_sel = 0;                          // narrow: the winner's key and
+        uint64_t fpos_sel = 0;                          // address, from the reduction
         if constexpr (L::kPacked) {
           // one 64-bit load per entry: (key, addr) compares lexicographically
-          // as (size, addr) for unsaturated sizes; uniform trip count, no
-          // divergence (the body is predicated)
+          // as (size, addr) (narrow keys never saturate); uniform trip count, no
+          // divergence (the body is predicated).
           // d = (key,addr) - (lo,0): candidates are exactly the d <= span64, and
           // they keep their (key,addr) order; non-candidates wrap above span64,
           // so one unsigned 64-bit min does the filter and the best fit at once
@@ -598,20 +659,16 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           }
           if (best > span64) { best = ~0ull; bf = kNone32; }
           else best += lo64;                                // back to (key, addr)
-          const bool has = bf != kNone32;
           const uint32_t bh = uint32_t(best >> 32);
           const uint32_t mh = __reduce_min_sync(kFull, bh);
-          // no real key is 0xFFFFFFFF: small-pool keys never saturate and the
-          // largest large-pool class is 30 (stream 15), so kNone32 means "none"
+          // no real key is 0xFFFFFFFF (the largest class is 31 with an
+          // unsaturated size), so kNone32 means "none"
           if (mh != kNone32) {
-            if ((mh & kKeyMax) == kKeyMax) {
-              fsel = best_fit_exact(S, nf, cls, s);        // saturated sizes: exact compare
-            } else {
-              const bool c1 = has && bh == mh;
-              const uint32_t ml = __reduce_min_sync(kFull, c1 ? uint32_t(best) : kNone32);
-              const unsigned win = __ballot_sync(kFull, c1 && uint32_t(best) == ml);
-              fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
-            }
+            const uint32_t ml = __reduce_min_sync(kFull, bh == mh ? uint32_t(best) : kNone32);
+            const unsigned win = __ballot_sync(kFull, bh == mh && uint32_t(best) == ml);
+            fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
+            fkey_sel = mh;
+            fpos_sel = ml;
           }
         } else {
           uint32_t best = kNone32, bf = kNone32;
@@ -667,7 +724,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
             reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
             if (reserved + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
-          if (bump + a > L::kMaxAddr) { status = kStatusOverflow; break; }  // address width
+          // layout limits (address width, narrow sizes): restart WIDE
+          if (bump + a > L::kMaxAddr || a > L::kMaxSeg) { status = kStatusOverflow; break; }
           bsize = a;
           bposu = bump;                                        // bump address, never reused
           bump += a;
@@ -677,10 +735,14 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           reserved += a;
           if (reserved > pk_res) { pk_res = reserved; ix_res = base + j; }
         } else {
-          bsize = S.F_size[fsel];
-          bprev = S.F_prev[fsel];
-          bnext = S.F_next[fsel];
-          bposu = fpos(S, fsel);
+          if constexpr (L::kPacked) {
+            bsize = fkey_sel & kKeyMax;
+            bposu = fpos_sel;
+          } else {
+            uint32_t k_;
+            f_load(S, fsel, k_, bposu, bsize);
+          }
+          load_links<L>(S.F_lk, fsel, bprev, bnext);
         }
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
@@ -694,29 +756,25 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
         if (remove && fsel != Lx) {
-          lk = fkey(S, Lx); lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = fpos(S, Lx);
+          f_load(S, Lx, lk, lpos, lsz);
+          load_links<L>(S.F_lk, Lx, lpv, lnx);
         }
         __syncwarp();
         // ---- store phase ----
         uint32_t asize;
         if (split) {
           uint32_t r = fsel;                           // remainder keeps the free entry
-          if (fsel == kNone32) {
-            r = nf++;
-            S.F_next[r] = Link(kNone);                 // new segment: no right neighbour
-          }
-          set_kp(S, r, make_key(cls, rem), bposu + s);
-          S.F_size[r] = rem;
-          S.F_prev[r] = Link(id);
-          S.A_next[id] = Link(kF | r);
+          if (fsel == kNone32) r = nf++;               // new segment: no right neighbour
+          f_store(S, r, make_key(cls, rem), bposu + s, rem);
+          store_links<L>(S.F_lk, r, id, bnext);
           asize = s;
+          bnext = kF | r;
         } else {
-          S.A_next[id] = Link(bnext);
           set_prev(S, bnext, id);
           if (remove) {                                // move the last entry into fsel
             if (fsel != Lx) {
-              set_kp(S, fsel, lk, lpos); S.F_size[fsel] = lsz;
-              S.F_prev[fsel] = Link(lpv); S.F_next[fsel] = Link(lnx);
+              f_store(S, fsel, lk, lpos, lsz);
+              store_links<L>(S.F_lk, fsel, lpv, lnx);
               set_next(S, lpv, kF | fsel);
               set_prev(S, lnx, kF | fsel);
             }
@@ -724,10 +782,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           }
           asize = bsize;
         }
-        S.A_size[id] = asize;
-        S.A_pos[id] = bposu;
-        S.A_prev[id] = Link(bprev);
-        S.A_cls[id] = uint8_t(cls);
+        a_store(S, id, bposu, asize, bprev, bnext);
         set_next(S, bprev, id);
         blk += asize;
         // a9: the block peak only moves up on allocs, first index (Q7)
@@ -735,18 +790,23 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
       } else {
         // ================= FREE =================
         // ---- load phase ----
-        const uint32_t sz = S.A_size[id];
-        const uint32_t p = S.A_prev[id];
-        const uint32_t q = S.A_next[id];
-        const uint64_t apos = S.A_pos[id];
-        const uint32_t acls = S.A_cls[id];
+        uint64_t apos;
+        uint32_t sz, p, q;
+        a_load(S, id, apos, sz, p, q);
+        // the block's pool: its stream (the loader gives a free its alloc's
+        // stream) and small iff its size is at most small_size (a small-pool
+        // block is exactly its request; a large-pool one exceeds small_size)
+        const uint32_t acls = ((w >> 28) << 1) | (sz <= u.small_u ? 1u : 0u);
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
         const uint32_t P_ = p & ~kF, N_ = q & ~kF;
-        uint32_t psz = 0, nsz0 = 0, nnx = kNone;
-        uint64_t ppos = 0;
-        if (pf) { psz = S.F_size[P_]; ppos = fpos(S, P_); }
-        if (qf) { nsz0 = S.F_size[N_]; nnx = S.F_next[N_]; }
+        uint32_t psz = 0, nsz0 = 0, nnx = kNone, k_, npv_;
+        uint64_t ppos = 0, npos_;
+        if (pf) f_load(S, P_, k_, ppos, psz);
+        if (qf) {
+          f_load(S, N_, k_, npos_, nsz0);
+          load_links<L>(S.F_lk, N_, npv_, nnx);
+        }
         if (!pf && !qf && nf >= S.cap_f && !grow_f(S, G, nf)) {
           status = kStatusOverflow;
           break;
@@ -755,7 +815,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
         uint64_t lpos = 0;
         if (pf && qf && N_ != Lx) {
-          lk = fkey(S, Lx); lsz = S.F_size[Lx]; lpv = S.F_prev[Lx]; lnx = S.F_next[Lx]; lpos = fpos(S, Lx);
+          f_load(S, Lx, lk, lpos, lsz);
+          load_links<L>(S.F_lk, Lx, lpv, lnx);
         }
         __syncwarp();
         // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
@@ -764,17 +825,16 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           const uint32_t nsz = psz + sz + (qf ? nsz0 : 0u);
           const uint32_t nn = qf ? nnx : q;
           const uint32_t nk = make_key(acls, nsz);
-          S.F_size[P_] = nsz;
-          set_kp(S, P_, nk, ppos);
-          S.F_next[P_] = Link(nn);
+          f_store(S, P_, nk, ppos, nsz);
+          set_next(S, p, nn);
           set_prev(S, nn, p);
           if (qf) {                                   // drop N_: move the last entry there
             if (N_ != Lx) {
               if (Lx == P_) {                         // the last entry is the merged one
                 lk = nk; lsz = nsz; lnx = nn;
               }
-              set_kp(S, N_, lk, lpos); S.F_size[N_] = lsz;
-              S.F_prev[N_] = Link(lpv); S.F_next[N_] = Link(lnx);
+              f_store(S, N_, lk, lpos, lsz);
+              store_links<L>(S.F_lk, N_, lpv, lnx);
               set_next(S, lpv, kF | N_);
               set_prev(S, lnx, kF | N_);
             }
@@ -782,16 +842,13 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           }
         } else if (qf) {
           const uint32_t nsz = nsz0 + sz;
-          set_kp(S, N_, make_key(acls, nsz), apos);
-          S.F_size[N_] = nsz;
-          S.F_prev[N_] = Link(p);
+          f_store(S, N_, make_key(acls, nsz), apos, nsz);
+          set_prev(S, q, p);
           set_next(S, p, q);
         } else {
           const uint32_t r = nf++;
-          set_kp(S, r, make_key(acls, sz), apos);
-          S.F_size[r] = sz;
-          S.F_prev[r] = Link(p);
-          S.F_next[r] = Link(q);
+          f_store(S, r, make_key(acls, sz), apos, sz);
+          store_links<L>(S.F_lk, r, p, q);
           set_next(S, p, kF | r);
           set_prev(S, q, kF | r);
         }

@@ -61,9 +61,16 @@ def test_loader_renumbers_densely():
         assert sb - sa == b - a
         by = c.bytes[a:b]
         assert (tr.bytes[sa:sb] == by).all()
-        assert (tr.tag[sa:sb] >> 28 == c.tag[a:b] >> 28).all()  # streams preserved
         dense = tr.tag[sa:sb] & ((1 << 28) - 1)
         raw = c.tag[a:b] & ((1 << 28) - 1)
+        # allocs keep their stream; a free carries its block's alloc stream
+        st_in, st_out, alloc_stream = c.tag[a:b] >> 28, tr.tag[sa:sb] >> 28, {}
+        for k in range(len(by)):
+            if by[k] > 0:
+                assert st_out[k] == st_in[k]
+                alloc_stream[raw[k]] = st_in[k]
+            else:
+                assert st_out[k] == alloc_stream.pop(raw[k])
         i = int(tr.pos[t])
         assert tr.n_ids[i] == _max_live(by)
         assert dense.max() < tr.n_ids[i]
