@@ -121,6 +121,8 @@ struct Narrow {                       // shared memory
   static constexpr uint32_t kMaxSeg = kKeyMax - 1;      // segments < 2^27-1 units, so a
                                                         // key never saturates: its low
                                                         // bits ARE the size
+  static constexpr uint32_t kCapMax = 0x7FC0u;          // free-list capacity: a multiple
+                                                        // of kScanBlock below kMaxIdx
   static constexpr size_t kABytes = 8 + 4;  // (size << 32 | addr), (next << 16 | prev)
   static constexpr size_t kFBytes = 8 + 4;  // (key << 32 | addr),  (next << 16 | prev)
   static constexpr bool kPacked = true;
@@ -130,13 +132,23 @@ struct Wide {                         // global-memory arena
   using Link = uint32_t;
   static constexpr uint32_t kNone = 0xFFFFFFFFu;
   static constexpr uint32_t kF = 0x80000000u;
-  static constexpr uint32_t kMaxIdx = 0x7FFFFFFFu;
   static constexpr uint64_t kMaxAddr = ~0ull;
   static constexpr uint32_t kMaxSeg = 0xFFFFFFFFu;
+  static constexpr uint32_t kCapMax = 0x7FFFFFFFu;
   static constexpr size_t kABytes = 8 + 4 + 8;          // addr, size, (prev, next)
   static constexpr size_t kFBytes = 8 + 8 + 4 + 4;      // addr, (prev, next), key, size
   static constexpr bool kPacked = false;
 };
+
+// Narrow free list: entries [nf, cap_f) hold kSentinel, which never wins the
+// best-fit minimum, and cap_f is a multiple of kScanBlock, so the scan reads
+// whole blocks of 64 entries (2 per lane) with no bounds test.
+constexpr uint64_t kSentinel = ~0ull;
+constexpr uint32_t kScanBlock = 64;
+
+__host__ __device__ inline uint32_t round_scan(uint32_t x) {
+  return (x + kScanBlock - 1) / kScanBlock * kScanBlock;
+}
 
 // Links are stored in pairs: lk[2i] = prev, lk[2i+1] = next of record i, so one
 // 32-bit (narrow) or 64-bit (wide) load fetches both.
@@ -187,6 +199,14 @@ __device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t 
     S.F_size = reinterpret_cast<uint32_t*>(p);
   }
   S.cap_f = nf;
+}
+
+// warp-cooperative: entries [from, to) of a narrow free list := kSentinel
+template <class L>
+__device__ __forceinline__ void fill_sentinels(const State<L>& S, uint32_t from, uint32_t to) {
+  if constexpr (L::kPacked) {
+    for (uint32_t f = from + (threadIdx.x & 31); f < to; f += 32) S.F_kp[f] = kSentinel;
+  }
 }
 
 __device__ __forceinline__ uint32_t make_key(uint32_t cls, uint32_t size) {
@@ -455,9 +475,9 @@ struct Grow {
 // frees up within a short bounded wait.
 template <class L>
 __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
-  if (G.fstart == kNone32 || S.cap_f >= L::kMaxIdx) return false;
+  if (G.fstart == kNone32 || S.cap_f >= L::kCapMax) return false;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t ncap = min(S.cap_f * 2 + 32, L::kMaxIdx);
+  const uint32_t ncap = min(S.cap_f * 2 + kScanBlock, L::kCapMax);
   const uint32_t np = uint32_t((f_bytes<L>(ncap) + kPage - 1) / kPage);
   if (np > G.total) return false;
   // Bounded wait (~2 ms): running traces finish and free pages long before a
@@ -484,6 +504,7 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
       reinterpret_cast<uint2*>(T.F_lk)[f] = reinterpret_cast<const uint2*>(S.F_lk)[f];
     }
   }
+  fill_sentinels(T, nf, ncap);
   __syncwarp();
   heap_free(G.h, G.fstart, G.fnp);
   G.fstart = st;
@@ -532,6 +553,8 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
     cnt += __popc(wm);
     freed += fs;
   }
+  fill_sentinels(S, newn, nf);
+  __syncwarp();
   nf = newn;
   reserved -= freed;
   n_release += cnt;
@@ -649,13 +672,15 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           const uint64_t span64 = (uint64_t(span) << 32) | 0xFFFFFFFFull;
           uint64_t best = ~0ull;
           uint32_t bf = kNone32;
-#pragma unroll 4
-          for (uint32_t b0 = 0; b0 < nf; b0 += 32) {
-            const uint32_t f = b0 + lane;
-            if (f < nf) {
-              const uint64_t dk = S.F_kp[f] - lo64;
-              if (dk < best) { best = dk; bf = f; }
-            }
+          // (a sentinel maps above span64 unless cls is 31, where it ties the
+          // top of the range with key 0xFFFFFFFF, which reads as "none")
+#pragma unroll 1
+          for (uint32_t b0 = 0; b0 < nf; b0 += kScanBlock) {
+            const uint32_t f0 = b0 + lane, f1 = f0 + 32;
+            const uint64_t d0 = S.F_kp[f0] - lo64;
+            const uint64_t d1 = S.F_kp[f1] - lo64;
+            if (d0 < best) { best = d0; bf = f0; }
+            if (d1 < best) { best = d1; bf = f1; }
           }
           if (best > span64) { best = ~0ull; bf = kNone32; }
           else best += lo64;                                // back to (key, addr)
@@ -778,6 +803,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
               set_next(S, lpv, kF | fsel);
               set_prev(S, lnx, kF | fsel);
             }
+            if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
             nf = Lx;
           }
           asize = bsize;
@@ -838,6 +864,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
               set_next(S, lpv, kF | N_);
               set_prev(S, lnx, kF | N_);
             }
+            if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
             nf = Lx;
           }
         } else if (qf) {
@@ -952,7 +979,7 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     int st = kStatusOverflow;
     // shared memory, NARROW layout: A region + an initial free list
     const uint32_t npa = uint32_t((a_bytes<Narrow>(na) + kPage - 1) / kPage);
-    const uint32_t nfc = min(min(nf_exact, na / 4 + 64), Narrow::kMaxIdx);
+    const uint32_t nfc = min(round_scan(min(nf_exact, na / 4 + 64)), Narrow::kCapMax);
     const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc) + kPage - 1) / kPage);
     if (na <= Narrow::kMaxIdx && npa + npf <= P.heap_pages) {
       const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);
@@ -960,6 +987,8 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       State<Narrow> S;
       carve_a(S, pages + size_t(start) * kPage, na);
       carve_f(S, pages + size_t(start + npa) * kPage, nfc);
+      fill_sentinels(S, 0, nfc);
+      __syncwarp();
       Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
       st = replay_trace(P, S, G, e0, n, cap_u, R);
       heap_free(hdr, start, npa);                  // A pages
