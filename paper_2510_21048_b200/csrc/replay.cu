@@ -126,6 +126,8 @@ struct Narrow {                       // shared memory
   static constexpr size_t kABytes = 8 + 4;  // (size << 32 | addr), (next << 16 | prev)
   static constexpr size_t kFBytes = 8 + 4;  // (key << 32 | addr),  (next << 16 | prev)
   static constexpr bool kPacked = true;
+  // byte counters in units: reserved <= bump < 2^32 units, so 32 bits suffice
+  using Acc = uint32_t;
 };
 struct Wide {                         // global-memory arena
   using Addr = uint64_t;
@@ -138,6 +140,7 @@ struct Wide {                         // global-memory arena
   static constexpr size_t kABytes = 8 + 4 + 8;          // addr, size, (prev, next)
   static constexpr size_t kFBytes = 8 + 8 + 4 + 4;      // addr, (prev, next), key, size
   static constexpr bool kPacked = false;
+  using Acc = uint64_t;
 };
 
 // Narrow free list: entries [nf, cap_f) hold kSentinel, which never wins the
@@ -521,7 +524,7 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
 // and streams. Warp-parallel stable compaction of the free list (lanes write
 // distinct entries; barriers separate the reads of each chunk from its writes).
 template <class L>
-__device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_t& reserved,
+__device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typename L::Acc& reserved,
                                         uint32_t& n_release, uint32_t& live_segs) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t newn = 0, cnt = 0;
@@ -556,7 +559,7 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, uint64_
   fill_sentinels(S, newn, nf);
   __syncwarp();
   nf = newn;
-  reserved -= freed;
+  reserved -= typename L::Acc(freed);
   n_release += cnt;
   live_segs -= cnt;
 }
@@ -600,23 +603,25 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t n
 // __syncwarp(): no lane stores before every lane has loaded, so a lagging
 // group can never read state this event already changed, and the barrier at
 // the end of the event orders the stores before the next event's loads.
-template <class L>
+template <class L, bool kCurve>
 __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow& G, int64_t e0,
                                             uint32_t n, uint64_t cap_u, xm_result& R) {
-  using Link = typename L::Link;
+  using Acc = typename L::Acc;
   constexpr uint32_t kNone = L::kNone, kF = L::kF;
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
   const uint64_t unit_m1 = (1ull << u.unit_shift) - 1;
   const long long* __restrict__ by = reinterpret_cast<const long long*>(P.bytes) + e0;
   const uint32_t* __restrict__ tg = P.tag + e0;
-  uint64_t* const curve = P.curve ? P.curve + 3 * size_t(e0) : nullptr;
-  uint64_t c_blk = 0, c_res = 0;          // curve: this lane's event of the tile
+  uint64_t* const curve = kCurve ? P.curve + 3 * size_t(e0) : nullptr;
+  Acc c_blk = 0, c_res = 0;               // curve: this lane's event of the tile
 
   uint32_t nf = 0, nseg = 0, live_segs = 0, max_live = 0, n_release = 0;
-  uint64_t reserved = 0, blk = 0, bump = 0;
+  Acc reserved = 0, blk = 0;
+  uint64_t bump = 0;
   int64_t tensor = 0;
-  uint64_t pk_tensor = 0, pk_blk = 0, pk_res = 0;
+  uint64_t pk_tensor = 0;
+  Acc pk_blk = 0, pk_res = 0;
   uint32_t ix_tensor = 0, ix_blk = 0, ix_res = 0;
   int status = kStatusOk;
   uint32_t done_total = 0;
@@ -690,8 +695,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           // unsaturated size), so kNone32 means "none"
           if (mh != kNone32) {
             const uint32_t ml = __reduce_min_sync(kFull, bh == mh ? uint32_t(best) : kNone32);
-            const unsigned win = __ballot_sync(kFull, bh == mh && uint32_t(best) == ml);
-            fsel = __shfl_sync(kFull, bf, __ffs(win) - 1);
+            // addresses are unique, so exactly one lane holds (mh, ml)
+            fsel = __reduce_min_sync(kFull, (bh == mh && uint32_t(best) == ml) ? bf : kNone32);
             fkey_sel = mh;
             fpos_sel = ml;
           }
@@ -745,9 +750,9 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           if (small) a = u.sbuf_u;
           else if (s < u.minlarge_u) a = u.lbuf_u;
           else a = uint32_t((uint64_t(s) + u.rlarge_u - 1) / u.rlarge_u * u.rlarge_u);
-          if (reserved + a > cap_u) {                          // device level refuses (Q10)
+          if (uint64_t(reserved) + a > cap_u) {                // device level refuses (Q10)
             reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
-            if (reserved + a > cap_u) { status = kStatusOom; break; }  // both levels failed
+            if (uint64_t(reserved) + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
           // layout limits (address width, narrow sizes): restart WIDE
           if (bump + a > L::kMaxAddr || a > L::kMaxSeg) { status = kStatusOverflow; break; }
@@ -757,7 +762,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           nseg += 1;
           live_segs += 1;
           max_live = max(max_live, live_segs);
-          reserved += a;
+          reserved += Acc(a);
           if (reserved > pk_res) { pk_res = reserved; ix_res = base + j; }
         } else {
           if constexpr (L::kPacked) {
@@ -881,15 +886,15 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         }
         blk -= sz;
       }
-      if (curve && lane == j) { c_blk = blk; c_res = reserved; }
+      if (kCurve && lane == j) { c_blk = blk; c_res = reserved; }
       __syncwarp();
     }
     __syncwarp();
-    if (curve && lane < j) {                 // one row per processed event of the tile
+    if (kCurve && lane < j) {                // one row per processed event of the tile
       uint64_t* row = curve + 3 * size_t(base + lane);
       row[0] = uint64_t(cur) << u.unit_shift;
-      row[1] = c_blk << u.unit_shift;
-      row[2] = c_res << u.unit_shift;
+      row[1] = uint64_t(c_blk) << u.unit_shift;
+      row[2] = uint64_t(c_res) << u.unit_shift;
     }
     // a3: allocated-tensor peak over the processed prefix of this tile
     const int64_t v = lane < j ? cur : INT64_MIN;
@@ -906,9 +911,9 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   }
   const uint32_t sh = u.unit_shift;
   R.peak_allocated = pk_tensor << sh;
-  R.peak_allocated_blk = pk_blk << sh;
-  R.peak_reserved = pk_res << sh;
-  R.final_reserved = reserved << sh;
+  R.peak_allocated_blk = uint64_t(pk_blk) << sh;
+  R.peak_reserved = uint64_t(pk_res) << sh;
+  R.final_reserved = uint64_t(reserved) << sh;
   R.peak_allocated_idx = ix_tensor;
   R.peak_allocated_blk_idx = ix_blk;
   R.peak_reserved_idx = ix_res;
@@ -990,7 +995,8 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       fill_sentinels(S, 0, nfc);
       __syncwarp();
       Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
-      st = replay_trace(P, S, G, e0, n, cap_u, R);
+      st = P.curve ? replay_trace<Narrow, true>(P, S, G, e0, n, cap_u, R)
+                   : replay_trace<Narrow, false>(P, S, G, e0, n, cap_u, R);
       heap_free(hdr, start, npa);                  // A pages
       heap_free(hdr, G.fstart, G.fnp);             // current F pages (maybe moved)
       if (st == kStatusOverflow && lane == 0) atomicAdd(stats, 1u);
@@ -1008,7 +1014,8 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       carve_a(S, base, na);
       carve_f(S, base + align16(a_bytes<Wide>(P.arena_ids)), nf_exact);
       Grow G{hdr, pages, P.heap_pages, kNone32, 0, stats};
-      st = replay_trace(P, S, G, e0, n, cap_u, R);
+      st = P.curve ? replay_trace<Wide, true>(P, S, G, e0, n, cap_u, R)
+                   : replay_trace<Wide, false>(P, S, G, e0, n, cap_u, R);
       __syncwarp();
       __threadfence();
       if (lane == 0) atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
