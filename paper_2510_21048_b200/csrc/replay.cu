@@ -679,8 +679,25 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           uint32_t bf = kNone32;
           // (a sentinel maps above span64 unless cls is 31, where it ties the
           // top of the range with key 0xFFFFFFFF, which reads as "none")
+          // 128 entries per step (4 independent loads per lane, tree minimum),
+          // then at most one 64-entry step: cap_f is a multiple of 64, so
+          // b0 + 64 < nf implies b0 + 128 <= cap_f (all reads in bounds)
+          uint32_t b0 = 0;
 #pragma unroll 1
-          for (uint32_t b0 = 0; b0 < nf; b0 += kScanBlock) {
+          for (; b0 + kScanBlock < nf; b0 += 2 * kScanBlock) {
+            const uint32_t f0 = b0 + lane;
+            const uint64_t d0 = S.F_kp[f0] - lo64;
+            const uint64_t d1 = S.F_kp[f0 + 32] - lo64;
+            const uint64_t d2 = S.F_kp[f0 + 64] - lo64;
+            const uint64_t d3 = S.F_kp[f0 + 96] - lo64;
+            const bool c01 = d1 < d0, c23 = d3 < d2;
+            const uint64_t m01 = c01 ? d1 : d0, m23 = c23 ? d3 : d2;
+            const uint32_t i01 = c01 ? f0 + 32 : f0, i23 = c23 ? f0 + 96 : f0 + 64;
+            const bool c = m23 < m01;
+            const uint64_t m = c ? m23 : m01;
+            if (m < best) { best = m; bf = c ? i23 : i01; }
+          }
+          if (b0 < nf) {
             const uint32_t f0 = b0 + lane, f1 = f0 + 32;
             const uint64_t d0 = S.F_kp[f0] - lo64;
             const uint64_t d1 = S.F_kp[f1] - lo64;
