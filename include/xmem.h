@@ -236,6 +236,41 @@ size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg);
 int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_config* cfg,
                      void* d_ws, size_t ws_bytes, xm_result* h_out, void* stream);
 
+/*
+ * Config-5 support (kernel K4; input generation, not part of
+ * the allocator model): expand Monte Carlo traces from templates ON THE DEVICE
+ * so that a paper-scale batch (1M traces) never crosses PCIe.
+ * The recipe is the counter-based one of workloads/mc5.py (the host side that
+ * rebuilds any single trace for the oracle). For stored trace k with template
+ * t = d_tpl[k] of length n = tpl_off[t+1] - tpl_off[t], event j is template
+ * position src(j):
+ *   c(j)    = j <= n-2 && splitmix64(d_seed[k] + j + 1) < swap_threshold
+ *   keep(j) = c(j) && !c(j-1) && id(j) != id(j+1)     (id = tag bits 0-27)
+ *   src(j)  = keep(j) ? j+1 : keep(j-1) ? j-1 : j   (CPU-timing jitter)
+ * bytes = fixed[src] + per[src] * d_b[k], tag = tag[src] (template block ids are
+ * already dense, so the output satisfies xm_batch's id contract).
+ *   tp: host struct of DEVICE template arrays (caller-owned):
+ *     fixed/per [n_tpl_events] signed per-event bytes (+ alloc, - free);
+ *     tag [n_tpl_events]; tpl_off [n_tpl+1].
+ *   d_tpl, d_b, d_seed [n_traces] (DEVICE, stored order); d_off [n_traces+1]
+ *     (DEVICE) output offsets, which must equal the template lengths; a trace
+ *     whose length disagrees is skipped and *d_flag (DEVICE u32) is set to 1.
+ *   d_bytes [off[n]], d_tag [off[n]]: DEVICE outputs (caller-owned).
+ * Asynchronous on `stream`; one kernel launch. Errors: XM_EINVAL (null or
+ * negative arguments), XM_ECUDA.
+ */
+typedef struct {
+  const int64_t* fixed;
+  const int64_t* per;
+  const uint32_t* tag;
+  const int64_t* tpl_off;
+  int64_t n_tpl;
+} xm_templates;
+int xm_expand_templates(const xm_templates* tp, const uint32_t* d_tpl, const uint32_t* d_b,
+                        const uint64_t* d_seed, uint64_t swap_threshold, const int64_t* d_off,
+                        int64_t n_traces, int64_t* d_bytes, uint32_t* d_tag, uint32_t* d_flag,
+                        void* stream);
+
 /* Number of device kernel launches the last xm_simulate_batch on this thread */
 /* issued (for the bench's gpu_launches claim).                               */
 int xm_last_launch_count(void);

@@ -23,7 +23,7 @@ import numpy as np
 from . import _build
 
 __all__ = ["Config", "Traces", "DeviceBatch", "load_traces", "simulate_batch", "peaks",
-           "simulate_host", "lib", "XMemError", "RESULT_DTYPE", "FIELDS", "UNLIMITED"]
+           "simulate_host", "Templates", "expand_templates", "lib", "XMemError", "RESULT_DTYPE", "FIELDS", "UNLIMITED"]
 
 UNLIMITED = 0xFFFFFFFFFFFFFFFF
 XM_FULL, XM_ALLOCATED_ONLY = 0, 1
@@ -65,6 +65,11 @@ class _Summary(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in
                 ("n_traces", "events_done", "n_oom", "n_overflow", "max_peak_reserved",
                  "max_peak_allocated", "sum_peak_reserved", "n_predicted_oom")]
+
+
+class _Tpl(ctypes.Structure):
+    _fields_ = [("fixed", ctypes.c_void_p), ("per", ctypes.c_void_p), ("tag", ctypes.c_void_p),
+                ("tpl_off", ctypes.c_void_p), ("n_tpl", ctypes.c_int64)]
 
 
 @dataclass
@@ -115,6 +120,7 @@ def lib():
         L.xm_host_ws_bytes.argtypes = [P, ctypes.POINTER(_Cfg)]
         L.xm_host_ws_bytes.restype = ctypes.c_size_t
         L.xm_simulate_host.argtypes = [P, P, ctypes.POINTER(_Cfg), P, ctypes.c_size_t, P, P]
+        L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
         _lib = L
@@ -300,3 +306,71 @@ def simulate_host(tr: Traces, cfg: Config = Config(), capacity: Optional[np.ndar
 
 def as_dict(h: np.ndarray) -> Dict[str, np.ndarray]:
     return {k: h[k].astype(np.uint64) for k in FIELDS}
+
+
+# ---- config 5: on-device template expansion (xm_expand_templates, K4) --------
+class Templates:
+    """A device-resident template pool (xm_templates): per-event signed fixed
+    and per-sample bytes, tags with dense ids, offsets, id space per template."""
+
+    def __init__(self, fixed, per, tag, tpl_off, n_ids, device=None):
+        import torch
+        device = torch.device(device or "cuda")
+        self.fixed = torch.from_numpy(np.ascontiguousarray(fixed, np.int64)).to(device)
+        self.per = torch.from_numpy(np.ascontiguousarray(per, np.int64)).to(device)
+        self.tag = torch.from_numpy(np.ascontiguousarray(tag, np.uint32).view(np.int32)).to(device)
+        self.tpl_off = torch.from_numpy(np.ascontiguousarray(tpl_off, np.int64)).to(device)
+        self.h_off = np.ascontiguousarray(tpl_off, np.int64)
+        self.n_ids = np.ascontiguousarray(n_ids, np.uint32)
+        self.n_tpl = len(self.h_off) - 1
+        self.device = device
+
+    def c(self) -> _Tpl:
+        return _Tpl(ctypes.c_void_p(self.fixed.data_ptr()), ctypes.c_void_p(self.per.data_ptr()),
+                    ctypes.c_void_p(self.tag.data_ptr()), ctypes.c_void_p(self.tpl_off.data_ptr()),
+                    self.n_tpl)
+
+
+def expand_templates(tp: Templates, tpl: np.ndarray, b: np.ndarray, seed: np.ndarray,
+                     swap_threshold: int, capacity: Optional[np.ndarray] = None, stream=None,
+                     check: bool = True) -> DeviceBatch:
+    """Build a DeviceBatch of len(tpl) traces (caller order = the given order)
+    entirely on the device with xm_expand_templates. Traces are stored
+    longest-first (ties in caller order), like xm_load_traces stores them."""
+    import torch
+    tpl = np.ascontiguousarray(tpl, np.uint32)
+    n = len(tpl)
+    lens = np.diff(tp.h_off)[tpl]
+    order = np.argsort(-lens, kind="stable").astype(np.uint32)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens[order])
+    nids = tp.n_ids[tpl][order]
+    dev = tp.device
+
+    def t(a, dt, view=None):
+        a = np.ascontiguousarray(a, dt)
+        return torch.from_numpy(a.view(view) if view else a).to(dev)
+    d_tpl = t(tpl[order], np.uint32, np.int32)
+    d_b = t(np.asarray(b)[order], np.uint32, np.int32)
+    d_seed = t(np.asarray(seed)[order], np.uint64, np.int64)
+    d_off = t(off, np.int64)
+    n_ev = int(off[-1])
+    d_bytes = torch.empty(n_ev, dtype=torch.int64, device=dev)
+    d_tag = torch.empty(n_ev, dtype=torch.int32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    c = tp.c()
+
+    def p(x):
+        return ctypes.c_void_p(x.data_ptr()) if x.numel() else None
+    rc = lib().xm_expand_templates(ctypes.byref(c), p(d_tpl), p(d_b), p(d_seed),
+                                   ctypes.c_uint64(swap_threshold), p(d_off), n, p(d_bytes),
+                                   p(d_tag), ctypes.c_void_p(flag.data_ptr()), _stream_ptr(stream))
+    _check(rc, "xm_expand_templates")
+    if check and int(flag.item()) != 0:
+        raise XMemError("xm_expand_templates: template lengths disagree with offsets")
+    cap = None
+    if capacity is not None:
+        cap = t(np.asarray(capacity, np.uint64), np.uint64, np.int64)
+    return DeviceBatch(d_bytes, d_tag, d_off, t(nids, np.uint32, np.int32),
+                       t(order, np.uint32, np.int32), cap, n, n_ev,
+                       int(nids.max()) if n else 0, int(lens.max()) if n else 0)

@@ -51,6 +51,7 @@ struct ReplayPlan {
 };
 
 int make_unit_config(const xm_config* cfg, UnitConfig* u);
+int& launch_counter();
 ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg);
 
 // Kernel launchers (replay.cu / scan.cu). Return cudaError_t as int.
