@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--cfg5-traces", type=int, default=1_000_000,
+                    help="config 5: total Monte Carlo traces (sharded over the GPUs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -180,7 +182,17 @@ def bounded_sample(batch, budget_events=60_000_000):
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    b, plan, desc, total_ev, total_tr = workload(args.workload, 1 if world == 1 else world, 0)
+    if args.workload == "cfg5":
+        from workloads import mc5
+        n = args.cfg5_traces
+        total_tr = n
+        total_ev = int(mc5.lengths(mc5.describe(np.arange(n))).sum())
+        k = max(1, int(np.ceil(total_ev / 25_000_000)))
+        b = mc5.batch(np.arange(0, n, k))
+        desc = f"configs[4] Monte Carlo, {n} traces (every {k}th trace replayed by the oracle)"
+        plan = None
+    else:
+        b, plan, desc, total_ev, total_tr = workload(args.workload, 1 if world == 1 else world, 0)
     if plan is not None:   # the whole pool, not rank 0's shard
         from workloads import suites
         b = suites.pool_batch(range(total_tr))
@@ -218,6 +230,8 @@ def main():
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if args.workload == "cfg5":
+        return main_cfg5(args, world, rank, local)
 
     import torch
     import torch.distributed as dist
@@ -402,6 +416,172 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "roofline_k1_allocated_only": k1, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clocks, "parity": parity}
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------------- config 5
+def main_cfg5(args, world, rank, local):
+    """configs[4]: N Monte Carlo traces (default 1M) generated ON
+    THE DEVICE by K4 from ~200 templates (only descriptors cross PCIe), LPT-
+    sharded over the GPUs (strong scaling: the total is fixed), replayed by K2,
+    per-trace results all-gathered (N>1). Timed step = replay (+ gather)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2510_21048_b200 as xm
+    from paper_2510_21048_b200.dist import gather_results, lpt_plan
+    from workloads import mc5
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: CUDA device required (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.cfg5_traces
+    d_all = mc5.describe(np.arange(n))
+    L = mc5.lengths(d_all)
+    plan = lpt_plan(L, world) if world > 1 else None
+    mine = plan.shards[rank] if plan else np.arange(n)
+    d = {k: v[mine] for k, v in d_all.items()}
+    pool = xm.Templates(*mc5.template_pool(), device=dev)
+    stream = torch.cuda.current_stream(dev)
+    # K4 (generation, not timed in the step; its kernel timed separately on a
+    # re-expansion into the same buffers: one launch)
+    db = xm.expand_templates(pool, d["tpl"], d["b"], d["seed"], mc5.SWAP_THRESHOLD,
+                             capacity=d["capacity"], stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    xm.expand_again(pool, db, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    k4_ms = e0.elapsed_time(e1)
+    cfg = xm.Config(smem_per_warp=args.smem_per_warp, warps_per_cta=args.warps_per_cta)
+    out = torch.empty((len(mine), 64), dtype=torch.uint8, device=dev)
+
+    def step():
+        r = xm.simulate_batch(db, cfg, stream, out=out)
+        if world > 1:
+            gather_results(r, plan, rank)
+        return r
+
+    sampler = ClockSampler(local)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    launches = xm.last_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    kt0, kt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kt0.record(stream)
+    for _ in range(args.steps):
+        xm.simulate_batch(db, cfg, stream, out=out)
+    kt1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = kt0.elapsed_time(kt1) / args.steps
+    h, summ = xm.peaks(out)
+    local_done = int(h["events_done"].astype(np.int64).sum())
+    vals = torch.tensor([ms, kern_ms, k4_ms, float(local_done)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm)
+        ms, kern_ms, k4_ms, done = float(mx[0]), float(mx[1]), float(mx[2]), int(sm[3])
+    else:
+        done = local_done
+    value = done / (ms / 1e3)
+
+    # e2e through the public API: host descriptors -> K4 -> K2 -> host results
+    e2e = None
+    n_ev_local = int(db.n_events)
+    if not args.no_e2e:
+        del db                              # HBM for a fresh expansion per step
+        torch.cuda.synchronize()
+        tt = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            db2 = xm.expand_templates(pool, d["tpl"], d["b"], d["seed"], mc5.SWAP_THRESHOLD,
+                                      capacity=d["capacity"], stream=stream, check=False)
+            r2 = xm.simulate_batch(db2, cfg, stream, out=out)
+            h2, _ = xm.peaks(r2)
+            del db2
+        dt = (time.perf_counter() - tt) / reps
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t[0])
+        T = len(mine)
+        e2e = {"value": done / dt, "unit": UNIT, "h2d_bytes_per_step": int(40 * T + 8),
+               "d2h_bytes_per_step": int(64 * T), "ms_per_step": dt * 1e3,
+               "api": "xm_expand_templates (descriptors host->device, events generated in HBM) "
+                      "+ xm_simulate_batch + xm_peaks (results device->host)",
+               "results_equal_device_path": bool((h2 == h).all())}
+    clocks = sampler.stop()
+
+    peak, peak_src = peaks_json()
+    alg = 12 * local_done + 24 * len(mine) + 64 * len(mine)
+    achieved = alg / (kern_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "kernel": "k_replay",
+            "alg_bytes_per_launch": alg, "kernel_ms": kern_ms, "peak_source": peak_src,
+            "note": "K2 is a serial integer state machine per trace (issue/latency-bound)"}
+    k4 = {"kernel": "k_expand", "ms": k4_ms, "bound": "hbm",
+          "achieved": 12 * n_ev_local / (k4_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+          "frac": 12 * n_ev_local / (k4_ms / 1e3) / 1e9 / peak,
+          "alg_bytes_per_launch": 12 * n_ev_local}
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k = max(1, int(np.ceil(n_ev_local / 25_000_000)))
+        sub = np.arange(0, n, k)
+        hb = mc5.batch(sub)
+        rate, sec, cores, o, ev = oracle_rate(hb)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"every {k}th trace: {hb.n_traces} traces ({hb.n_events} events); "
+                         f"{sec:.2f} s wall on {cores} host processes"}
+        if not args.no_parity:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from gpu_util import COMPARE
+            mism = 0
+            for f in COMPARE:
+                exp = o[f].astype(np.uint64)
+                if f == "n_free_blocks_end":
+                    exp = np.minimum(exp, 65535)
+                mism += int((h[f][sub].astype(np.uint64) != exp).sum())
+            parity = {"traces": int(len(sub)), "fields": len(COMPARE), "mismatched_values": mism,
+                      "sample": f"every {k}th of {n} traces"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"configs[4] Monte Carlo: {n} perturbed traces generated on "
+                                   f"device (K4), LPT-sharded over {world} GPU(s)",
+                       "n_traces": n, "n_events": int(L.sum()), "events_done": done,
+                       "traces_per_s": n / (ms / 1e3),
+                       "l2": f"inputs larger than L2 ({12 * n_ev_local / 2**30:.1f} GiB/GPU)",
+                       "parallelism": f"dp{world} (trace-sharded)",
+                       "n_oom": summ["n_oom"], "n_overflow": summ["n_overflow"]},
+            "gpu_launches": launches * args.steps, "roofline": roof, "k4_expand": k4,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "parity": parity}
     if rank == 0:
         s = json.dumps(line)
         print(s, flush=True)

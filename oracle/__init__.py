@@ -47,6 +47,7 @@ class _Cfg(ctypes.Structure):
                 ("small_buffer", ctypes.c_uint64), ("large_buffer", ctypes.c_uint64),
                 ("min_large_alloc", ctypes.c_uint64), ("round_large", ctypes.c_uint64),
                 ("capacity", ctypes.c_uint64), ("large_split_strict", ctypes.c_int32),
+                ("roundup_power2_divisions", ctypes.c_int32), ("reclaim_policy", ctypes.c_int32),
                 ("_pad", ctypes.c_int32)]
 
 
@@ -61,11 +62,14 @@ class Config:
     round_large: int = 2 * MiB
     capacity: int = UNLIMITED
     large_split_strict: int = 1
+    roundup_power2_divisions: int = 0    # NEXT-4 variant (torch knob); 0/1 = off
+    reclaim_policy: int = 0              # 0 torch release-all (Q3); 1 SPEC.md:283 D3
 
     def c(self) -> _Cfg:
         return _Cfg(self.min_block, self.small_size, self.small_buffer, self.large_buffer,
                     self.min_large_alloc, self.round_large, self.capacity,
-                    self.large_split_strict, 0)
+                    self.large_split_strict, self.roundup_power2_divisions,
+                    self.reclaim_policy, 0)
 
 
 def build(force: bool = False) -> str:

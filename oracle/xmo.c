@@ -64,6 +64,10 @@ typedef struct {
   uint64_t round_large;      /* 2 MiB    SPEC.md:211 large_round */
   uint64_t capacity;         /* device capacity; UINT64_MAX = unlimited */
   int32_t  large_split_strict; /* 1: split iff rem > small_size (torch); 0: rem >= */
+  int32_t  roundup_power2_divisions; /* NEXT-4 variant: torch PYTORCH_CUDA_ALLOC_CONF          */
+                                     /* roundup_power2_divisions:N (uniform N); 0/1 = off      */
+  int32_t  reclaim_policy;           /* 0: torch release all cached segments (reading Q3);     */
+                                     /* 1: SPEC.md:283 D3 largest first until capacity suffices */
   int32_t  _pad;
 } xmo_config;
 
@@ -74,6 +78,20 @@ typedef struct {
 /* SPEC.md:227-235 round_size: smallest multiple of min_block >= request.
  * PAPER.md:256 (i) "rounded up to the nearest hardware-required multiple". */
 uint64_t xmo_round_size(uint64_t request, const xmo_config* c) {
+  /* Variant (reading Q15): torch's roundup_power2_divisions:N.
+   * A request above min_block * N is rounded up to the next multiple of
+   * 2^k / N, where 2^k is the largest power of two <= the request (N equal
+   * divisions of [2^k, 2^(k+1))); a power of two is kept as is. */
+  uint64_t div = c->roundup_power2_divisions > 1 ? (uint64_t)c->roundup_power2_divisions : 0;
+  if (div && request > c->min_block * div) {
+    uint64_t p2 = 1;
+    while (p2 <= request / 2) p2 *= 2;
+    if (p2 == request) return request;
+    uint64_t step = p2 / div;
+    uint64_t k = request / step;
+    if (k * step < request) k += 1;
+    return k * step;
+  }
   uint64_t q = request / c->min_block;
   if (q * c->min_block < request) q += 1;
   if (q == 0) q = 1;
@@ -193,6 +211,32 @@ static void release_cached(State* S, uint64_t* out) {
   }
 }
 
+/* Variant: SPEC.md:283 D3 "Reclamation releases only
+ * fully-free segments, both pools, largest first, stopping when capacity
+ * suffices" (ties in size: lowest address first -- a reading, Q19). */
+static void release_largest_first(State* S, uint64_t need, uint64_t capacity, uint64_t* out) {
+  while (S->reserved + need > capacity) {
+    int64_t best = -1;
+    for (int64_t k = 0; k < S->nfr; ++k) {
+      Block* b = &S->blk[S->fr[k]];
+      if (b->prev >= 0 || b->next >= 0) continue;        /* not a whole segment */
+      if (best < 0 || b->size > S->blk[S->fr[best]].size ||
+          (b->size == S->blk[S->fr[best]].size && b->addr < S->blk[S->fr[best]].addr))
+        best = k;
+    }
+    if (best < 0) return;
+    Block* b = &S->blk[S->fr[best]];
+    Segment* g = &S->seg[b->seg];
+    g->alive = 0;
+    S->reserved -= g->size;
+    S->live_segs -= 1;
+    out[F_NSEG_RELEASE] += 1;
+    b->alive = 0;
+    S->fr[best] = S->fr[S->nfr - 1];
+    S->nfr--;
+  }
+}
+
 /* Invariants (SPEC.md:272-279 plus DESIGN.md §Invariants), checked after every
  * event in check mode. Returns 0 or XMO_E_INVARIANT. */
 static int check_state(State* S, const xmo_config* c) {
@@ -297,7 +341,10 @@ int xmo_simulate(const int64_t* bytes, const uint32_t* tag, int64_t n,
          * are requested from the GPU only if this cache is insufficient"). */
         uint64_t a = xmo_segment_size(s, &cc);
         if (S.reserved + a > cc.capacity) {           /* device refuses (Q10) */
-          release_cached(&S, out);                    /* reclaim (Q3)          */
+          if (cc.reclaim_policy == 1)
+            release_largest_first(&S, a, cc.capacity, out);  /* SPEC D3 variant */
+          else
+            release_cached(&S, out);                  /* reclaim (Q3)          */
           if (S.reserved + a > cc.capacity) {         /* retry refused: OOM    */
             status = XMO_T_OOM;                       /* PAPER.md:260 (v)      */
             break;

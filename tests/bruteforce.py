@@ -18,7 +18,16 @@ MiB = 1 << 20
 UNLIMITED = (1 << 64) - 1
 
 
-def rnd(req, g=512):
+def rnd(req, g=512, div=0):
+    """512 B round-up; with torch's roundup_power2_divisions:div (NEXT-4 variant)
+    a request above g*div goes to the next of the div equal steps between the
+    powers of two around it (a power of two stays)."""
+    if div > 1 and req > g * div:
+        lo = 1 << (req.bit_length() - 1)          # 2^k <= req < 2^(k+1)
+        if lo == req:
+            return req
+        steps = [lo + i * (lo // div) for i in range(div + 1)]   # lo ... 2*lo
+        return min(x for x in steps if x >= req)
     return max(g, -(-req // g) * g)
 
 
@@ -53,7 +62,7 @@ class Seg:
             yield (a, self.base + self.size - a)
 
 
-def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None):
+def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, reclaim=0):
     """bases: optional segment base addresses in creation order (e.g. the real
     cudaMalloc addresses torch got); default = bump addresses (reading Q4)."""
     segs = []
@@ -70,7 +79,7 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None):
         bid = int(tag[i]) & ((1 << 28) - 1)
         st = int(tag[i]) >> 28
         if nb > 0:
-            s = rnd(nb)
+            s = rnd(nb, div=div)
             small = s <= MiB
             best = None
             for g in segs:
@@ -81,7 +90,19 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None):
                         best = (L, a, g)
             if best is None:
                 need = seg_size(s)
-                if reserved + need > capacity:
+                if reserved + need > capacity and reclaim == 1:
+                    # SPEC.md:283 D3: empty segments, largest first (then lowest
+                    # base), only until the request fits
+                    for g in sorted([g for g in segs if not g.ext], key=lambda g: (-g.size, g.base)):
+                        if reserved + need <= capacity:
+                            break
+                        segs.remove(g)
+                        reserved -= g.size
+                        out["n_seg_release"] += 1
+                    if reserved + need > capacity:
+                        out["status"] = 1
+                        break
+                elif reserved + need > capacity:
                     keep = []
                     for g in segs:
                         if g.ext:

@@ -36,8 +36,8 @@ MUTANTS = [
     ("best fit: tie by high addr", "B->addr < S.blk[best].addr", "B->addr > S.blk[best].addr"),
     ("capacity: >=", "if (S.reserved + a > cc.capacity) {           /* device refuses",
      "if (S.reserved + a >= cc.capacity) {           /* device refuses"),
-    ("no reclamation", "release_cached(&S, out);                    /* reclaim",
-     "/* release_cached */;                    /* reclaim"),
+    ("no reclamation", "release_cached(&S, out);                  /* reclaim",
+     "/* release_cached */;                  /* reclaim"),
     ("no merge prev", "if (p >= 0 && !S.blk[p].allocated) {", "if (0) {"),
     ("no merge next", "if (q >= 0 && !S.blk[q].allocated) {", "if (0) {"),
     ("split remainder at low end", "R->addr = B->addr + s;", "R->addr = B->addr;"),
@@ -49,6 +49,7 @@ MUTANTS = [
 
 
 def _build(src_text, d):
+    os.makedirs(d, exist_ok=True)
     c = os.path.join(d, "m.c")
     so = os.path.join(d, "m.so")
     with open(c, "w") as f:
@@ -61,12 +62,12 @@ def _build(src_text, d):
     return L
 
 
-def _run(L, by, tg, cap):
+def _run(L, by, tg, cap, cfg=None):
     by = np.ascontiguousarray(by, np.int64)
     tg = np.ascontiguousarray(tg, np.uint32)
     out = np.zeros(oracle.NF, np.uint64)
     cv = np.zeros((len(by), 3), np.uint64)
-    c = oracle.Config().c()
+    c = (cfg or oracle.Config()).c()
     rc = L.xmo_simulate(by.ctypes.data_as(P := ctypes.c_void_p), tg.ctypes.data_as(P), len(by),
                         ctypes.byref(c), cap, out.ctypes.data_as(P), cv.ctypes.data_as(P), 0)
     return rc, dict(zip(oracle.FIELDS, map(int, out))), cv
@@ -106,3 +107,50 @@ def test_mutant_rejected(name, old, new, golden):
     with tempfile.TemporaryDirectory() as d:
         L = _build(src.replace(old, new, 1), d)
         assert _pins_reject(L, golden) is not None, f"pins did not catch mutant: {name}"
+
+
+# ---- NEXT-4 variants (tests/test_oracle_variants.py pins) ----------------------
+VARIANT_MUTANTS = [
+    ("roundup: interval one power too high", "while (p2 <= request / 2) p2 *= 2;",
+     "while (p2 <= request) p2 *= 2;"),
+    ("roundup: step 2^k/(2N)", "uint64_t step = p2 / div;", "uint64_t step = p2 / div / 2;"),
+    ("roundup: threshold min_block*N/4", "if (div && request > c->min_block * div) {",
+     "if (div && request > c->min_block * div / 4) {"),
+    ("roundup: floor", "if (k * step < request) k += 1;", ""),
+    ("D3: smallest first", "if (best < 0 || b->size > S->blk[S->fr[best]].size ||",
+     "if (best < 0 || b->size < S->blk[S->fr[best]].size ||"),
+    ("D3: partial segments", "if (b->prev >= 0 || b->next >= 0) continue;",
+     "if (b->prev >= 0 && b->next >= 0) continue;"),
+    ("D3: release all", "      if (cc.reclaim_policy == 1)", "      if (0)"),
+]
+
+
+def _variant_pins_reject(L):
+    from workloads import hand as H
+    b = H.h8()
+    by, tg = b.trace(0)
+    rc, r, _ = _run(L, by, tg, 32 << 20, oracle.Config(reclaim_policy=1))
+    if rc or (r["n_seg_release"], r["final_reserved"]) != (1, 14 << 20):
+        return "H8"
+    for div, corpus in ((4, fuzz.spec1_corpus(60, 300, salt=64)),
+                        (2, fuzz.small_size_corpus(30, 300, salt=72)),
+                        (0, fuzz.capacity_corpus(60, 300, salt=81))):
+        cfg = oracle.Config(roundup_power2_divisions=div, reclaim_policy=int(div == 0))
+        for t in range(corpus.n_traces):
+            by, tg = corpus.trace(t)
+            cap = int(corpus.capacity[t])
+            rc, r, cv = _run(L, by, tg, cap, cfg)
+            bb, bc = bruteforce.simulate(by, tg, cap, div=div, reclaim=int(div == 0))
+            if rc or any(r[k] != v for k, v in bb.items()):
+                return f"bruteforce div={div} trace {t}"
+    return None
+
+
+@pytest.mark.parametrize("name,old,new", VARIANT_MUTANTS, ids=[m[0] for m in VARIANT_MUTANTS])
+def test_variant_mutant_rejected(name, old, new):
+    src = open(SRC).read()
+    assert src.count(old) >= 1, f"mutation site missing: {name}"
+    with tempfile.TemporaryDirectory() as d:
+        assert _variant_pins_reject(_build(src, d)) is None
+        L = _build(src.replace(old, new, 1), d + "/m")
+        assert _variant_pins_reject(L) is not None, f"pins did not catch mutant: {name}"

@@ -177,3 +177,17 @@ def all_named() -> Dict[str, Batch]:
     d.update(spec_examples())
     d.update(paper_examples())
     return d
+
+
+def h8() -> Batch:
+    """H8 (SPEC.md:283 D3 vs torch release-all): a 2 MiB small and a 20 MiB
+    large segment are cached (fully free); a 12 MiB request on another stream
+    needs a new segment under a 32 MiB capacity."""
+    def f(b):
+        b.alloc(0, 512)
+        b.alloc(1, 2 * MiB)
+        b.free(0)
+        b.free(1)
+        b.alloc(2, 12 * MiB, stream=1)
+        b.free(2, stream=1)
+    return _one(f, capacity=32 * MiB, name="H8")
