@@ -51,6 +51,8 @@ extern "C" {
 
 /* -------------------------------------------------------------- modes */
 #define XM_FULL 0            /* full allocator replay (K2)                     */
+#define XM_RECLAIM_ALL 0
+#define XM_RECLAIM_LARGEST_FIRST 1
 #define XM_ALLOCATED_ONLY 1  /* only peak_allocated / _idx via the segmented   */
                              /* prefix-scan/max (K1). Exact only with unlimited */
                              /* capacity, which it requires (else XM_EINVAL).   */
@@ -84,6 +86,18 @@ typedef struct {
                                /* smem_per_warp * warps_per_cta bytes (tests);  */
                                /* 0 = the whole 227 KB                          */
   uint32_t warps_per_cta;      /* 0 = default (12)                              */
+  /* Allocator variants (readings Q19, Q20):  */
+  uint32_t roundup_power2_divisions; /* torch PYTORCH_CUDA_ALLOC_CONF          */
+                               /* roundup_power2_divisions:N, one N for all sizes: */
+                               /* a request above min_block*N is rounded up to the */
+                               /* next of N equal steps between the powers of two  */
+                               /* around it. 0 or 1 = off (default); else a power  */
+                               /* of two <= 64 (XM_EINVAL otherwise)               */
+  uint32_t reclaim_policy;     /* XM_RECLAIM_ALL (default, torch                  */
+                               /* release_cached_blocks, reading Q3) or            */
+                               /* XM_RECLAIM_LARGEST_FIRST (SPEC.md:283 D3: fully  */
+                               /* free segments largest first, ties lowest address,*/
+                               /* only until the request fits)                     */
 } xm_config;
 
 /*

@@ -50,6 +50,11 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
     return set_error(XM_EINVAL, "xm_config: segment sizes must cover the small threshold");
   if (c->mode != XM_FULL && c->mode != XM_ALLOCATED_ONLY)
     return set_error(XM_EINVAL, "xm_config: unknown mode");
+  const uint32_t dv = c->roundup_power2_divisions;
+  if (dv > 1 && (dv & (dv - 1) || dv > 64))
+    return set_error(XM_EINVAL, "xm_config: roundup_power2_divisions must be a power of two <= 64");
+  if (c->reclaim_policy != XM_RECLAIM_ALL && c->reclaim_policy != XM_RECLAIM_LARGEST_FIRST)
+    return set_error(XM_EINVAL, "xm_config: unknown reclaim_policy");
   int sh = 0;
   while ((1ull << sh) < m) ++sh;
   u->unit_shift = uint32_t(sh);
@@ -59,6 +64,9 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
   u->minlarge_u = uint32_t(c->min_large_alloc / m);
   u->rlarge_u = uint32_t(c->round_large / m);
   u->strict = c->large_split_strict ? 1u : 0u;
+  u->div_shift = 0;
+  while (dv > 1 && (1u << u->div_shift) < dv) ++u->div_shift;
+  u->reclaim_d3 = c->reclaim_policy == XM_RECLAIM_LARGEST_FIRST ? 1u : 0u;
   return XM_OK;
 }
 

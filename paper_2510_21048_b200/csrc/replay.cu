@@ -15,23 +15,24 @@
 //    blocks (A, fixed size) and the free list (F), which moves to a region
 //    twice as large when it fills (entries keep their indices). Occupancy thus
 //    adapts to the traces actually running. Shared-memory state uses the
-//    NARROW layout (32-bit addresses, 16-bit links: 13 B per A record, 16 B
-//    per F entry); a trace that exceeds it (>= 32767 live blocks or free
-//    blocks, >= 2 TiB of segments ever created) or cannot grow restarts in a
-//    global-memory arena with the WIDE layout (64-bit addresses, 32-bit links),
-//    sized to the exact bound so it cannot overflow;
+//    NARROW layout (32-bit addresses and byte counters, 16-bit links: 12 B per
+//    A record, 12 B per F entry); a trace that exceeds it (>= 32767 live
+//    blocks or free blocks, >= 2 TiB of segments ever created) or cannot grow
+//    restarts in a global-memory arena with the WIDE layout (64-bit addresses,
+//    32-bit links), sized to the exact bound so it cannot overflow;
 //  * events stream through registers in 32-event tiles (coalesced streaming
 //    loads, next tile prefetched); round-up and the allocated-bytes prefix
 //    scan of a tile are lane-parallel (a2, a3);
 //  * the serial state machine is warp-uniform (every lane computes the same
 //    scalars, so no broadcasts); the best-fit search scans the free list
-//    lane-strided with ONE packed 32-bit key per entry (class in the top 5
-//    bits, saturated size below) and __reduce_min_sync; ties in size are
-//    broken by address, loaded only when needed (a5).
+//    lane-strided, 4 entries per lane per step, with ONE packed 64-bit
+//    (key << 32 | addr) word per entry (key = class in the top 5 bits, size
+//    below), so a single unsigned minimum is the (size, addr) best fit; three
+//    __reduce_min_sync pick the winner across lanes (a5).
 //
 // State (structure of arrays):
-//  A[id]  allocated block of dense id: addr, size u32, prev, next, cls u8
-//  F[f]   free block f (unordered, nf entries): key u32, size u32, addr, prev, next
+//  A[id]  allocated block of dense id: (size << 32 | addr), (next << 16 | prev)
+//  F[f]   free block f (unordered, nf entries): (key << 32 | addr), (next << 16 | prev)
 //  addr = bump address in units of min_block (segments are never reused, so
 //         (size, addr) order == SPEC D2's (size, segment, offset), reading Q4)
 //  prev/next = address-order neighbours in the segment: kNone, an id, or kF|f
@@ -40,6 +41,7 @@
 
 #include <algorithm>
 
+#include "rounding.cuh"
 #include "xm_internal.h"
 
 #ifdef XM_DEBUG
@@ -564,6 +566,61 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typenam
   live_segs -= cnt;
 }
 
+// Variant (SPEC.md:283 D3): release fully-free segments one at a
+// time, largest first (ties: lowest address, reading Q19), only until
+// reserved + need <= cap. Each round: a warp arg-max over the free list, then
+// the chosen entry is dropped by moving the last entry into its slot. A
+// whole-segment entry has no neighbours; the moved one's are re-pointed.
+template <class L>
+__device__ __noinline__ void reclaim_largest_first(State<L>& S, uint32_t& nf,
+                                                   typename L::Acc& reserved, uint32_t& n_release,
+                                                   uint32_t& live_segs, uint64_t need,
+                                                   uint64_t cap_u) {
+  const uint32_t lane = threadIdx.x & 31;
+  while (uint64_t(reserved) + need > cap_u) {
+    uint32_t bsz = 0, bf = kNone32;
+    uint64_t bpos = ~0ull;
+    for (uint32_t f = lane; f < nf; f += 32) {
+      uint32_t k, sz, pv, nx;
+      uint64_t pos;
+      f_load(S, f, k, pos, sz);
+      load_links<L>(S.F_lk, f, pv, nx);
+      if (pv != L::kNone || nx != L::kNone) continue;
+      if (sz > bsz || (sz == bsz && pos < bpos)) { bsz = sz; bpos = pos; bf = f; }
+    }
+    __syncwarp();
+    const uint32_t msz = __reduce_max_sync(kFull, bsz);
+    if (msz == 0) break;                                   // nothing left to release
+    const bool c1 = bsz == msz && bf != kNone32;
+    const uint32_t hi = c1 ? uint32_t(bpos >> 32) : kNone32;
+    const uint32_t mh = __reduce_min_sync(kFull, hi);
+    const uint32_t lo = (c1 && hi == mh) ? uint32_t(bpos) : kNone32;
+    const uint32_t ml = __reduce_min_sync(kFull, lo);
+    const uint32_t fsel = __reduce_min_sync(kFull, (c1 && hi == mh && uint32_t(bpos) == ml) ? bf : kNone32);
+    // load phase: the last entry (moved into fsel)
+    const uint32_t Lx = nf - 1;
+    uint32_t lk = 0, lsz = 0, lpv = L::kNone, lnx = L::kNone;
+    uint64_t lpos = 0;
+    if (fsel != Lx) {
+      f_load(S, Lx, lk, lpos, lsz);
+      load_links<L>(S.F_lk, Lx, lpv, lnx);
+    }
+    __syncwarp();
+    if (fsel != Lx) {
+      f_store(S, fsel, lk, lpos, lsz);
+      store_links<L>(S.F_lk, fsel, lpv, lnx);
+      set_next(S, lpv, L::kF | fsel);
+      set_prev(S, lnx, L::kF | fsel);
+    }
+    if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
+    __syncwarp();
+    nf = Lx;
+    reserved -= typename L::Acc(msz);
+    n_release += 1;
+    live_segs -= 1;
+  }
+}
+
 // Exact best fit: min (size, addr) over entries of class cls with size >= s.
 // Used when the saturated key cannot decide (sizes >= 2^27 units; WIDE only).
 template <class L>
@@ -610,7 +667,6 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   constexpr uint32_t kNone = L::kNone, kF = L::kF;
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
-  const uint64_t unit_m1 = (1ull << u.unit_shift) - 1;
   const long long* __restrict__ by = reinterpret_cast<const long long*>(P.bytes) + e0;
   const uint32_t* __restrict__ tg = P.tag + e0;
   uint64_t* const curve = kCurve ? P.curve + 3 * size_t(e0) : nullptr;
@@ -638,7 +694,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;
     const uint64_t mag = is_alloc ? uint64_t(bc) : uint64_t(-bc);
-    const uint32_t su = uint32_t((mag + unit_m1) >> u.unit_shift);
+    const uint32_t su = xm_internal::round_units(mag, u);
     // ---- a3: tile prefix-scan of +-s (allocated tensor bytes) ----
     int64_t d = lane < cnt ? (is_alloc ? int64_t(su) : -int64_t(su)) : 0;
 #pragma unroll
@@ -768,7 +824,10 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           else if (s < u.minlarge_u) a = u.lbuf_u;
           else a = uint32_t((uint64_t(s) + u.rlarge_u - 1) / u.rlarge_u * u.rlarge_u);
           if (uint64_t(reserved) + a > cap_u) {                // device level refuses (Q10)
-            reclaim(S, nf, reserved, n_release, live_segs);    // reclaim cached segments (Q3)
+            if (u.reclaim_d3)                                  // SPEC D3 variant (NEXT-4)
+              reclaim_largest_first(S, nf, reserved, n_release, live_segs, a, cap_u);
+            else
+              reclaim(S, nf, reserved, n_release, live_segs);  // reclaim cached segments (Q3)
             if (uint64_t(reserved) + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
           // layout limits (address width, narrow sizes): restart WIDE

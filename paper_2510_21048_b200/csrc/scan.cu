@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "rounding.cuh"
 #include "xm_internal.h"
 
 namespace {
@@ -78,12 +79,20 @@ __device__ __forceinline__ int64_t rounded_delta(int64_t b, uint32_t sh) {
   return (b + (b > 0 ? int64_t((1ull << sh) - 1) : 0)) >> sh;
 }
 
+// with the roundup_power2_divisions variant (NEXT-4): the shared a2 rule
+__device__ __forceinline__ int64_t rounded_delta(int64_t b, const xm_internal::UnitConfig& u) {
+  if (!u.div_shift) return rounded_delta(b, u.unit_shift);
+  const int64_t r = int64_t(xm_internal::round_units(uint64_t(b > 0 ? b : -b), u));
+  return b > 0 ? r : -r;
+}
+
 struct SParams {
   const int64_t* __restrict__ bytes;
   const int64_t* __restrict__ off;
   const uint32_t* __restrict__ order;   // caller index of each stored trace
   int64_t n_traces, n_events;
   uint32_t unit_shift;
+  xm_internal::UnitConfig u;
   int64_t n_tiles;
   uint32_t* row_trace;      // [n_tiles * kThreads] trace owning each thread row's first event
   Mono* tile_first;         // [n_tiles] piece before the tile's first trace start
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         if (i < nvalid) {
-          run += rounded_delta(d[i], P.unit_shift);
+          run += rounded_delta(d[i], P.u);
           if (run > mx) { mx = run; arg = rel0 + i; }
         }
       }
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
           cur.tr = tcur;
           run = 0;
         }
-        run += rounded_delta(d[i], P.unit_shift);
+        run += rounded_delta(d[i], P.u);
         cur.sum = run;
         if (run > cur.mx) { cur.mx = run; cur.arg = rel0 + i; }
       }
@@ -355,6 +364,7 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
   P.n_traces = b->n_traces;
   P.n_events = b->n_events;
   P.unit_shift = u.unit_shift;
+  P.u = u;
   P.n_tiles = n_tiles_of(b);
   char* s = static_cast<char*>(d_scratch) + 256;
   P.tile_first = reinterpret_cast<Mono*>(s);

@@ -37,6 +37,8 @@ struct UnitConfig {
   uint32_t minlarge_u;   // min_large_alloc / min_block
   uint32_t rlarge_u;     // round_large / min_block
   uint32_t strict;       // large split iff rem > small (1) or >= (0)
+  uint32_t div_shift;    // log2(roundup_power2_divisions), 0 = off (NEXT-4 variant)
+  uint32_t reclaim_d3;   // 1: SPEC D3 largest-first reclamation (NEXT-4 variant)
 };
 
 // Launch geometry + scratch layout of the replay kernel for one batch.

@@ -21,8 +21,9 @@ def gpu_run(batch, cfg=None, capacity=True):
     return h, summ
 
 
-def oracle_run(batch, strict=1, parallel=False):
-    ocfg = oracle.Config(large_split_strict=strict)
+def oracle_run(batch, strict=1, parallel=False, div=0, reclaim=0):
+    ocfg = oracle.Config(large_split_strict=strict, roundup_power2_divisions=div,
+                         reclaim_policy=reclaim)
     if parallel:
         return oracle.simulate_batch_parallel(batch, ocfg)
     return oracle.simulate_batch(batch, ocfg)

@@ -166,3 +166,41 @@ def test_memory_curve_output():
         assert int(h["events_done"][t]) == n
         assert (cv[a:a + n] == oc[:n]).all(), (b.names[t], np.flatnonzero((cv[a:a + n] != oc[:n]).any(1))[:3])
         assert (cv[a + n:z] == 0).all()                    # unprocessed rows untouched
+
+
+# ---- NEXT-4 allocator variants (oracle pins: tests/test_oracle_variants.py) ----
+@pytest.mark.parametrize("div", [2, 4, 8])
+def test_variant_roundup_power2_divisions(div):
+    b = concat([fuzz.spec1_corpus(300, 800, salt=90 + div), fuzz.small_size_corpus(100, 500, salt=95),
+                fuzz.capacity_corpus(100, 500, salt=96), suites.config3().subset([0, 30])])
+    h, _ = gpu_run(b, xm.Config(roundup_power2_divisions=div))
+    assert_parity(b, h, oracle_run(b, div=div))
+
+
+def test_variant_roundup_allocated_only_mode():
+    b = concat([fuzz.spec1_corpus(300, 1000, salt=97), suites.config2().subset([0, 31])])
+    h, _ = gpu_run(b, xm.Config(mode=1, roundup_power2_divisions=4))
+    assert_parity(b, h, oracle_run(b, div=4),
+                  fields=["peak_allocated", "peak_allocated_idx", "events_done"])
+
+
+def test_variant_d3_largest_first_reclaim(golden):
+    b = concat([hand.h8(), fuzz.capacity_corpus(400, 800, salt=98)])
+    cfg = xm.Config(reclaim_policy=1)
+    h, _ = gpu_run(b, cfg)
+    o = oracle_run(b, reclaim=1)
+    assert_parity(b, h, o)
+    assert (int(h["n_seg_release"][0]), int(h["final_reserved"][0])) == (1, 14 << 20)
+    h2, _ = gpu_run(b, xm.Config(reclaim_policy=1, roundup_power2_divisions=4))
+    assert_parity(b, h2, oracle_run(b, reclaim=1, div=4))
+    # the global-arena (wide) layout takes the same variant paths
+    h3, _ = gpu_run(b, xm.Config(reclaim_policy=1, smem_per_warp=4096, warps_per_cta=1))
+    assert_parity(b, h3, o)
+
+
+def test_variant_config_validation():
+    b = hand.h7()
+    with pytest.raises(xm.XMemError):
+        gpu_run(b, xm.Config(roundup_power2_divisions=3))
+    with pytest.raises(xm.XMemError):
+        gpu_run(b, xm.Config(reclaim_policy=7))

@@ -32,13 +32,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 MiB = 1 << 20
 
 
-def torch_replay_batch(batch, full=False):
+def torch_replay_batch(batch, full=False, conf=""):
     """All traces of a workloads.Batch in one fresh process (cache emptied between).
     Returns per-trace stats (and, if full, the per-event curve and pointers)."""
     with tempfile.TemporaryDirectory() as d:
         p, q = os.path.join(d, "t.npz"), os.path.join(d, "o.npz")
         np.savez(p, bytes=batch.bytes, tag=batch.tag, off=batch.off, capacity=batch.capacity)
-        r = subprocess.run([sys.executable, os.path.join(HERE, "torch_replay.py"), p, q],
+        r = subprocess.run([sys.executable, os.path.join(HERE, "torch_replay.py"), p, q]
+                           + ([conf] if conf else []),
                            capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, r.stderr[-2000:]
         o = np.load(q)
@@ -145,3 +146,59 @@ def test_fuzz_traces_match_real_torch():
     for t in range(c.n_traces):
         agree += all(int(o[f][t]) == reals[t][f] for f in FIELDS)
     assert agree >= int(0.9 * c.n_traces), f"{agree}/{c.n_traces} traces agree with real torch"
+
+
+# ---- NEXT-4 variant: roundup_power2_divisions against the real allocator ----
+CONF4 = "roundup_power2_divisions:4"
+
+
+def test_roundup_power2_divisions_sizes_match_real_torch():
+    """Each request alone on a fresh cache (alloc then free): torch's
+    memory_allocated() right after the alloc is the block size = the rounded
+    request (small pool: always split at >= 512 B remainders; large pool below
+    10 MiB: the 20 MiB segment always leaves > 1 MiB). Pins reading Q20: the
+    N-division rounding, its min_block * N threshold, powers of two kept."""
+    from workloads.trace import TraceBuilder
+    sizes = [1, 511, 600, 1200, 2000, 2048, 2049, 3000, 4097, 70_000, 1_000_000, MiB - 1,
+             MiB, MiB + 1, 3 * MiB // 2 + 1, 3 * MiB, 5_000_000, 7 * MiB + 12345, 9_999_999]
+    tb = TraceBuilder()
+    for i, sz in enumerate(sizes):
+        tb.alloc(i, sz).free(i)
+    tb.end_trace()
+    b = tb.build()
+    stats, curve, _ = torch_replay_batch(b, full=True, conf=CONF4)
+    _, oc = oracle.simulate_trace(b.bytes, b.tag, cfg=oracle.Config(roundup_power2_divisions=4),
+                                  curve=True)
+    got = curve[0::2, 0]                      # allocated right after each alloc
+    exp = oc[0::2, 1].astype(np.int64)
+    assert got.tolist() == exp.tolist(), list(zip(sizes, got.tolist(), exp.tolist()))
+    assert exp.tolist() != [oracle.round_size(s) for s in sizes]   # the knob changes sizes
+
+
+def test_roundup_power2_divisions_traces_match_real_torch():
+    named = hand.all_named()
+    b = concat([named[k] for k in HAND] + [suites.config1()])
+    reals = torch_replay_batch(b, conf=CONF4)
+    o = oracle.simulate_batch(b, oracle.Config(roundup_power2_divisions=4))
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    g, _ = xm.peaks(xm.simulate_batch(tr.to_device(), xm.Config(roundup_power2_divisions=4)))
+    for t in range(b.n_traces):
+        for f in FIELDS:
+            assert int(o[f][t]) == reals[t][f], (t, f, int(o[f][t]), reals[t][f])
+            assert int(g[f][t]) == reals[t][f], (t, f)
+
+
+def test_roundup_power2_divisions_training_traces_given_torch_addresses():
+    import bruteforce
+    b = concat([suites.config2().subset([0, 31]), suites.config3().subset([0, 43])])
+    stats, curve, ptr = torch_replay_batch(b, full=True, conf=CONF4)
+    for t in range(b.n_traces):
+        a, z = int(b.off[t]), int(b.off[t + 1])
+        by, tg = b.bytes[a:z], b.tag[a:z]
+        res = curve[a:z, 1]
+        grew = np.flatnonzero(res > np.concatenate([[0], res[:-1]]))
+        bases = [int(ptr[a + i]) for i in grew]
+        _, bc = bruteforce.simulate(by, tg, bases=bases, div=4)
+        bc = np.asarray(bc, np.int64)
+        assert (bc[:, 2] == res).all(), (b.names[t], "reserved curve")
+        assert (bc[:, 1] == curve[a:z, 0]).all(), (b.names[t], "allocated curve")

@@ -7,7 +7,8 @@ the request on the event's stream, free = drop the tensor (no record_stream), a
 finite capacity = torch.cuda.set_per_process_memory_fraction. Used only by
 tests/test_torch_allocator_pin.py.
 
-usage: torch_replay.py IN.npz OUT.npz   (IN: bytes, tag, off, capacity)
+usage: torch_replay.py IN.npz OUT.npz [ALLOC_CONF]   (IN: bytes, tag, off, capacity)
+ALLOC_CONF: optional PYTORCH_CUDA_ALLOC_CONF for the replay (allocator variants).
 OUT: stats (JSON string, one dict per trace), and per event: allocated bytes,
 reserved bytes and the returned device pointer (0 for frees).
 """
@@ -63,8 +64,10 @@ def replay_one(torch, by, tg, cap, curve, ptr):
     return out
 
 
-def main(inp, outp):
+def main(inp, outp, conf=""):
     os.environ.pop("PYTORCH_CUDA_ALLOC_CONF", None)
+    if conf:
+        os.environ["PYTORCH_CUDA_ALLOC_CONF"] = conf
     import torch
     torch.cuda.init()
     d = np.load(inp)
@@ -81,4 +84,4 @@ def main(inp, outp):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "")
