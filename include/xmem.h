@@ -285,6 +285,50 @@ int xm_expand_templates(const xm_templates* tp, const uint32_t* d_tpl, const uin
                         int64_t n_traces, int64_t* d_bytes, uint32_t* d_tag, uint32_t* d_flag,
                         void* stream);
 
+/*
+ * Batched evaluation metrics: the paper's MRE, PEF
+ * and MCP over N runs (SPEC.md:339-417 metrics module),
+ * given the estimates (e.g. xm_result.peak_reserved and Eq. 1's ÔOM from the
+ * replay) and user-supplied measurements of real runs (Table 1 notation).
+ * One record per run, DEVICE memory, 40 bytes:
+ */
+#define XM_ROUND2_NOT_RUN 2
+typedef struct {
+  uint64_t m_peak_est;    /* M̂peak_jde, the estimate                              */
+  uint64_t m_peak_meas1;  /* Mpeak_jd1, measured in round 1 (used iff OOM_jd1 = 0)  */
+  uint64_t m_peak_meas2;  /* Mpeak_jd2, measured in round 2 (used iff OOM_jde2 = 0) */
+  uint64_t m_max;         /* M_d^max                                               */
+  uint8_t oom_pred;       /* ÔOM_jde (Eq. 1: M̂peak > M_d^max)          */
+  uint8_t oom1;           /* OOM_jd1 (round 1 with full device memory)             */
+  uint8_t oom2;           /* OOM_jde2: 0, 1, or XM_ROUND2_NOT_RUN (round 2 runs     */
+                          /* only when C1 = 1 and OOM_jd1 = 0)              */
+  uint8_t _pad[5];
+} xm_run;
+
+typedef struct {
+  uint64_t n;             /* N runs                                                */
+  uint64_t n_mre;         /* runs with OOM_jd1 = 0 (the MRE selection)       */
+  double mre;             /* median of error_jde2 if OOM_jde2 = 0 else error_jde1; */
+                          /* even count: mean of the central pair; NaN if none     */
+  double pef1, pef2;      /* (N - sum C_1) / N and (N - sum C_2) / N                */
+  double mcp;             /* mean of M_save (bytes, signed)                         */
+  int64_t sum_save;       /* exact sum of M_save                                    */
+  uint64_t sum_c1, sum_c2;
+} xm_metrics;
+
+/* Device scratch needed for n runs (host-only computation). */
+size_t xm_metrics_scratch_bytes(int64_t n_runs);
+/*
+ * Evaluate the metrics of d_runs[n] (DEVICE) into *h_out (HOST); synchronises
+ * `stream`. Errors: XM_EINVAL for n == 0 (SPEC.md:386 no-data), null
+ * pointers, or an invalid record (round-2 fields where P:385's gating excludes
+ * round 2; a zero measured peak that the MRE would divide by);
+ * XM_ENOMEM (scratch too small); XM_ECUDA. Floating point: fp64, each error
+ * computed as double(|est - meas|) / double(meas).
+ */
+int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch, size_t scratch_bytes,
+                     xm_metrics* h_out, void* stream);
+
 /* Number of device kernel launches the last xm_simulate_batch on this thread */
 /* issued (for the bench's gpu_launches claim).                               */
 int xm_last_launch_count(void);

@@ -68,6 +68,20 @@ class _Summary(ctypes.Structure):
                  "max_peak_allocated", "sum_peak_reserved", "n_predicted_oom")]
 
 
+class _Metrics(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("n_mre", ctypes.c_uint64), ("mre", ctypes.c_double),
+                ("pef1", ctypes.c_double), ("pef2", ctypes.c_double), ("mcp", ctypes.c_double),
+                ("sum_save", ctypes.c_int64), ("sum_c1", ctypes.c_uint64), ("sum_c2", ctypes.c_uint64)]
+
+
+# xm_run (include/xmem.h): one evaluated run, 40 B
+RUN_DTYPE = np.dtype([("m_peak_est", "<u8"), ("m_peak_meas1", "<u8"), ("m_peak_meas2", "<u8"),
+                      ("m_max", "<u8"), ("oom_pred", "u1"), ("oom1", "u1"), ("oom2", "u1"),
+                      ("_pad", "u1", (5,))])
+assert RUN_DTYPE.itemsize == 40
+ROUND2_NOT_RUN = 2
+
+
 class _Tpl(ctypes.Structure):
     _fields_ = [("fixed", ctypes.c_void_p), ("per", ctypes.c_void_p), ("tag", ctypes.c_void_p),
                 ("tpl_off", ctypes.c_void_p), ("n_tpl", ctypes.c_int64)]
@@ -124,6 +138,9 @@ def lib():
         L.xm_host_ws_bytes.argtypes = [P, ctypes.POINTER(_Cfg)]
         L.xm_host_ws_bytes.restype = ctypes.c_size_t
         L.xm_simulate_host.argtypes = [P, P, ctypes.POINTER(_Cfg), P, ctypes.c_size_t, P, P]
+        L.xm_metrics_scratch_bytes.argtypes = [I64]
+        L.xm_metrics_scratch_bytes.restype = ctypes.c_size_t
+        L.xm_metrics_batch.argtypes = [P, I64, P, ctypes.c_size_t, ctypes.POINTER(_Metrics), P]
         L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
@@ -398,3 +415,24 @@ def expand_again(tp: Templates, db: DeviceBatch, stream=None):
     """Re-run K4 into db's event arrays with its resident descriptors (one
     launch, nothing else: used to time the kernel)."""
     _launch_expand(tp, db._scratch["k4"], db.n_traces, db.bytes, db.tag, stream)
+
+
+# ---- NEXT-4: batched evaluation metrics (xm_metrics_batch) ----------------------
+def metrics(runs, stream=None) -> Dict[str, float]:
+    """MRE / PEF / MCP of N runs. runs: numpy RUN_DTYPE array
+    (copied to the device) or a uint8 device tensor [N, 40]."""
+    import torch
+    if isinstance(runs, np.ndarray):
+        assert runs.dtype == RUN_DTYPE
+        d = torch.from_numpy(np.ascontiguousarray(runs).view(np.uint8).reshape(-1, 40)).cuda()
+    else:
+        d = runs
+    n = d.shape[0]
+    need = int(lib().xm_metrics_scratch_bytes(n))
+    scr = torch.empty(max(need, 256), dtype=torch.uint8, device=d.device)
+    m = _Metrics()
+    rc = lib().xm_metrics_batch(ctypes.c_void_p(d.data_ptr()) if n else None, n,
+                                ctypes.c_void_p(scr.data_ptr()), scr.numel(), ctypes.byref(m),
+                                _stream_ptr(stream))
+    _check(rc, "xm_metrics_batch")
+    return {k: getattr(m, k) for k, _ in _Metrics._fields_}
