@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "xmo.c")
+_SRCS = [_SRC, os.path.join(_HERE, "lifecycle.c")]
 _LIB = os.path.join(_HERE, "libxmo.so")
 
 FIELDS = ["peak_allocated", "peak_allocated_idx", "peak_allocated_blk", "peak_allocated_blk_idx",
@@ -73,10 +74,11 @@ class Config:
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or \
+            os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, *_SRCS])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -99,6 +101,7 @@ def lib():
             getattr(L, f).restype = ctypes.c_uint64
         L.xmo_is_small.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Cfg)]
         L.xmo_should_split.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(_Cfg)]
+        L.xmo_reconstruct.argtypes = [P, P, ctypes.c_int64, P, P, P]
         assert L.xmo_nfields() == NF
         _lib = L
     return _lib
@@ -194,3 +197,38 @@ def simulate_batch_parallel(batch, cfg: Config = Config(), workers: Optional[int
     with ctx.Pool(workers) as pool:
         parts = pool.map(_worker, jobs)
     return {k: np.concatenate([p[k] for p in parts]) for k in FIELDS}
+
+
+# ---- lifecycle reconstruction (oracle/lifecycle.c) -------------
+LIFECYCLE_TALLIES = ["n_blocks", "n_orphan", "n_mismatch", "n_persistent", "n_kept", "max_open"]
+
+
+def reconstruct(addr: np.ndarray, bytes_: np.ndarray):
+    """One trace of instants -> (partner int64[n], mismatch uint8[n], tallies dict)."""
+    a = np.ascontiguousarray(addr, np.uint64)
+    b = np.ascontiguousarray(bytes_, np.int64)
+    n = len(b)
+    partner = np.zeros(n, np.int64)
+    mism = np.zeros(n, np.uint8)
+    t = np.zeros(6, np.uint64)
+    rc = lib().xmo_reconstruct(_ptr(a), _ptr(b), n, _ptr(partner), _ptr(mism), _ptr(t))
+    if rc:
+        raise OracleError(rc, 0)
+    return partner, mism, {k: int(v) for k, v in zip(LIFECYCLE_TALLIES, t)}
+
+
+def wire_from_partner(bytes_: np.ndarray, stream: np.ndarray, partner: np.ndarray):
+    """The replay input a reconstruction defines (the definition, written out):
+    kept events = allocations + matched frees, in order; an allocation keeps
+    its bytes and stream, a matched free becomes -(its block's size) on its
+    block's stream (the wire contract, include/xmem.h xm_batch); block ids =
+    allocation ordinals. Returns (bytes', tag', kept index)."""
+    b = np.asarray(bytes_, np.int64)
+    st = np.asarray(stream, np.uint32)
+    is_alloc = b > 0
+    kept = np.flatnonzero(is_alloc | (partner >= 0))
+    ordinal = np.cumsum(is_alloc) - 1
+    out_b = np.where(is_alloc[kept], b[kept], -b[np.maximum(partner[kept], 0)])
+    blk = np.where(is_alloc[kept], kept, partner[kept])
+    out_t = (ordinal[blk].astype(np.uint32) | (st[blk] << np.uint32(28))).astype(np.uint32)
+    return out_b.astype(np.int64), out_t, kept
