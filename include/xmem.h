@@ -329,6 +329,60 @@ size_t xm_metrics_scratch_bytes(int64_t n_runs);
 int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch, size_t scratch_bytes,
                      xm_metrics* h_out, void* stream);
 
+/*
+ * Lifecycle reconstruction (the Analyzer step two
+ * before the Simulator): pair the profiler's memory instants (address, signed
+ * bytes, in time order) into blocks -- "pairing allocation and deallocation
+ * events based on address tracking and timing ... correctly handling address
+ * reuse. Blocks lacking a deallocation event are considered persistent"
+ * (§3.2). Rules: a free closes the most
+ * recently opened still-open block at its address (LIFO, D1); none open ->
+ * orphan (tallied, dropped); |bytes| != the block's size -> mismatch
+ * (tallied; the block is closed with its own size).
+ */
+typedef struct {
+  const uint64_t* addr;     /* [n_events] DEVICE: the instant's address                   */
+  const int64_t* bytes;     /* [n_events] DEVICE: +size allocation, -size deallocation;    */
+                            /* 0 is invalid (counted in n_invalid, otherwise ignored)      */
+  const uint8_t* stream;    /* [n_events] DEVICE stream (0..15) or NULL (all 0)            */
+  const int64_t* off;       /* [n_traces+1] DEVICE: trace t = instants [off[t], off[t+1])  */
+  int64_t n_traces, n_events;
+  uint32_t max_events;      /* longest trace (host value; sizes the scratch)               */
+} xm_instants;
+
+typedef struct {            /* per trace, 56 bytes                                         */
+  uint64_t n_blocks;        /* allocations                                                 */
+  uint64_t n_orphan;        /* frees with no open block at their address                   */
+  uint64_t n_mismatch;      /* matched frees whose |bytes| differs from the block's size   */
+  uint64_t n_persistent;    /* blocks never closed                                         */
+  uint64_t n_kept;          /* allocations + matched frees = replay events of the trace    */
+  uint64_t n_invalid;       /* zero-byte instants                                          */
+  uint32_t max_open;        /* most blocks open at once                                    */
+  uint32_t n_ids;           /* dense id space of the wire trace (<= max_open + 31)         */
+} xm_lifecycle;
+
+size_t xm_reconstruct_scratch_bytes(const xm_instants* in);
+/*
+ * Reconstruct every trace (asynchronous on `stream`; 1 launch, 3 with wire
+ * output). Outputs, DEVICE, caller-owned:
+ *   d_partner[n_events] int32, trace-local index: for an allocation the free
+ *     that closes it (-1 = persistent), for a free the allocation it closes
+ *     (-1 = orphan); d_mismatch[n_events] 1 on a mismatched free;
+ *   d_rec[n_traces] per-trace tallies;
+ *   optional wire output (all four or none): the replay input the
+ *     reconstruction defines -- per trace, its allocations and matched frees
+ *     in order, a free carrying -(its block's size) and its block's stream,
+ *     block ids dense (reused only after the block is closed) -- as
+ *     d_wire_bytes / d_wire_tag [<= n_events], d_wire_off [n_traces+1],
+ *     d_wire_nids [n_traces]: an xm_batch without order (any permutation).
+ * Errors: XM_EINVAL (null / negative), XM_ERANGE (a trace of >= 2^31
+ * instants), XM_ENOMEM (scratch), XM_ECUDA.
+ */
+int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scratch_bytes,
+                   int32_t* d_partner, uint8_t* d_mismatch, xm_lifecycle* d_rec,
+                   int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
+                   uint32_t* d_wire_nids, void* stream);
+
 /* Number of device kernel launches the last xm_simulate_batch on this thread */
 /* issued (for the bench's gpu_launches claim).                               */
 int xm_last_launch_count(void);

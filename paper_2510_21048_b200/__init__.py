@@ -82,6 +82,19 @@ assert RUN_DTYPE.itemsize == 40
 ROUND2_NOT_RUN = 2
 
 
+class _Instants(ctypes.Structure):
+    _fields_ = [("addr", ctypes.c_void_p), ("bytes", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+                ("off", ctypes.c_void_p), ("n_traces", ctypes.c_int64), ("n_events", ctypes.c_int64),
+                ("max_events", ctypes.c_uint32)]
+
+
+# xm_lifecycle (include/xmem.h): per-trace reconstruction tallies, 56 B
+LIFECYCLE_DTYPE = np.dtype([("n_blocks", "<u8"), ("n_orphan", "<u8"), ("n_mismatch", "<u8"),
+                            ("n_persistent", "<u8"), ("n_kept", "<u8"), ("n_invalid", "<u8"),
+                            ("max_open", "<u4"), ("n_ids", "<u4")])
+assert LIFECYCLE_DTYPE.itemsize == 56
+
+
 class _Tpl(ctypes.Structure):
     _fields_ = [("fixed", ctypes.c_void_p), ("per", ctypes.c_void_p), ("tag", ctypes.c_void_p),
                 ("tpl_off", ctypes.c_void_p), ("n_tpl", ctypes.c_int64)]
@@ -141,6 +154,9 @@ def lib():
         L.xm_metrics_scratch_bytes.argtypes = [I64]
         L.xm_metrics_scratch_bytes.restype = ctypes.c_size_t
         L.xm_metrics_batch.argtypes = [P, I64, P, ctypes.c_size_t, ctypes.POINTER(_Metrics), P]
+        L.xm_reconstruct_scratch_bytes.argtypes = [ctypes.POINTER(_Instants)]
+        L.xm_reconstruct_scratch_bytes.restype = ctypes.c_size_t
+        L.xm_reconstruct.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 8
         L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
@@ -436,3 +452,72 @@ def metrics(runs, stream=None) -> Dict[str, float]:
                                 _stream_ptr(stream))
     _check(rc, "xm_metrics_batch")
     return {k: getattr(m, k) for k, _ in _Metrics._fields_}
+
+
+# ---- NEXT-3: lifecycle reconstruction (xm_reconstruct) ---------------------------
+@dataclass
+class DeviceInstants:
+    addr: "object"        # uint64 as int64 tensor [E]
+    bytes: "object"       # int64 [E]
+    stream: "object"      # uint8 [E] or None
+    off: "object"         # int64 [T+1]
+    n_traces: int
+    n_events: int
+    max_events: int
+
+    @staticmethod
+    def from_host(addr, bytes_, stream, off, device=None) -> "DeviceInstants":
+        import torch
+        device = torch.device(device or "cuda")
+        off = np.ascontiguousarray(off, np.int64)
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(device)
+        lens = np.diff(off)
+        return DeviceInstants(t(np.asarray(addr, np.uint64).view(np.int64), np.int64),
+                              t(bytes_, np.int64),
+                              t(stream, np.uint8) if stream is not None else None, t(off, np.int64),
+                              len(off) - 1, int(off[-1]), int(lens.max()) if len(lens) else 0)
+
+    def c(self) -> _Instants:
+        def p(x):
+            return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
+        return _Instants(p(self.addr), p(self.bytes), p(self.stream), p(self.off), self.n_traces,
+                         self.n_events, self.max_events)
+
+
+def reconstruct(ins: DeviceInstants, wire: bool = True, stream=None, scratch=None):
+    """xm_reconstruct: partner / mismatch (device int32 / uint8 tensors), the
+    per-trace tallies (numpy LIFECYCLE_DTYPE) and, with wire=True, the replay
+    batch the reconstruction defines (DeviceBatch, stored in trace order)."""
+    import torch
+    dev = ins.off.device
+    c = ins.c()
+    need = int(lib().xm_reconstruct_scratch_bytes(ctypes.byref(c)))
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    E, T = ins.n_events, ins.n_traces
+    partner = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    mism = torch.empty(max(E, 1), dtype=torch.uint8, device=dev)
+    rec = torch.empty((max(T, 1), 56), dtype=torch.uint8, device=dev)
+    wb = wt = wo = wn = None
+    if wire:
+        wb = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+        wt = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+        wo = torch.empty(T + 1, dtype=torch.int64, device=dev)
+        wn = torch.empty(max(T, 1), dtype=torch.int32, device=dev)
+
+    def p(x):
+        return ctypes.c_void_p(x.data_ptr()) if x is not None else None
+    rc = lib().xm_reconstruct(ctypes.byref(c), ctypes.c_void_p(scratch.data_ptr()), scratch.numel(),
+                              p(partner), p(mism), p(rec), p(wb), p(wt), p(wo), p(wn),
+                              _stream_ptr(stream))
+    _check(rc, "xm_reconstruct")
+    r = rec[:T].cpu().numpy().reshape(-1).view(LIFECYCLE_DTYPE) if T else np.zeros(0, LIFECYCLE_DTYPE)
+    batch = None
+    if wire:
+        import torch as _t
+        order = _t.arange(T, dtype=_t.int32, device=dev)
+        n_wire = int(r["n_kept"].sum()) if T else 0
+        batch = DeviceBatch(wb[:max(n_wire, 0)], wt[:max(n_wire, 0)], wo, wn[:T], order, None, T,
+                            n_wire, int(r["n_ids"].max()) if T else 0,
+                            int(r["n_kept"].max()) if T else 0)
+    return partner[:E], mism[:E], r, batch

@@ -1,0 +1,384 @@
+// lifecycle.cu -- K5: batched lifecycle reconstruction,
+// the Analyzer step two before the Simulator: "pairing allocation and
+// deallocation events based on address tracking and timing ... while
+// correctly handling address reuse. Blocks lacking a deallocation event are
+// considered persistent" (§3.2); SPEC.md:104-112 (LIFO per
+// address, orphan and mismatch tallies). Its output is also the replay's
+// input: the kept events (allocations + matched frees) in the xm_batch wire
+// format with dense block ids, so profiler instants go to k_replay without a
+// host round trip.
+//
+//   k_reconstruct  one warp per trace (persistent grid), 32-instant tiles:
+//     * allocations take dense ids at the tile start from a per-warp free-id
+//       stack (ids freed in earlier tiles; then fresh ids), so an id is never
+//       reused while its block is open and n_ids <= max open + 31;
+//     * matching: a per-warp open-addressing hash table in global memory maps
+//       address -> top of that address's stack of open blocks (linked through
+//       the allocations' event indices), tagged with a per-trace generation so
+//       it is cleared once per call, not per trace. When the tile's addresses are distinct (the common
+//       case: __match_any_sync) every lane does its own lookup, insertions are
+//       resolved by a read phase / claim phase loop; otherwise the tile runs
+//       one instant at a time;
+//     * per instant: partner (alloc <-> free, -1 persistent / orphan),
+//       mismatch flag; kept events are written compacted within the trace at
+//       its input offset (staging), ids of matched blocks go back on the stack;
+//   k_wire_offsets  one CTA: exclusive scan of the kept counts -> wire offsets;
+//   k_wire_compact  one warp per trace: staging -> dense wire arrays, n_ids.
+// HBM: 17 B/instant read, 5 B written (partner, mismatch) + 12 B staging write
+// and read + 12 B wire write; hash probes and the stack links hit L2.
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "xm_internal.h"
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kWarps = 8;                 // per CTA; scratch is per warp slot
+
+struct Slot {                             // 16 B hash slot
+  unsigned long long addr;
+  unsigned int gen;                       // trace index + 1 that owns it (0 = never)
+  int top;                                // local index of the top open block, -1 none
+};
+
+struct LParams {
+  const uint64_t* __restrict__ addr;
+  const int64_t* __restrict__ bytes;
+  const uint8_t* __restrict__ stream;
+  const int64_t* __restrict__ off;
+  int64_t n_traces;
+  uint32_t hbits;                         // log2 slots per warp table
+  Slot* tables;                           // [n_slots][1 << hbits]
+  uint32_t* idstacks;                     // [n_slots][max_events]
+  uint32_t max_events;
+  int* below;                             // [n_events] stack link of an allocation
+  uint32_t* id_of;                        // [n_events] dense id of an allocation
+  int64_t* st_bytes;                      // [n_events] staging (trace-compacted wire)
+  uint32_t* st_tag;
+  int32_t* partner;
+  uint8_t* mismatch;
+  xm_lifecycle* rec;
+  unsigned int* work;
+};
+
+__device__ __forceinline__ uint32_t hash_addr(uint64_t a, uint32_t bits) {
+  return uint32_t((a * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+}
+
+// One instant, done by one lane: the sequential definition (probe, insert if
+// absent, push or pop). Used when addresses repeat inside a tile.
+__device__ __forceinline__ void op_serial(const LParams& P, Slot* T, uint32_t hmask,
+                                          uint32_t hbits, unsigned gen, int64_t e0, int li,
+                                          uint64_t a, int64_t b, bool& matched, int& blk) {
+  uint32_t h = hash_addr(a, hbits);
+  for (;;) {
+    if (T[h].gen != gen) break;
+    if (T[h].addr == a) break;
+    h = (h + 1) & hmask;
+  }
+  const bool found = T[h].gen == gen;
+  if (b > 0) {
+    if (!found) { T[h].addr = a; T[h].gen = gen; T[h].top = -1; }
+    P.below[e0 + li] = T[h].top;
+    T[h].top = li;
+  } else if (found && T[h].top >= 0) {
+    blk = T[h].top;
+    T[h].top = P.below[e0 + blk];
+    matched = true;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t slot = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  Slot* T = P.tables + (size_t(slot) << P.hbits);
+  uint32_t* ids = P.idstacks + size_t(slot) * P.max_events;
+  const uint32_t hmask = (1u << P.hbits) - 1u;
+  for (;;) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(P.work, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (int64_t(k) >= P.n_traces) break;
+    const unsigned gen = k + 1;
+    const int64_t e0 = P.off[k];
+    const int n = int(P.off[k + 1] - e0);
+    uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
+    unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int li = base + int(lane);
+      const bool valid = li < n;
+      const uint64_t a = valid ? P.addr[e0 + li] : ~0ull - lane;
+      const int64_t b = valid ? P.bytes[e0 + li] : 0;
+      const uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
+      const bool is_alloc = b > 0, is_free = b < 0;
+      // ---- dense ids for this tile's allocations (ids freed before the tile) ----
+      const unsigned am = __ballot_sync(kFull, is_alloc);
+      const uint32_t na = __popc(am), ka = __popc(am & lt);
+      const uint32_t take = min(na, top);
+      if (is_alloc) {
+        const uint32_t id = ka < take ? ids[top - 1 - ka] : fresh + (ka - take);
+        P.id_of[e0 + li] = id;
+        P.partner[e0 + li] = -1;
+        P.mismatch[e0 + li] = 0;
+      }
+      top -= take;
+      fresh += na - take;
+      __syncwarp();
+      // ---- matching (LIFO per address) ----
+      bool matched = false;
+      int blk = -1;
+      const unsigned grp = __match_any_sync(kFull, a);
+      const bool repeat = __any_sync(kFull, valid && __popc(grp) > 1);
+      if (!repeat) {
+        // read phase: find my key or the first free slot of my probe sequence
+        uint32_t h = hash_addr(a, P.hbits);
+        bool found = false;
+        if (valid) {
+          for (;;) {
+            if (T[h].gen != gen) break;
+            if (T[h].addr == a) { found = true; break; }
+            h = (h + 1) & hmask;
+          }
+        }
+        // claim phase for allocations at new addresses: lanes aiming at the
+        // same free slot -> the lowest wins, the others probe on
+        bool pend = is_alloc && !found;
+        while (__any_sync(kFull, pend)) {
+          const unsigned same = __match_any_sync(kFull, pend ? h : 0xFFFFFFFFu);
+          const bool win = pend && (__ffs(same) - 1) == int(lane);
+          __syncwarp();
+          if (win) { T[h].addr = a; T[h].gen = gen; T[h].top = -1; }
+          __syncwarp();
+          if (pend && !win) {
+            h = (h + 1) & hmask;
+            for (;;) {                       // next free slot (or, never, my key)
+              if (T[h].gen != gen) break;
+              h = (h + 1) & hmask;
+            }
+          }
+          pend = pend && !win;
+        }
+        __syncwarp();
+        if (is_alloc) {
+          P.below[e0 + li] = T[h].top;
+          T[h].top = li;
+        } else if (is_free && found && T[h].top >= 0) {
+          blk = T[h].top;
+          T[h].top = P.below[e0 + blk];
+          matched = true;
+        }
+      } else {
+        const int cnt = min(32, n - base);
+        for (int j = 0; j < cnt; ++j) {
+          if (int(lane) == j && b != 0) op_serial(P, T, hmask, P.hbits, gen, e0, li, a, b, matched, blk);
+          __syncwarp();
+        }
+      }
+      __syncwarp();
+      // ---- per-instant outputs ----
+      bool mism = false;
+      if (is_free) {
+        P.partner[e0 + li] = matched ? blk : -1;
+        if (matched) {
+          P.partner[e0 + blk] = li;
+          mism = P.bytes[e0 + blk] != -b;
+        }
+        P.mismatch[e0 + li] = mism ? 1 : 0;
+      } else if (valid && b == 0) {
+        P.partner[e0 + li] = -1;
+        P.mismatch[e0 + li] = 0;
+      }
+      __syncwarp();
+      // ---- matched blocks' ids go back on the stack ----
+      const unsigned mm = __ballot_sync(kFull, matched);
+      if (matched) ids[top + __popc(mm & lt)] = P.id_of[e0 + blk];
+      top += __popc(mm);
+      // ---- staging: kept events, compacted within the trace ----
+      const bool kept = is_alloc || matched;
+      const unsigned km = __ballot_sync(kFull, kept);
+      if (kept) {
+        const int64_t dst = e0 + int64_t(n_kept) + __popc(km & lt);
+        if (is_alloc) {
+          P.st_bytes[dst] = b;
+          P.st_tag[dst] = P.id_of[e0 + li] | (s << 28);
+        } else {
+          const uint32_t sb = P.stream ? P.stream[e0 + blk] : 0u;
+          P.st_bytes[dst] = -P.bytes[e0 + blk];          // the block's size
+          P.st_tag[dst] = P.id_of[e0 + blk] | (sb << 28);
+        }
+      }
+      // ---- open count (max open = the minimal id space) ----
+      int d = is_alloc ? 1 : (matched ? -1 : 0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, d, o);
+        if (int(lane) >= o) d += y;
+      }
+      const uint32_t mo = __reduce_max_sync(kFull, uint32_t(int(open) + d));
+      max_open = max(max_open, mo);
+      open = uint32_t(int(open) + __shfl_sync(kFull, d, 31));
+      n_blocks += na;
+      n_matched += __popc(mm);
+      n_kept += __popc(km);
+      n_orphan += __popc(__ballot_sync(kFull, is_free && !matched));
+      n_mism += __popc(__ballot_sync(kFull, mism));
+      n_inv += __popc(__ballot_sync(kFull, valid && b == 0));
+      __syncwarp();
+    }
+    if (lane == 0) {
+      xm_lifecycle r;
+      r.n_blocks = n_blocks;
+      r.n_orphan = n_orphan;
+      r.n_mismatch = n_mism;
+      r.n_persistent = n_blocks - n_matched;
+      r.n_kept = n_kept;
+      r.n_invalid = n_inv;
+      r.max_open = max_open;
+      r.n_ids = fresh;
+      P.rec[k] = r;
+    }
+    __syncwarp();
+  }
+}
+
+// exclusive scan of rec[t].n_kept -> woff[T+1] (one CTA; T <= 2^31)
+__global__ void __launch_bounds__(1024) k_wire_offsets(const xm_lifecycle* rec, int64_t T,
+                                                       int64_t* woff) {
+  __shared__ long long part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (T + 1023) / 1024;
+  const int64_t a = min(T, int64_t(tid) * per), z = min(T, a + per);
+  long long s = 0;
+  for (int64_t t = a; t < z; ++t) s += (long long)rec[t].n_kept;
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {            // Hillis-Steele inclusive scan
+    const long long v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  long long run = part[tid] - s;
+  for (int64_t t = a; t < z; ++t) {
+    woff[t] = run;
+    run += (long long)rec[t].n_kept;
+  }
+  if (tid == 1023) woff[T] = part[1023];
+}
+
+__global__ void k_wire_compact(const int64_t* __restrict__ off, const int64_t* __restrict__ woff,
+                               const xm_lifecycle* __restrict__ rec, const int64_t* st_bytes,
+                               const uint32_t* st_tag, int64_t T, int64_t* w_bytes,
+                               uint32_t* w_tag, uint32_t* w_nids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = w0; t < T; t += nw) {
+    const int64_t src = off[t], dst = woff[t], m = woff[t + 1] - dst;
+    for (int64_t j = lane; j < m; j += 32) {
+      w_bytes[dst + j] = st_bytes[src + j];
+      w_tag[dst + j] = st_tag[src + j];
+    }
+    if (lane == 0) w_nids[t] = rec[t].n_ids;
+  }
+}
+
+struct Layout {
+  uint32_t hbits, n_slots, ctas;
+  size_t tables, stacks, below, id_of, st_bytes, st_tag, total;
+};
+
+Layout layout(const xm_instants* in) {
+  Layout L{};
+  int dev = 0, sms = 148;
+  if (xm_internal::cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  const int64_t want_ctas = (in->n_traces + kWarps - 1) / kWarps;
+  L.ctas = uint32_t(want_ctas < sms ? (want_ctas > 0 ? want_ctas : 1) : sms);
+  L.n_slots = L.ctas * kWarps;
+  uint32_t hb = 6;
+  while ((1ull << hb) < 2ull * in->max_events) ++hb;
+  L.hbits = hb;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t o = 256;                                   // header: work counter
+  L.tables = o; o += al((size_t(L.n_slots) << hb) * sizeof(Slot));
+  L.stacks = o; o += al(size_t(L.n_slots) * (in->max_events ? in->max_events : 1) * 4);
+  const size_t E = size_t(in->n_events > 0 ? in->n_events : 1);
+  L.below = o; o += al(E * 4);
+  L.id_of = o; o += al(E * 4);
+  L.st_bytes = o; o += al(E * 8);
+  L.st_tag = o; o += al(E * 4);
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+using namespace xm_internal;
+
+extern "C" size_t xm_reconstruct_scratch_bytes(const xm_instants* in) {
+  if (!in || in->n_traces < 0 || in->n_events < 0) return 0;
+  return layout(in).total;
+}
+
+extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scratch_bytes,
+                              int32_t* d_partner, uint8_t* d_mismatch, xm_lifecycle* d_rec,
+                              int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
+                              uint32_t* d_wire_nids, void* stream) {
+  launch_counter() = 0;
+  if (!in || in->n_traces < 0 || in->n_events < 0)
+    return set_error(XM_EINVAL, "xm_reconstruct: bad arguments");
+  if (in->n_events > 0x7FFFFFFFll || in->max_events > 0x7FFFFFFFu)
+    return set_error(XM_ERANGE, "xm_reconstruct: trace longer than 2^31-1 instants");
+  if (in->n_traces == 0) return XM_OK;
+  if (!in->off || (in->n_events > 0 && (!in->addr || !in->bytes)) || !d_partner || !d_mismatch ||
+      !d_rec || !d_scratch)
+    return set_error(XM_EINVAL, "xm_reconstruct: null pointer");
+  const bool wire = d_wire_bytes || d_wire_tag || d_wire_off || d_wire_nids;
+  if (wire && !(d_wire_bytes && d_wire_tag && d_wire_off && d_wire_nids))
+    return set_error(XM_EINVAL, "xm_reconstruct: wire outputs must be all set or all NULL");
+  const Layout L = layout(in);
+  if (scratch_bytes < L.total) return set_error(XM_ENOMEM, "xm_reconstruct: scratch too small");
+  if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(d_scratch);
+  // zero the header and the hash tables (generation 0 = never used)
+  cudaError_t e = cudaMemsetAsync(base, 0, L.stacks, st);
+  if (e != cudaSuccess) return set_error(XM_ECUDA, cudaGetErrorString(e));
+  LParams P{};
+  P.addr = in->addr;
+  P.bytes = in->bytes;
+  P.stream = in->stream;
+  P.off = in->off;
+  P.n_traces = in->n_traces;
+  P.hbits = L.hbits;
+  P.tables = reinterpret_cast<Slot*>(base + L.tables);
+  P.idstacks = reinterpret_cast<uint32_t*>(base + L.stacks);
+  P.max_events = in->max_events ? in->max_events : 1;
+  P.below = reinterpret_cast<int*>(base + L.below);
+  P.id_of = reinterpret_cast<uint32_t*>(base + L.id_of);
+  P.st_bytes = reinterpret_cast<int64_t*>(base + L.st_bytes);
+  P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
+  P.partner = d_partner;
+  P.mismatch = d_mismatch;
+  P.rec = d_rec;
+  P.work = reinterpret_cast<unsigned int*>(base);
+  k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
+  int launches = 1;
+  if (wire) {
+    k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, in->n_traces, d_wire_off);
+    const int64_t want = (in->n_traces + 7) / 8;
+    const int g = int(want < int64_t(L.ctas) * 8 ? want : int64_t(L.ctas) * 8);
+    k_wire_compact<<<g > 0 ? g : 1, 256, 0, st>>>(in->off, d_wire_off, d_rec, P.st_bytes, P.st_tag,
+                                                  in->n_traces, d_wire_bytes, d_wire_tag, d_wire_nids);
+    launches += 2;
+  }
+  launch_counter() = launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct: ") + cudaGetErrorString(e));
+  return XM_OK;
+}
