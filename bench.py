@@ -152,6 +152,21 @@ def ncu_traffic(kernel="k_replay"):
         return None, None
 
 
+def ncu_issue(kernel="k_replay"):
+    """Warp-issue efficiency (smsp__issue_active %) and warp-instructions per
+    launch from the committed ncu summary (the north_star's second measure)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            k = json.load(f)["kernels"][kernel]
+        return {"issue_active_pct": k["issue_active_pct"],
+                "warp_instructions_per_launch": k["warp_instructions"],
+                "achieved_occupancy_pct": k["achieved_occupancy_pct"],
+                "source": "profiles/ncu_summary.json (" + k.get("source", "") + ")"}
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- cpu oracle
 def oracle_rate(batch, cores=None, passes=1):
     """The oracle as it stands (oracle/xmo.c), traces spread over host processes."""
@@ -348,9 +363,10 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "kernel": "k_replay",
             "alg_bytes_per_launch": alg, "kernel_ms": kern_ms, "peak_source": peak_src,
-            "traffic_source": tsrc,
+            "traffic_source": tsrc, "issue": ncu_issue(),
             "note": "K2 is a serial integer state machine per trace (issue/latency-bound); "
-                    "HBM fraction reported as the north_star asks"}
+                    "HBM fraction reported as the north_star asks, warp-issue efficiency "
+                    "from ncu in 'issue'"}
 
     # ---- K1 (XM_ALLOCATED_ONLY: segmented prefix-scan/max), the HBM-bound kernel,
     # timed on the same resident events (capacities dropped: the mode needs none)

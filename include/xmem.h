@@ -363,25 +363,34 @@ typedef struct {            /* per trace, 56 bytes                              
 
 size_t xm_reconstruct_scratch_bytes(const xm_instants* in);
 /*
- * Reconstruct every trace (asynchronous on `stream`; 1 launch, 3 with wire
- * output). Outputs, DEVICE, caller-owned:
+ * Reconstruct every trace (asynchronous on `stream`, one launch). Outputs,
+ * DEVICE, caller-owned:
  *   d_partner[n_events] int32, trace-local index: for an allocation the free
  *     that closes it (-1 = persistent), for a free the allocation it closes
  *     (-1 = orphan); d_mismatch[n_events] 1 on a mismatched free;
- *   d_rec[n_traces] per-trace tallies;
- *   optional wire output (all four or none): the replay input the
- *     reconstruction defines -- per trace, its allocations and matched frees
- *     in order, a free carrying -(its block's size) and its block's stream,
- *     block ids dense (reused only after the block is closed) -- as
- *     d_wire_bytes / d_wire_tag [<= n_events], d_wire_off [n_traces+1],
- *     d_wire_nids [n_traces]: an xm_batch without order (any permutation).
- * Errors: XM_EINVAL (null / negative), XM_ERANGE (a trace of >= 2^31
- * instants), XM_ENOMEM (scratch), XM_ECUDA.
+ *   d_rec[n_traces] per-trace tallies.
+ * d_scratch (>= xm_reconstruct_scratch_bytes) also keeps the replay trace each
+ * reconstruction defines, for xm_reconstruct_wire. Errors: XM_EINVAL (null /
+ * negative), XM_ERANGE (a trace of >= 2^31 instants), XM_ENOMEM (scratch),
+ * XM_ECUDA.
  */
 int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scratch_bytes,
-                   int32_t* d_partner, uint8_t* d_mismatch, xm_lifecycle* d_rec,
-                   int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
-                   uint32_t* d_wire_nids, void* stream);
+                   int32_t* d_partner, uint8_t* d_mismatch, xm_lifecycle* d_rec, void* stream);
+/*
+ * After xm_reconstruct (same `in`, same scratch, d_rec its output): write the
+ * replay input the reconstruction defines -- per trace, its allocations and
+ * matched frees in order, a free carrying -(its block's size) and its block's
+ * stream, block ids dense (reused only after their block closes) -- as an
+ * xm_batch's arrays, traces STORED in the order d_order[n_traces] (stored ->
+ * caller index, a permutation; NULL = identity; e.g. longest first by
+ * d_rec[].n_kept, as xm_load_traces stores). Outputs, DEVICE, caller-owned:
+ * d_wire_bytes / d_wire_tag [sum n_kept], d_wire_off [n_traces+1],
+ * d_wire_nids [n_traces] (stored order). Two launches, asynchronous.
+ */
+int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch, size_t scratch_bytes,
+                        const xm_lifecycle* d_rec, const uint32_t* d_order,
+                        int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
+                        uint32_t* d_wire_nids, void* stream);
 
 /* Number of device kernel launches the last xm_simulate_batch on this thread */
 /* issued (for the bench's gpu_launches claim).                               */

@@ -156,7 +156,8 @@ def lib():
         L.xm_metrics_batch.argtypes = [P, I64, P, ctypes.c_size_t, ctypes.POINTER(_Metrics), P]
         L.xm_reconstruct_scratch_bytes.argtypes = [ctypes.POINTER(_Instants)]
         L.xm_reconstruct_scratch_bytes.restype = ctypes.c_size_t
-        L.xm_reconstruct.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 8
+        L.xm_reconstruct.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 4
+        L.xm_reconstruct_wire.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 7
         L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
@@ -508,14 +509,18 @@ def reconstruct(ins: DeviceInstants, wire: bool = True, stream=None, scratch=Non
     def p(x):
         return ctypes.c_void_p(x.data_ptr()) if x is not None else None
     rc = lib().xm_reconstruct(ctypes.byref(c), ctypes.c_void_p(scratch.data_ptr()), scratch.numel(),
-                              p(partner), p(mism), p(rec), p(wb), p(wt), p(wo), p(wn),
-                              _stream_ptr(stream))
+                              p(partner), p(mism), p(rec), _stream_ptr(stream))
     _check(rc, "xm_reconstruct")
     r = rec[:T].cpu().numpy().reshape(-1).view(LIFECYCLE_DTYPE) if T else np.zeros(0, LIFECYCLE_DTYPE)
     batch = None
     if wire:
-        import torch as _t
-        order = _t.arange(T, dtype=_t.int32, device=dev)
+        # stored longest first (ties in trace order), like xm_load_traces stores
+        order_h = np.argsort(-r["n_kept"].astype(np.int64), kind="stable").astype(np.uint32)
+        order = torch.from_numpy(order_h.view(np.int32)).to(dev)
+        rc = lib().xm_reconstruct_wire(ctypes.byref(c), ctypes.c_void_p(scratch.data_ptr()),
+                                       scratch.numel(), p(rec), p(order), p(wb), p(wt), p(wo),
+                                       p(wn), _stream_ptr(stream))
+        _check(rc, "xm_reconstruct_wire")
         n_wire = int(r["n_kept"].sum()) if T else 0
         batch = DeviceBatch(wb[:max(n_wire, 0)], wt[:max(n_wire, 0)], wo, wn[:T], order, None, T,
                             n_wire, int(r["n_ids"].max()) if T else 0,

@@ -63,17 +63,33 @@ __global__ void __launch_bounds__(256) k_expand(EParams P) {
     const int64_t* fx = P.fixed + s0;
     const int64_t* pr = P.per + s0;
     const uint32_t* tg = P.ttag + s0;
-    for (int64_t j = lane; j < n; j += 32) {
-      // candidate flags c(j-2), c(j-1), c(j)
-      const bool cj = j + 1 < n && splitmix64(sg + uint64_t(j) + 1) < P.threshold;
-      const bool cm = j >= 1 && splitmix64(sg + uint64_t(j)) < P.threshold;
-      const bool cmm = j >= 2 && splitmix64(sg + uint64_t(j) - 1) < P.threshold;
-      const uint32_t id = __ldg(tg + j) & 0x0FFFFFFFu;
-      const bool keep_j = cj && !cm && id != (__ldg(tg + j + 1) & 0x0FFFFFFFu);
-      const bool keep_m = cm && !cmm && (__ldg(tg + j - 1) & 0x0FFFFFFFu) != id;
-      const int64_t src = keep_j ? j + 1 : (keep_m ? j - 1 : j);
-      P.bytes[d0 + j] = __ldg(fx + src) + __ldg(pr + src) * b;
-      P.tag[d0 + j] = __ldg(tg + src);
+    // One splitmix64 per event: c(j-1), c(j-2) and the neighbours' ids come
+    // from the adjacent lanes, or from the previous tile's lanes 30-31.
+    bool c31 = false, c30 = false;              // c(base-1), c(base-2)
+    uint32_t id31 = 0xFFFFFFFFu;                // id(base-1)
+    for (int64_t base = 0; base < n; base += 32) {
+      const int64_t j = base + lane;
+      const bool v = j < n;
+      const uint32_t tj = v ? __ldg(tg + j) : 0u;
+      const uint32_t id = tj & 0x0FFFFFFFu;
+      const bool cj = v && j + 1 < n && splitmix64(sg + uint64_t(j) + 1) < P.threshold;
+      bool cm = __shfl_up_sync(0xFFFFFFFFu, cj, 1);
+      bool cmm = __shfl_up_sync(0xFFFFFFFFu, cj, 2);
+      uint32_t idm = __shfl_up_sync(0xFFFFFFFFu, id, 1);
+      uint32_t idp = __shfl_down_sync(0xFFFFFFFFu, id, 1);
+      if (lane == 0) { cm = c31; cmm = c30; idm = id31; }
+      if (lane == 1) cmm = c31;
+      if (lane == 31 && cj) idp = __ldg(tg + j + 1) & 0x0FFFFFFFu;
+      const bool keep_j = cj && !cm && id != idp;             // swap (j, j+1)
+      const bool keep_m = cm && !cmm && idm != id;            // swap (j-1, j)
+      if (v) {
+        const int64_t src = keep_j ? j + 1 : (keep_m ? j - 1 : j);
+        P.bytes[d0 + j] = __ldg(fx + src) + __ldg(pr + src) * b;
+        P.tag[d0 + j] = src == j ? tj : __ldg(tg + src);
+      }
+      c31 = __shfl_sync(0xFFFFFFFFu, cj, 31);
+      c30 = __shfl_sync(0xFFFFFFFFu, cj, 30);
+      id31 = __shfl_sync(0xFFFFFFFFu, id, 31);
     }
   }
 }

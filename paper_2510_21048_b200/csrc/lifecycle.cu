@@ -35,7 +35,7 @@
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kWarps = 8;                 // per CTA; scratch is per warp slot
+constexpr int kWarps = 16;                // per CTA; scratch is per warp slot
 
 struct Slot {                             // 16 B hash slot
   unsigned long long addr;
@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
   const uint32_t slot = blockIdx.x * kWarps + (threadIdx.x >> 5);
   Slot* T = P.tables + (size_t(slot) << P.hbits);
   uint32_t* ids = P.idstacks + size_t(slot) * P.max_events;
-  const uint32_t hmask = (1u << P.hbits) - 1u;
   for (;;) {
     unsigned k = 0;
     if (lane == 0) k = atomicAdd(P.work, 1u);
@@ -105,6 +104,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     const unsigned gen = k + 1;
     const int64_t e0 = P.off[k];
     const int n = int(P.off[k + 1] - e0);
+    // this trace's table: the first 2^hb slots of the warp's region (>= 2n:
+    // at most n distinct addresses, load <= 1/2); other traces' entries in it
+    // carry other generations
+    uint32_t hb = 6;
+    while ((1u << hb) < 2u * uint32_t(n) && hb < P.hbits) ++hb;
+    const uint32_t hmask = (1u << hb) - 1u;
     uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
     unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0;
     for (int base = 0; base < n; base += 32) {
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       const bool repeat = __any_sync(kFull, valid && __popc(grp) > 1);
       if (!repeat) {
         // read phase: find my key or the first free slot of my probe sequence
-        uint32_t h = hash_addr(a, P.hbits);
+        uint32_t h = hash_addr(a, hb);
         bool found = false;
         if (valid) {
           for (;;) {
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       } else {
         const int cnt = min(32, n - base);
         for (int j = 0; j < cnt; ++j) {
-          if (int(lane) == j && b != 0) op_serial(P, T, hmask, P.hbits, gen, e0, li, a, b, matched, blk);
+          if (int(lane) == j && b != 0) op_serial(P, T, hmask, hb, gen, e0, li, a, b, matched, blk);
           __syncwarp();
         }
       }
@@ -244,15 +249,16 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
   }
 }
 
-// exclusive scan of rec[t].n_kept -> woff[T+1] (one CTA; T <= 2^31)
-__global__ void __launch_bounds__(1024) k_wire_offsets(const xm_lifecycle* rec, int64_t T,
+// exclusive scan of rec[order[k]].n_kept over stored k -> woff[T+1] (one CTA)
+__global__ void __launch_bounds__(1024) k_wire_offsets(const xm_lifecycle* rec,
+                                                       const uint32_t* order, int64_t T,
                                                        int64_t* woff) {
   __shared__ long long part[1024];
   const int tid = threadIdx.x;
   const int64_t per = (T + 1023) / 1024;
   const int64_t a = min(T, int64_t(tid) * per), z = min(T, a + per);
   long long s = 0;
-  for (int64_t t = a; t < z; ++t) s += (long long)rec[t].n_kept;
+  for (int64_t t = a; t < z; ++t) s += (long long)rec[order ? order[t] : t].n_kept;
   part[tid] = s;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {            // Hillis-Steele inclusive scan
@@ -264,25 +270,26 @@ __global__ void __launch_bounds__(1024) k_wire_offsets(const xm_lifecycle* rec, 
   long long run = part[tid] - s;
   for (int64_t t = a; t < z; ++t) {
     woff[t] = run;
-    run += (long long)rec[t].n_kept;
+    run += (long long)rec[order ? order[t] : t].n_kept;
   }
   if (tid == 1023) woff[T] = part[1023];
 }
 
 __global__ void k_wire_compact(const int64_t* __restrict__ off, const int64_t* __restrict__ woff,
-                               const xm_lifecycle* __restrict__ rec, const int64_t* st_bytes,
-                               const uint32_t* st_tag, int64_t T, int64_t* w_bytes,
-                               uint32_t* w_tag, uint32_t* w_nids) {
+                               const xm_lifecycle* __restrict__ rec, const uint32_t* order,
+                               const int64_t* st_bytes, const uint32_t* st_tag, int64_t T,
+                               int64_t* w_bytes, uint32_t* w_tag, uint32_t* w_nids) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t t = w0; t < T; t += nw) {
-    const int64_t src = off[t], dst = woff[t], m = woff[t + 1] - dst;
+  for (int64_t k = w0; k < T; k += nw) {               // stored trace k
+    const int64_t t = order ? order[k] : k;
+    const int64_t src = off[t], dst = woff[k], m = woff[k + 1] - dst;
     for (int64_t j = lane; j < m; j += 32) {
       w_bytes[dst + j] = st_bytes[src + j];
       w_tag[dst + j] = st_tag[src + j];
     }
-    if (lane == 0) w_nids[t] = rec[t].n_ids;
+    if (lane == 0) w_nids[k] = rec[t].n_ids;
   }
 }
 
@@ -327,8 +334,7 @@ extern "C" size_t xm_reconstruct_scratch_bytes(const xm_instants* in) {
 
 extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scratch_bytes,
                               int32_t* d_partner, uint8_t* d_mismatch, xm_lifecycle* d_rec,
-                              int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
-                              uint32_t* d_wire_nids, void* stream) {
+                              void* stream) {
   launch_counter() = 0;
   if (!in || in->n_traces < 0 || in->n_events < 0)
     return set_error(XM_EINVAL, "xm_reconstruct: bad arguments");
@@ -338,9 +344,6 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   if (!in->off || (in->n_events > 0 && (!in->addr || !in->bytes)) || !d_partner || !d_mismatch ||
       !d_rec || !d_scratch)
     return set_error(XM_EINVAL, "xm_reconstruct: null pointer");
-  const bool wire = d_wire_bytes || d_wire_tag || d_wire_off || d_wire_nids;
-  if (wire && !(d_wire_bytes && d_wire_tag && d_wire_off && d_wire_nids))
-    return set_error(XM_EINVAL, "xm_reconstruct: wire outputs must be all set or all NULL");
   const Layout L = layout(in);
   if (scratch_bytes < L.total) return set_error(XM_ENOMEM, "xm_reconstruct: scratch too small");
   if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
@@ -368,17 +371,37 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
   k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
-  int launches = 1;
-  if (wire) {
-    k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, in->n_traces, d_wire_off);
-    const int64_t want = (in->n_traces + 7) / 8;
-    const int g = int(want < int64_t(L.ctas) * 8 ? want : int64_t(L.ctas) * 8);
-    k_wire_compact<<<g > 0 ? g : 1, 256, 0, st>>>(in->off, d_wire_off, d_rec, P.st_bytes, P.st_tag,
-                                                  in->n_traces, d_wire_bytes, d_wire_tag, d_wire_nids);
-    launches += 2;
-  }
-  launch_counter() = launches;
+  launch_counter() = 1;
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct: ") + cudaGetErrorString(e));
+  return XM_OK;
+}
+
+extern "C" int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch,
+                                   size_t scratch_bytes, const xm_lifecycle* d_rec,
+                                   const uint32_t* d_order, int64_t* d_wire_bytes,
+                                   uint32_t* d_wire_tag, int64_t* d_wire_off,
+                                   uint32_t* d_wire_nids, void* stream) {
+  launch_counter() = 0;
+  if (!in || in->n_traces < 0 || in->n_events < 0)
+    return set_error(XM_EINVAL, "xm_reconstruct_wire: bad arguments");
+  if (in->n_traces == 0) return XM_OK;
+  if (!in->off || !d_rec || !d_scratch || !d_wire_bytes || !d_wire_tag || !d_wire_off || !d_wire_nids)
+    return set_error(XM_EINVAL, "xm_reconstruct_wire: null pointer");
+  const Layout L = layout(in);
+  if (scratch_bytes < L.total) return set_error(XM_ENOMEM, "xm_reconstruct_wire: scratch too small");
+  if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* base = static_cast<const char*>(d_scratch);
+  k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, d_order, in->n_traces, d_wire_off);
+  const int64_t want = (in->n_traces + 7) / 8;
+  const int g = int(want < int64_t(L.ctas) * 8 ? want : int64_t(L.ctas) * 8);
+  k_wire_compact<<<g > 0 ? g : 1, 256, 0, st>>>(
+      in->off, d_wire_off, d_rec, d_order, reinterpret_cast<const int64_t*>(base + L.st_bytes),
+      reinterpret_cast<const uint32_t*>(base + L.st_tag), in->n_traces, d_wire_bytes, d_wire_tag,
+      d_wire_nids);
+  launch_counter() = 2;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct_wire: ") + cudaGetErrorString(e));
   return XM_OK;
 }

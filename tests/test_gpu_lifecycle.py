@@ -63,6 +63,12 @@ def _check(ins):
     wtag = wb.tag.cpu().numpy().view(np.uint32)
     woff = wb.off.cpu().numpy()
     wnids = wb.n_ids.cpu().numpy().view(np.uint32)
+    order = wb.order.cpu().numpy().view(np.uint32)
+    assert sorted(order.tolist()) == list(range(ins.n_traces))        # a permutation
+    kept = rec["n_kept"].astype(np.int64)
+    assert (np.diff(kept[order]) <= 0).all()                          # longest first
+    pos = np.empty(ins.n_traces, np.int64)
+    pos[order] = np.arange(ins.n_traces)
     o_parts = []
     for t in range(ins.n_traces):
         a, by, st = ins.trace(t)
@@ -74,13 +80,14 @@ def _check(ins):
             assert int(rec[k][t]) == tal[k], (t, k, int(rec[k][t]), tal[k])
         assert tal["max_open"] <= int(rec["n_ids"][t]) <= tal["max_open"] + 31
         ob, ot, kept = oracle.wire_from_partner(by, st, p)
-        gb = wbytes[woff[t]:woff[t + 1]]
-        gt = wtag[woff[t]:woff[t + 1]]
+        q = pos[t]
+        gb = wbytes[woff[q]:woff[q + 1]]
+        gt = wtag[woff[q]:woff[q + 1]]
         assert (gb == ob).all(), t
         assert ((gt >> 28) == (ot >> 28)).all(), t
         # ids: an allocation's id comes back on its own free, never on two open blocks
         gid = gt & 0x0FFFFFFF
-        assert (gid < wnids[t]).all()
+        assert (gid < wnids[q]).all() and wnids[q] == rec["n_ids"][t]
         live = {}
         ordinal_to_id = {}
         for j in range(len(gb)):

@@ -32,3 +32,5 @@ W = 148 * (cfg.warps_per_cta or 12)
 print(f"warp-slot utilisation {busy / (en.max() * W) * 100:.1f}% (sum of trace durations / makespan x {W} warps)")
 for q in (0.5, 0.8, 0.9, 0.95, 1.0):
     print(f"  {q*100:.0f}% of traces done by {np.quantile(en, q):.3f} ms")
+np.savez(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "k2_timing.npz"),
+         start=st, end=en, n=L, done=done, n_ids=tr.n_ids[tr.pos].astype(np.int64), names=np.asarray(b.names))
