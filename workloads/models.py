@@ -351,10 +351,18 @@ class _Tpl:
         self.stream: List[int] = []
         self.live: Dict[int, Tuple[int, int, int]] = {}
         self.next = 0
+        self.marks: List[Tuple[str, int]] = []     # (phase marker, event position)
+        self.kinds: List[str] = []                 # per allocation, in order
 
-    def alloc(self, fixed, per=0, stream=0) -> int:
+    def mark(self, name: str):
+        """A training-loop phase boundary before the next event (the profiler's
+        user_annotation windows)."""
+        self.marks.append((name, len(self.sign)))
+
+    def alloc(self, fixed, per=0, stream=0, kind="act") -> int:
         if fixed + per <= 0:
             fixed = 4
+        self.kinds.append(kind)
         h = self.next
         self.next += 1
         self.live[h] = (fixed, per, stream)
@@ -407,6 +415,21 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
     """Event template: (sign, fixed, per_sample, id, stream) numpy arrays.
 
     micro: small autograd temporaries (alloc+free) per op in forward and backward."""
+    return _build(name, opt, zero_grad, streams, iterations, img, seq, micro).arrays()
+
+
+@lru_cache(maxsize=None)
+def template_phases(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False,
+                    iterations: int = 3, img: int = IMG, seq: int = SEQ, micro: int = 0):
+    """The same template plus its phase markers [(name, position)] and the kind
+    of every allocation (param, data, act, grad, state, temp) -- what a CPU
+    profile's annotations and the Analyzer's attribution provide (PAPER.md:212,
+    240-246)."""
+    T = _build(name, opt, zero_grad, streams, iterations, img, seq, micro)
+    return T.arrays(), tuple(T.marks), tuple(T.kinds)
+
+
+def _build(name, opt, zero_grad, streams, iterations, img, seq, micro):
     ops = model_ops(name, img, seq)
     T = _Tpl()
     s_data = 1 if streams else 0
@@ -417,14 +440,14 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
     for op in ops:
         hs = []
         for shp in op.params:
-            h = T.alloc(shp[0] * shp[1] * F32)
+            h = T.alloc(shp[0] * shp[1] * F32, kind="param")
             params.append((h, shp))
             hs.append(len(params) - 1)
         op_params.append(hs)
     state = []
     if opt == "adagrad":        # Adagrad initialises its state in the constructor
         for (_, shp) in params:
-            state += [T.alloc(x) for x in _opt_state(opt, shp)]
+            state += [T.alloc(x, kind="state") for x in _opt_state(opt, shp)]
     grads: Dict[int, int] = {}
 
     n = len(ops)
@@ -436,11 +459,17 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
             cur = op.out
 
     for it in range(iterations):
+        T.mark("iter_start")
         if zero_grad == "pos1":
+            T.mark("zg_start")
             for k in list(grads):
                 T.free(grads.pop(k))
-        x = T.alloc(0, in_numel * in_es, s_data)
-        y = T.alloc(0, 8, s_data)                                 # labels
+            T.mark("zg_end")
+        T.mark("data_start")
+        x = T.alloc(0, in_numel * in_es, s_data, kind="data")
+        y = T.alloc(0, 8, s_data, kind="data")                    # labels
+        T.mark("data_end")
+        T.mark("fw_start")
         # ---- forward ----
         act = x                  # current activation handle
         act_owner = -1           # op index that produced act (-1 = batch data)
@@ -471,10 +500,14 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
                     saved[k].append(out)
                 act, act_owner = out, k
         loss = T.alloc(F32)
+        T.mark("fw_end")
         if zero_grad == "pos0":
+            T.mark("zg_start")
             for k in list(grads):
                 T.free(grads.pop(k))
+            T.mark("zg_end")
         # ---- backward ----
+        T.mark("bw_start")
         g = T.alloc(0, ops[-1].out * F32 if ops[-1].out else F32)
         if not _kept(saved, act) and act != x:
             T.free(act)
@@ -492,21 +525,24 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
                 if pi in grads:
                     T.free(T.alloc(shp[0] * shp[1] * F32))
                 else:
-                    grads[pi] = T.alloc(shp[0] * shp[1] * F32)
+                    grads[pi] = T.alloc(shp[0] * shp[1] * F32, kind="grad")
             for h in saved.pop(k, []):
                 if h in T.live:
                     T.free(h)
             T.free(g)
             g = gi
         T.free(g)
+        T.mark("bw_end")
         # ---- optimizer.step ----
+        T.mark("opt_start")
         if it == 0 and opt != "adagrad":
             for (_, shp) in params:
-                state += [T.alloc(x_) for x_ in _opt_state(opt, shp)]
+                state += [T.alloc(x_, kind="state") for x_ in _opt_state(opt, shp)]
         for _ in range(_opt_temps(opt)):
-            tmps = [T.alloc(shp[0] * shp[1] * F32, 0, s_opt) for (_, shp) in params]
+            tmps = [T.alloc(shp[0] * shp[1] * F32, 0, s_opt, kind="temp") for (_, shp) in params]
             for h in tmps:
                 T.free(h)
+        T.mark("opt_end")
         for h in list(saved.values()):
             for hh in h:
                 if hh in T.live:
@@ -514,6 +550,7 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
         T.free(loss)
         T.free(y)
         T.free(x)
+        T.mark("iter_end")
         # leftover activations (defensive)
     for k in list(grads):
         T.free(grads.pop(k))
@@ -523,7 +560,7 @@ def template(name: str, opt: str, zero_grad: str = "pos1", streams: bool = False
         T.free(h)
     for h in list(T.live):
         T.free(h)
-    return T.arrays()
+    return T
 
 
 def _kept(saved: Dict[int, List[int]], h: int) -> bool:
