@@ -392,6 +392,77 @@ int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch, size_t scr
                         int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
                         uint32_t* d_wire_nids, void* stream);
 
+/*
+ * Memory Orchestrator (§3.3;
+ * SPEC.md:151-203), the step directly before the Simulator. Input: the
+ * Analyzer's blocks of each trace in allocation order (CPU timestamps in
+ * microseconds) and the training loop's annotation windows per
+ * iteration. Output: each block's class and, for the analysis
+ * iteration (SPEC D1: the second, index 1), the re-timed sequence ordered by
+ * (ts, Free before Alloc, block) (D4). Rules (Q22-Q25):
+ * classes by priority Parameter (no free, allocated before the first
+ * iteration), OptimizerState (allocated in an optimizer.step window with a
+ * Parameter's size; two per Parameter of that size, in allocation order,
+ * SPEC D3), Gradient (allocated in a backward window, not freed before its
+ * end), BatchData (allocated in a data window), Activation (forward or
+ * backward window), Other. Re-timing for W = [Ws, We) of the analysis
+ * iteration: blocks allocated at/after We or dead at Ws are left out; a
+ * BatchData free is clamped to its iteration's end; carried-over blocks are
+ * allocated at Ws, Parameter/OptimizerState never freed, a carried-over
+ * Gradient freed at the end of W's zero_grad window (We if none, SPEC D5);
+ * a Gradient allocated in W is freed at We; other frees are kept if before
+ * We, else at We; a free never precedes or ties its allocation (F' >= A'+1).
+ */
+#define XM_O_OK 0
+#define XM_O_FEW_ITERATIONS 1   /* fewer iterations than analysis_iter + 1      */
+#define XM_O_TS_RANGE 2         /* a re-timed timestamp is >= 2^32 us after Ws  */
+typedef struct {
+  const int64_t* alloc_ts;  /* [n_blocks] DEVICE, allocation time (us)                  */
+  const int64_t* free_ts;   /* [n_blocks] DEVICE, deallocation time, -1 = none observed */
+  const int64_t* size;      /* [n_blocks] DEVICE, bytes (> 0)                           */
+  const uint8_t* stream;    /* [n_blocks] DEVICE stream (0..15) or NULL                 */
+  const int64_t* boff;      /* [n_traces+1] DEVICE, blocks of trace t, allocation order */
+  const int64_t* win;       /* [n_iters][6][2] DEVICE windows [start, end] per          */
+                            /* iteration: iteration, data, forward, backward,          */
+                            /* zero_grad (-1,-1 = none), optimizer.step                */
+  const int64_t* woff;      /* [n_traces+1] DEVICE, iterations of trace t              */
+  int64_t n_traces, n_blocks;
+  uint32_t max_blocks;      /* largest trace (host value; sizes the scratch)           */
+} xm_profiles;
+
+typedef struct {            /* per trace, 56 bytes                                      */
+  int64_t ws, we;           /* the analysis window                                      */
+  uint64_t n_events;        /* length of the re-timed sequence                          */
+  uint32_t n_ids;           /* dense id space of its wire form                          */
+  uint32_t status;          /* XM_O_*                                                   */
+  uint32_t n_class[6];      /* blocks per class (Parameter, OptimizerState, Gradient,   */
+                            /* BatchData, Activation, Other)                            */
+} xm_orchestrated;
+
+size_t xm_orchestrate_scratch_bytes(const xm_profiles* in);
+/*
+ * Orchestrate every trace (asynchronous, one launch). Outputs, DEVICE,
+ * caller-owned: d_class[n_blocks] (0-5 as above; undefined for traces whose
+ * status is not XM_O_OK); d_seq[2 n_blocks]: trace t's sorted sequence at
+ * d_seq[2 boff[t] ...], n_events keys each (ts - ws) << 32 | kind << 31 |
+ * block (kind 0 = Free, 1 = Alloc; block = index in the trace's allocation
+ * order); d_rec[n_traces]. The scratch keeps the staged wire form for
+ * xm_orchestrate_wire. Errors: XM_EINVAL, XM_ERANGE, XM_ENOMEM, XM_ECUDA.
+ */
+int xm_orchestrate(const xm_profiles* in, uint32_t analysis_iter, void* d_scratch,
+                   size_t scratch_bytes, uint8_t* d_class, uint64_t* d_seq,
+                   xm_orchestrated* d_rec, void* stream);
+/*
+ * After xm_orchestrate (same in / scratch): the re-timed sequences as an
+ * xm_batch's arrays (allocation +size, free -size, dense ids, the block's
+ * stream), traces stored in d_order (stored -> caller; NULL = identity).
+ * DEVICE outputs sized sum n_events / n_traces+1 / n_traces. Two launches.
+ */
+int xm_orchestrate_wire(const xm_profiles* in, const void* d_scratch, size_t scratch_bytes,
+                        const xm_orchestrated* d_rec, const uint32_t* d_order,
+                        int64_t* d_wire_bytes, uint32_t* d_wire_tag, int64_t* d_wire_off,
+                        uint32_t* d_wire_nids, void* stream);
+
 /* Number of device kernel launches the last xm_simulate_batch on this thread */
 /* issued (for the bench's gpu_launches claim).                               */
 int xm_last_launch_count(void);

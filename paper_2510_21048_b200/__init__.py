@@ -95,6 +95,19 @@ LIFECYCLE_DTYPE = np.dtype([("n_blocks", "<u8"), ("n_orphan", "<u8"), ("n_mismat
 assert LIFECYCLE_DTYPE.itemsize == 56
 
 
+class _Profiles(ctypes.Structure):
+    _fields_ = [("alloc_ts", ctypes.c_void_p), ("free_ts", ctypes.c_void_p), ("size", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p), ("boff", ctypes.c_void_p), ("win", ctypes.c_void_p),
+                ("woff", ctypes.c_void_p), ("n_traces", ctypes.c_int64), ("n_blocks", ctypes.c_int64),
+                ("max_blocks", ctypes.c_uint32)]
+
+
+# xm_orchestrated (include/xmem.h), 56 B
+ORCH_DTYPE = np.dtype([("ws", "<i8"), ("we", "<i8"), ("n_events", "<u8"), ("n_ids", "<u4"),
+                       ("status", "<u4"), ("n_class", "<u4", (6,))])
+assert ORCH_DTYPE.itemsize == 56
+
+
 class _Tpl(ctypes.Structure):
     _fields_ = [("fixed", ctypes.c_void_p), ("per", ctypes.c_void_p), ("tag", ctypes.c_void_p),
                 ("tpl_off", ctypes.c_void_p), ("n_tpl", ctypes.c_int64)]
@@ -158,6 +171,11 @@ def lib():
         L.xm_reconstruct_scratch_bytes.restype = ctypes.c_size_t
         L.xm_reconstruct.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 4
         L.xm_reconstruct_wire.argtypes = [ctypes.POINTER(_Instants), P, ctypes.c_size_t] + [P] * 7
+        L.xm_orchestrate_scratch_bytes.argtypes = [ctypes.POINTER(_Profiles)]
+        L.xm_orchestrate_scratch_bytes.restype = ctypes.c_size_t
+        L.xm_orchestrate.argtypes = [ctypes.POINTER(_Profiles), ctypes.c_uint32, P, ctypes.c_size_t,
+                                     P, P, P, P]
+        L.xm_orchestrate_wire.argtypes = [ctypes.POINTER(_Profiles), P, ctypes.c_size_t] + [P] * 7
         L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
@@ -526,3 +544,79 @@ def reconstruct(ins: DeviceInstants, wire: bool = True, stream=None, scratch=Non
                             n_wire, int(r["n_ids"].max()) if T else 0,
                             int(r["n_kept"].max()) if T else 0)
     return partner[:E], mism[:E], r, batch
+
+
+# ---- NEXT-2: memory orchestrator (xm_orchestrate) --------------------------------
+@dataclass
+class DeviceProfiles:
+    alloc_ts: "object"
+    free_ts: "object"
+    size: "object"
+    stream: "object"
+    boff: "object"
+    win: "object"
+    woff: "object"
+    n_traces: int
+    n_blocks: int
+    max_blocks: int
+
+    @staticmethod
+    def from_host(p, device=None) -> "DeviceProfiles":
+        """p: workloads.cpu_profile.Profiles (or any object with its fields)."""
+        import torch
+        device = torch.device(device or "cuda")
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(device)
+        boff = np.ascontiguousarray(p.boff, np.int64)
+        lens = np.diff(boff)
+        return DeviceProfiles(t(p.alloc_ts, np.int64), t(p.free_ts, np.int64), t(p.size, np.int64),
+                              t(p.stream, np.uint8) if p.stream is not None else None, t(boff, np.int64),
+                              t(np.asarray(p.win, np.int64).reshape(-1), np.int64), t(p.woff, np.int64),
+                              len(boff) - 1, int(boff[-1]), int(lens.max()) if len(lens) else 0)
+
+    def c(self) -> _Profiles:
+        def p(x):
+            return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
+        return _Profiles(p(self.alloc_ts), p(self.free_ts), p(self.size), p(self.stream), p(self.boff),
+                         p(self.win), p(self.woff), self.n_traces, self.n_blocks, self.max_blocks)
+
+
+def orchestrate(prof: DeviceProfiles, analysis_iter: int = 1, wire: bool = True, stream=None,
+                scratch=None):
+    """xm_orchestrate (+ xm_orchestrate_wire): classes (device uint8 [n_blocks]),
+    sorted sequences (device uint64 keys, trace t at 2*boff[t]), per-trace
+    records (numpy ORCH_DTYPE) and, with wire=True, the replay batch of the
+    re-timed sequences stored longest first (DeviceBatch)."""
+    import torch
+    dev = prof.boff.device
+    c = prof.c()
+    need = int(lib().xm_orchestrate_scratch_bytes(ctypes.byref(c)))
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    B, T = prof.n_blocks, prof.n_traces
+    cls = torch.empty(max(B, 1), dtype=torch.uint8, device=dev)
+    seq = torch.empty(max(2 * B, 1), dtype=torch.int64, device=dev)
+    rec = torch.empty((max(T, 1), 56), dtype=torch.uint8, device=dev)
+
+    def p(x):
+        return ctypes.c_void_p(x.data_ptr()) if x is not None else None
+    rc = lib().xm_orchestrate(ctypes.byref(c), analysis_iter, ctypes.c_void_p(scratch.data_ptr()),
+                              scratch.numel(), p(cls), p(seq), p(rec), _stream_ptr(stream))
+    _check(rc, "xm_orchestrate")
+    r = rec[:T].cpu().numpy().reshape(-1).view(ORCH_DTYPE) if T else np.zeros(0, ORCH_DTYPE)
+    batch = None
+    if wire:
+        n_ev = r["n_events"].astype(np.int64)
+        order_h = np.argsort(-n_ev, kind="stable").astype(np.uint32)
+        order = torch.from_numpy(order_h.view(np.int32)).to(dev)
+        n_wire = int(n_ev.sum())
+        wb = torch.empty(max(n_wire, 1), dtype=torch.int64, device=dev)
+        wt = torch.empty(max(n_wire, 1), dtype=torch.int32, device=dev)
+        wo = torch.empty(T + 1, dtype=torch.int64, device=dev)
+        wn = torch.empty(max(T, 1), dtype=torch.int32, device=dev)
+        rc = lib().xm_orchestrate_wire(ctypes.byref(c), ctypes.c_void_p(scratch.data_ptr()),
+                                       scratch.numel(), p(rec), p(order), p(wb), p(wt), p(wo), p(wn),
+                                       _stream_ptr(stream))
+        _check(rc, "xm_orchestrate_wire")
+        batch = DeviceBatch(wb[:n_wire], wt[:n_wire], wo, wn[:T], order, None, T, n_wire,
+                            int(r["n_ids"].max()) if T else 0, int(n_ev.max()) if T else 0)
+    return cls[:B], seq, r, batch

@@ -11,7 +11,7 @@ INCLUDE = os.path.join(ROOT, "include")
 DEBUG = bool(os.environ.get("XM_DEBUG"))
 TIMING = bool(os.environ.get("XM_TIMING"))
 LIB = os.path.join(PKG, "libxmem_debug.so" if DEBUG else ("libxmem_timing.so" if TIMING else "libxmem.so"))
-SOURCES = ["loader.cpp", "capi.cu", "replay.cu", "scan.cu", "expand.cu", "metrics.cu", "lifecycle.cu"]
+SOURCES = ["loader.cpp", "capi.cu", "replay.cu", "scan.cu", "expand.cu", "metrics.cu", "lifecycle.cu", "orchestrate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
