@@ -572,7 +572,7 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typenam
 // the chosen entry is dropped by moving the last entry into its slot. A
 // whole-segment entry has no neighbours; the moved one's are re-pointed.
 template <class L>
-__device__ __noinline__ void reclaim_largest_first(State<L>& S, uint32_t& nf,
+__device__ __forceinline__ void reclaim_largest_first(State<L>& S, uint32_t& nf,
                                                    typename L::Acc& reserved, uint32_t& n_release,
                                                    uint32_t& live_segs, uint64_t need,
                                                    uint64_t cap_u) {

@@ -7,8 +7,10 @@
 // allocator state is needed for this quantity, so it is exact whenever no OOM
 // truncates the trace (the mode requires unlimited capacity).
 //
-// Flat, trace-oblivious decomposition so that long traces never bound the
-// launch (DESIGN.md §6 K1):
+// Batches whose traces are all at most 65536 events long (every paper-shaped
+// config) take K1t, one CTA per trace (below). Otherwise the flat,
+// trace-oblivious decomposition, so that long traces never bound the launch
+// (DESIGN.md §6 K1):
 //   K1z  row_trace[r] = trace owning the first event of 16-event row r
 //   K1a  persistent CTAs over 4096-event tiles (cp.async double-buffered in
 //        shared memory), 16 contiguous events per thread. A tile
@@ -98,6 +100,7 @@ struct SParams {
   Mono* tile_first;         // [n_tiles] piece before the tile's first trace start
   Mono* tile_last;          // [n_tiles] piece from the tile's last trace start
   xm_result* out;
+  unsigned int* work;       // trace counter of k_scan_trace
 };
 
 __device__ __forceinline__ Mono to_global(const MonoR& m, int64_t t0e) {
@@ -343,6 +346,110 @@ __global__ void k_scan_combine(SParams P) {
   write_result(P, uint32_t(t), m.mx, m.arg);
 }
 
+// K1t: one CTA (8 warps) per trace, persistent over the stored (longest-first)
+// order -- the path for batches of traces up to kTraceMax events (all of the
+// paper-shaped configs). Each step covers kStep = 8 x 32 x kSub events: warp w
+// takes kSub coalesced 32-event slices (the next step's loads are in flight
+// meanwhile), scans them warp-locally and reduces (sum, max prefix, first
+// argmax); warp 0 folds the 8 warp pieces in order onto the running prefix.
+// 8 B read per event, 2 barriers per step.
+constexpr int kTraceMax = 1 << 16;
+constexpr int kTThreads = 256;
+constexpr int kSub = 8;
+constexpr int kWarpSpan = 32 * kSub;
+constexpr int kStep = 8 * kWarpSpan;
+
+__global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
+  __shared__ long long s_sum[8], s_mx[8];
+  __shared__ int s_arg[8];
+  __shared__ unsigned int s_k;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long* by = reinterpret_cast<const long long*>(P.bytes);
+  for (;;) {
+    if (tid == 0) s_k = atomicAdd(P.work, 1u);
+    __syncthreads();
+    const unsigned k = s_k;
+    __syncthreads();                        // s_k is rewritten by the next pull
+    if (int64_t(k) >= P.n_traces) break;
+    const int64_t e0 = P.off[k];
+    const int n = int(P.off[k + 1] - e0);
+    long long carry = 0, best = kNeg;       // warp 0 (uniform across its lanes)
+    int barg = -1;
+    long long cur[kSub], nxt[kSub];
+#pragma unroll
+    for (int s = 0; s < kSub; ++s) {
+      const int idx = kWarpSpan * w + 32 * s + lane;
+      cur[s] = idx < n ? __ldcs(by + e0 + idx) : 0;
+    }
+    for (int base = 0; base < n; base += kStep) {
+#pragma unroll
+      for (int s = 0; s < kSub; ++s) {
+        const int idx = base + kStep + kWarpSpan * w + 32 * s + lane;
+        nxt[s] = idx < n ? __ldcs(by + e0 + idx) : 0;
+      }
+      long long run = 0, lmx = kNeg;
+      int larg = -1;
+#pragma unroll
+      for (int s = 0; s < kSub; ++s) {
+        const int idx = base + kWarpSpan * w + 32 * s + lane;
+        const bool v = idx < n;
+        long long x = v ? rounded_delta(cur[s], P.u) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        x += run;
+        if (v && x > lmx) { lmx = x; larg = idx; }
+        run = __shfl_sync(kFull, x, 31);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {          // first argmax of the warp
+        const long long m2 = __shfl_xor_sync(kFull, lmx, o);
+        const int a2 = __shfl_xor_sync(kFull, larg, o);
+        if (m2 > lmx || (m2 == lmx && a2 < larg && m2 != kNeg)) { lmx = m2; larg = a2; }
+      }
+      if (lane == 0) { s_sum[w] = run; s_mx[w] = lmx; s_arg[w] = larg; }
+      __syncthreads();
+      if (w == 0) {                           // fold the 8 pieces in order (lanes 0-7)
+        const long long ps = lane < 8 ? s_sum[lane] : 0;
+        const long long pm = lane < 8 ? s_mx[lane] : kNeg;
+        const int pa = lane < 8 ? s_arg[lane] : -1;
+        long long ex = ps;                    // exclusive prefix of the piece sums
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          const long long y = __shfl_up_sync(kFull, ex, o);
+          if (lane >= o) ex += y;
+        }
+        ex -= ps;
+        long long c = pm == kNeg ? kNeg : carry + ex + pm;
+        int ca = pa;
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+          const long long m2 = __shfl_xor_sync(kFull, c, o);
+          const int a2 = __shfl_xor_sync(kFull, ca, o);
+          if (m2 > c || (m2 == c && a2 < ca && m2 != kNeg)) { c = m2; ca = a2; }
+        }
+        c = __shfl_sync(kFull, c, 0);
+        ca = __shfl_sync(kFull, ca, 0);
+        if (c != kNeg && c > best) { best = c; barg = ca; }
+        carry += __shfl_sync(kFull, ex + ps, 7);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < kSub; ++s) cur[s] = nxt[s];
+    }
+    if (tid == 0) {
+      xm_result R{};
+      R.peak_allocated = best > 0 ? uint64_t(best) << P.unit_shift : 0ull;
+      R.peak_allocated_idx = best > 0 ? uint32_t(barg) : 0u;
+      R.events_done = uint32_t(n);
+      R.status = XM_T_OK;
+      P.out[P.order[k]] = R;
+    }
+  }
+}
+
 }  // namespace
 
 namespace xm_internal {
@@ -373,6 +480,19 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
   s += size_t(P.n_tiles) * sizeof(Mono);
   P.row_trace = reinterpret_cast<uint32_t*>(s);
   P.out = d_out;
+  P.work = static_cast<unsigned int*>(d_scratch);
+  if (b->max_events <= uint32_t(kTraceMax)) {
+    // every trace is short enough for one CTA: the trace-per-CTA path
+    cudaError_t e = cudaMemsetAsync(d_scratch, 0, 4, st);
+    if (e != cudaSuccess) return int(e);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * 8);
+    k_scan_trace<<<unsigned(grid), kTThreads, 0, st>>>(P);
+    *n_launches += 1;
+    return int(cudaGetLastError());
+  }
   const int tb = 256;
   const int gt = int((b->n_traces + tb - 1) / tb);
   if (P.n_tiles > 0) {

@@ -125,6 +125,25 @@ def test_allocated_only_mode():
     assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
 
 
+def test_allocated_only_mode_long_traces():
+    """Traces above 65536 events take K1's flat segmented-scan path (shorter
+    batches take the trace-per-CTA path tested above)."""
+    tb = TraceBuilder()
+    rng = np.random.default_rng(5)
+    live = []
+    for i in range(90_000):
+        if live and rng.random() < 0.45:
+            tb.free(live.pop(int(rng.integers(0, len(live)))))
+        else:
+            tb.alloc(i, int(rng.integers(1, 1 << 22)))
+            live.append(i)
+    tb.end_trace()
+    b = concat([tb.build(), fuzz.spec1_corpus(200, 900, salt=12), suites.config1()])
+    h, _ = gpu_run(b, xm.Config(mode=1))
+    o = oracle_run(b)
+    assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
+
+
 def test_determinism():
     b = fuzz.capacity_corpus(200, 500, salt=11)
     h1, _ = gpu_run(b)
