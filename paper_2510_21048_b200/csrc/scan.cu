@@ -346,22 +346,24 @@ __global__ void k_scan_combine(SParams P) {
   write_result(P, uint32_t(t), m.mx, m.arg);
 }
 
-// K1t: one CTA (8 warps) per trace, persistent over the stored (longest-first)
+// K1t: one CTA (kTWarps warps) per trace, persistent over the stored (longest-first)
 // order -- the path for batches of traces up to kTraceMax events (all of the
-// paper-shaped configs). Each step covers kStep = 8 x 32 x kSub events: warp w
-// takes kSub coalesced 32-event slices (the next step's loads are in flight
-// meanwhile), scans them warp-locally and reduces (sum, max prefix, first
-// argmax); warp 0 folds the 8 warp pieces in order onto the running prefix.
-// 8 B read per event, 2 barriers per step.
+// paper-shaped configs). A step covers kStep = kTWarps x 32 lanes x kPerLane
+// events: each lane takes kPerLane CONSECUTIVE events with 16-byte loads (the
+// next step's loads are in flight meanwhile), scans them serially (sum, max
+// prefix, first argmax), the warp combines its lanes with one exclusive scan
+// and one arg-max reduction, and warp 0 folds the warp pieces in order onto
+// the running prefix. 8 B read per event, 2 barriers per step.
 constexpr int kTraceMax = 1 << 16;
-constexpr int kTThreads = 256;
-constexpr int kSub = 8;
-constexpr int kWarpSpan = 32 * kSub;
-constexpr int kStep = 8 * kWarpSpan;
+constexpr int kTWarps = 4;
+constexpr int kTThreads = 32 * kTWarps;
+constexpr int kPerLane = 8;
+constexpr int kWarpSpan = 32 * kPerLane;
+constexpr int kStep = kTWarps * kWarpSpan;
 
 __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
-  __shared__ long long s_sum[8], s_mx[8];
-  __shared__ int s_arg[8];
+  __shared__ long long s_sum[kTWarps], s_mx[kTWarps];
+  __shared__ int s_arg[kTWarps];
   __shared__ unsigned int s_k;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const long long* by = reinterpret_cast<const long long*>(P.bytes);
@@ -373,71 +375,81 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
     if (int64_t(k) >= P.n_traces) break;
     const int64_t e0 = P.off[k];
     const int n = int(P.off[k + 1] - e0);
+    // positions relative to the 16-byte aligned event pair holding e0
+    const int sh = int(e0 & 1);
+    const long long* b2 = by + (e0 - sh);
+    const int m = n + sh;
     long long carry = 0, best = kNeg;       // warp 0 (uniform across its lanes)
     int barg = -1;
-    long long cur[kSub], nxt[kSub];
+    longlong2 cur[kPerLane / 2], nxt[kPerLane / 2];
+    const int p0 = kWarpSpan * w + kPerLane * lane;     // this lane's first position
+    auto load = [&](longlong2* dst, int base) {
 #pragma unroll
-    for (int s = 0; s < kSub; ++s) {
-      const int idx = kWarpSpan * w + 32 * s + lane;
-      cur[s] = idx < n ? __ldcs(by + e0 + idx) : 0;
-    }
-    for (int base = 0; base < n; base += kStep) {
-#pragma unroll
-      for (int s = 0; s < kSub; ++s) {
-        const int idx = base + kStep + kWarpSpan * w + 32 * s + lane;
-        nxt[s] = idx < n ? __ldcs(by + e0 + idx) : 0;
+      for (int q = 0; q < kPerLane / 2; ++q) {
+        const int p = base + p0 + 2 * q;
+        if (p + 1 < m) dst[q] = __ldcs(reinterpret_cast<const longlong2*>(b2 + p));
+        else dst[q] = make_longlong2(p < m ? __ldcs(b2 + p) : 0, 0);
       }
+    };
+    load(cur, 0);
+    for (int base = 0; base < m; base += kStep) {
+      load(nxt, base + kStep);
       long long run = 0, lmx = kNeg;
       int larg = -1;
 #pragma unroll
-      for (int s = 0; s < kSub; ++s) {
-        const int idx = base + kWarpSpan * w + 32 * s + lane;
-        const bool v = idx < n;
-        long long x = v ? rounded_delta(cur[s], P.u) : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long y = __shfl_up_sync(kFull, x, o);
-          if (lane >= o) x += y;
+      for (int q = 0; q < kPerLane; ++q) {
+        const int idx = base + p0 + q - sh;             // event index in the trace
+        const long long raw = (q & 1) ? cur[q >> 1].y : cur[q >> 1].x;
+        if (idx >= 0 && idx < n) {
+          run += rounded_delta(raw, P.u);
+          if (run > lmx) { lmx = run; larg = idx; }
         }
-        x += run;
-        if (v && x > lmx) { lmx = x; larg = idx; }
-        run = __shfl_sync(kFull, x, 31);
       }
+      long long ex = run;                     // exclusive scan of the lane sums
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(kFull, ex, o);
+        if (lane >= o) ex += y;
+      }
+      const long long wsum = __shfl_sync(kFull, ex, 31);
+      ex -= run;
+      long long c = lmx == kNeg ? kNeg : ex + lmx;
+      int ca = larg;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {          // first argmax of the warp
-        const long long m2 = __shfl_xor_sync(kFull, lmx, o);
-        const int a2 = __shfl_xor_sync(kFull, larg, o);
-        if (m2 > lmx || (m2 == lmx && a2 < larg && m2 != kNeg)) { lmx = m2; larg = a2; }
+        const long long m2 = __shfl_xor_sync(kFull, c, o);
+        const int a2 = __shfl_xor_sync(kFull, ca, o);
+        if (m2 > c || (m2 == c && a2 < ca && m2 != kNeg)) { c = m2; ca = a2; }
       }
-      if (lane == 0) { s_sum[w] = run; s_mx[w] = lmx; s_arg[w] = larg; }
+      if (lane == 0) { s_sum[w] = wsum; s_mx[w] = c; s_arg[w] = ca; }
       __syncthreads();
-      if (w == 0) {                           // fold the 8 pieces in order (lanes 0-7)
-        const long long ps = lane < 8 ? s_sum[lane] : 0;
-        const long long pm = lane < 8 ? s_mx[lane] : kNeg;
-        const int pa = lane < 8 ? s_arg[lane] : -1;
-        long long ex = ps;                    // exclusive prefix of the piece sums
+      if (w == 0) {                           // fold the warp pieces in order
+        const long long ps = lane < kTWarps ? s_sum[lane] : 0;
+        const long long pm = lane < kTWarps ? s_mx[lane] : kNeg;
+        const int pa = lane < kTWarps ? s_arg[lane] : -1;
+        long long pe = ps;
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-          const long long y = __shfl_up_sync(kFull, ex, o);
-          if (lane >= o) ex += y;
+        for (int o = 1; o < kTWarps; o <<= 1) {
+          const long long y = __shfl_up_sync(kFull, pe, o);
+          if (lane >= o) pe += y;
         }
-        ex -= ps;
-        long long c = pm == kNeg ? kNeg : carry + ex + pm;
-        int ca = pa;
+        pe -= ps;
+        long long cc = pm == kNeg ? kNeg : carry + pe + pm;
+        int cca = pa;
 #pragma unroll
-        for (int o = 4; o; o >>= 1) {
-          const long long m2 = __shfl_xor_sync(kFull, c, o);
-          const int a2 = __shfl_xor_sync(kFull, ca, o);
-          if (m2 > c || (m2 == c && a2 < ca && m2 != kNeg)) { c = m2; ca = a2; }
+        for (int o = kTWarps / 2; o; o >>= 1) {
+          const long long m2 = __shfl_xor_sync(kFull, cc, o);
+          const int a2 = __shfl_xor_sync(kFull, cca, o);
+          if (m2 > cc || (m2 == cc && a2 < cca && m2 != kNeg)) { cc = m2; cca = a2; }
         }
-        c = __shfl_sync(kFull, c, 0);
-        ca = __shfl_sync(kFull, ca, 0);
-        if (c != kNeg && c > best) { best = c; barg = ca; }
-        carry += __shfl_sync(kFull, ex + ps, 7);
+        cc = __shfl_sync(kFull, cc, 0);
+        cca = __shfl_sync(kFull, cca, 0);
+        if (cc != kNeg && cc > best) { best = cc; barg = cca; }
+        carry += __shfl_sync(kFull, pe + ps, kTWarps - 1);
       }
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < kSub; ++s) cur[s] = nxt[s];
+      for (int q = 0; q < kPerLane / 2; ++q) cur[q] = nxt[q];
     }
     if (tid == 0) {
       xm_result R{};
@@ -488,7 +500,7 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * 8);
+    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * 16);
     k_scan_trace<<<unsigned(grid), kTThreads, 0, st>>>(P);
     *n_launches += 1;
     return int(cudaGetLastError());
