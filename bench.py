@@ -227,7 +227,8 @@ def run_reference(args, world, rank):
     value = ev / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "cfg5" else "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": desc, "sample": sdesc, "n_traces": total_tr,
                        "n_events": total_ev},

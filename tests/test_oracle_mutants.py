@@ -7,6 +7,7 @@ goldens plus the gap-model brute force on a small fuzz slice -- reject it.
 This is evidence that the pins are strong enough to pin the oracle.
 """
 import ctypes
+import sys
 import os
 import subprocess
 import tempfile
@@ -154,3 +155,123 @@ def test_variant_mutant_rejected(name, old, new):
         assert _variant_pins_reject(_build(src, d)) is None
         L = _build(src.replace(old, new, 1), d + "/m")
         assert _variant_pins_reject(L) is not None, f"pins did not catch mutant: {name}"
+
+
+# ---- NEXT-3 lifecycle oracle (oracle/lifecycle.c) -------------------------------
+LC_SRC = os.path.join(os.path.dirname(oracle.__file__), "lifecycle.c")
+LC_MUTANTS = [
+    ("pop empties the address", "s->top = below[b];", "s->top = -1;"),
+    ("mismatch sign", "if (bytes[b] != -bytes[i])", "if (bytes[b] != bytes[i])"),
+    ("orphan closes nothing but counts", "tallies[1] += 1;", ""),
+    ("push keeps old top", "below[i] = s->top;\n      s->top = i;", "below[i] = -1;\n      s->top = i;"),
+    ("persistent count", "tallies[3] = open;", "tallies[3] = tallies[0] - open;"),
+]
+
+
+def _lc_build(src_text, d):
+    os.makedirs(d, exist_ok=True)
+    c = os.path.join(d, "lc.c")
+    so = os.path.join(d, "lc.so")
+    with open(c, "w") as f:
+        f.write(src_text)
+    subprocess.check_call(["gcc", "-O1", "-std=c99", "-shared", "-fPIC", "-w", "-o", so, c])
+    L = ctypes.CDLL(so)
+    P = ctypes.c_void_p
+    L.xmo_reconstruct.argtypes = [P, P, ctypes.c_int64, P, P, P]
+    return L
+
+
+def _lc_pins_reject(L):
+    import test_oracle_lifecycle as TL
+    from workloads import instants
+    P = ctypes.c_void_p
+
+    def rec(a, by):
+        a = np.ascontiguousarray(a, np.uint64)
+        by = np.ascontiguousarray(by, np.int64)
+        p = np.zeros(len(by), np.int64)
+        m = np.zeros(len(by), np.uint8)
+        t = np.zeros(6, np.uint64)
+        rc = L.xmo_reconstruct(a.ctypes.data_as(P), by.ctypes.data_as(P), len(by),
+                               p.ctypes.data_as(P), m.ctypes.data_as(P), t.ctypes.data_as(P))
+        return rc, p, m, t
+    # SPEC examples + LIFO / mismatch cases
+    cases = [([0xA, 0xA], [1024, -1024], [1, 0], [1, 0, 0, 0]), ([0xB], [-512], [-1], [0, 1, 0, 0]),
+             ([5, 5, 5, 5], [100, 200, -200, -100], [3, 2, 1, 0], [2, 0, 0, 0]),
+             ([5, 5], [100, -96], [1, 0], [1, 0, 1, 0]), ([7, 7, 7], [8, -8, 16], [1, 0, -1], [2, 0, 0, 1])]
+    for a, by, part, tal in cases:
+        rc, p, m, t = rec(a, by)
+        if rc or p.tolist() != part or t[:4].tolist() != tal:
+            return f"case {a}"
+    b = fuzz.spec1_corpus(20, 300, salt=31)
+    ins = instants.from_batch(b, salt=1, p_orphan=0.02, p_mismatch=0.02, p_lost=0.03)
+    for t in range(ins.n_traces):
+        a, by, st = ins.trace(t)
+        rc, p, m, tal = rec(a, by)
+        if rc or p.tolist() != TL.brute(a.tolist(), by.tolist()):
+            return f"brute trace {t}"
+    return None
+
+
+@pytest.mark.parametrize("name,old,new", LC_MUTANTS, ids=[m[0] for m in LC_MUTANTS])
+def test_lifecycle_mutant_rejected(name, old, new):
+    src = open(LC_SRC).read()
+    assert src.count(old) >= 1, f"mutation site missing: {name}"
+    with tempfile.TemporaryDirectory() as d:
+        assert _lc_pins_reject(_lc_build(src, d)) is None
+        assert _lc_pins_reject(_lc_build(src.replace(old, new, 1), d + "/m")) is not None, name
+
+
+# ---- NEXT-2 orchestrator and NEXT-4 metrics oracles (Python) ---------------------
+PY_MUTANTS = [
+    ("orchestrator", "quota 1 per parameter", "quota[int(size[i])] += 2", "quota[int(size[i])] += 1"),
+    ("orchestrator", "gradient needs no survival", "(free_ts[i] == -1 or free_ts[i] > w[BW][1])", "True"),
+    ("orchestrator", "open window bounds", "return w[0] >= 0 and w[0] <= ts <= w[1]", "return w[0] >= 0 and w[0] < ts < w[1]"),
+    ("orchestrator", "carried gradient at We", "F2 = zg_end if zg_end is not None else We", "F2 = We"),
+    ("orchestrator", "batch data not clamped", "if e >= 0 and (F == -1 or F > e):", "if False:"),
+    ("orchestrator", "Alloc before Free on ties", "FREE, ALLOC = 0, 1", "FREE, ALLOC = 1, 0"),
+    ("metrics", "median upper", "return (s[n // 2 - 1] + s[n // 2]) / 2.0", "return s[n // 2]"),
+    ("metrics", "C2 without OOM_jd1", "return int(c1 == 1 and ((oom2 is not None and not oom2) or bool(oom1)))",
+     "return int(c1 == 1 and (oom2 is not None and not oom2))"),
+    ("metrics", "saving sign", "    return -int(m_max)", "    return int(m_max)"),
+    ("metrics", "MRE uses round 1 always", 'errs.append(relative_error(r["est"], r["meas2"]))',
+     'errs.append(relative_error(r["est"], r["meas1"]))'),
+]
+
+
+@pytest.mark.parametrize("mod,name,old,new", PY_MUTANTS, ids=[m[1] for m in PY_MUTANTS])
+def test_python_oracle_mutant_rejected(mod, name, old, new, monkeypatch):
+    import importlib
+    import types
+    path = os.path.join(os.path.dirname(oracle.__file__), f"{mod}.py")
+    src = open(path).read()
+    assert src.count(old) >= 1, f"mutation site missing: {name}"
+    m = types.ModuleType(f"oracle.{mod}")
+    exec(compile(src.replace(old, new, 1), path, "exec"), m.__dict__)
+    monkeypatch.setitem(sys.modules, f"oracle.{mod}", m)
+    monkeypatch.setattr(oracle, mod, m, raising=False)
+    test_mod = importlib.import_module(f"test_oracle_{'orchestrator' if mod == 'orchestrator' else 'metrics'}")
+    importlib.reload(test_mod)
+    failed = False
+    for k, fn in vars(test_mod).items():
+        if not k.startswith("test_") or not callable(fn):
+            continue
+        try:
+            args = []
+            import inspect
+            params = inspect.signature(fn).parameters
+            if params:
+                # parametrized examples: run their table
+                marks = getattr(fn, "pytestmark", [])
+                for mk in marks:
+                    if mk.name == "parametrize":
+                        for vals in mk.args[1]:
+                            fn(*vals)
+                continue
+            fn()
+        except Exception:
+            failed = True
+            break
+    monkeypatch.undo()                 # the real oracle module back, then rebind
+    importlib.reload(test_mod)
+    assert failed, f"pins did not catch mutant: {name}"

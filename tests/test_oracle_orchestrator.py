@@ -115,3 +115,38 @@ def test_needs_two_iterations():
     W = _win(ITS[:1])
     with pytest.raises(O.OrchestratorError):
         O.orchestrate(np.array([1]), np.array([-1]), np.array([8]), W)
+
+
+def test_window_bounds_are_closed():
+    """Windows contain their end points (closed bounds, as SPEC.md:146 D2 fixes
+    for operator windows): an allocation exactly at a window's start or end
+    belongs to it."""
+    W = _win(ITS)
+    a = np.array([10, 171, 199, 146, 170, 100])
+    f = np.array([-1, -1, -1, 180, 185, 150])
+    s = np.array([64, 64, 64, 8, 8, 8])
+    cls = O.classify(a, f, s, W)
+    assert cls == [O.PARAMETER, O.OPTSTATE, O.OPTSTATE, O.GRADIENT, O.GRADIENT, O.BATCHDATA]
+
+
+def test_previous_batch_does_not_carry_over():
+    """P:242 "Batch Data ... lifecycles limited within one training iteration":
+    the batch of iteration 1, freed on the CPU only when iteration 2 loads the
+    next batch, must not appear in iteration 2's sequence."""
+    W = _win(ITS)
+    a = np.array([101, 201])          # batch of iteration 1, batch of iteration 2
+    f = np.array([202, 302])          # each freed when the next batch loads
+    s = np.array([4096, 4096])
+    cls, ev = O.orchestrate(a, f, s, W)
+    assert cls == [O.BATCHDATA, O.BATCHDATA]
+    assert ev == [(201, O.ALLOC, 1), (299, O.FREE, 1)]
+
+
+def test_free_before_alloc_on_equal_timestamps():
+    """SPEC.md:162 / D4: events are ordered by (ts, Free before Alloc, block)."""
+    W = _win(ITS)
+    a = np.array([210, 230])
+    f = np.array([230, 235])
+    s = np.array([512, 512])
+    cls, ev = O.orchestrate(a, f, s, W)
+    assert ev == [(210, O.ALLOC, 0), (230, O.FREE, 0), (230, O.ALLOC, 1), (235, O.FREE, 1)]
