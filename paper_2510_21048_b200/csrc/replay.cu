@@ -369,6 +369,9 @@ __device__ __forceinline__ bool try_claim(HeapHdr* h, uint32_t start, uint32_t n
   }
   const bool any_clash = __any_sync(kFull, clash);
   if (any_clash && mine) atomicAnd(&h->bitmap[w], ~mine);
+  // acquire: the previous owner's accesses to these pages (fenced before its
+  // heap_free) happen before our writes to them
+  if (!any_clash) __threadfence_block();
   __syncwarp();
   return !any_clash;
 }
@@ -606,13 +609,15 @@ __device__ __forceinline__ void reclaim_largest_first(State<L>& S, uint32_t& nf,
       load_links<L>(S.F_lk, Lx, lpv, lnx);
     }
     __syncwarp();
-    if (fsel != Lx) {
-      f_store(S, fsel, lk, lpos, lsz);
-      store_links<L>(S.F_lk, fsel, lpv, lnx);
-      set_next(S, lpv, L::kF | fsel);
-      set_prev(S, lnx, L::kF | fsel);
+    if (lane == 0) {                                       // one lane writes
+      if (fsel != Lx) {
+        f_store(S, fsel, lk, lpos, lsz);
+        store_links<L>(S.F_lk, fsel, lpv, lnx);
+        set_next(S, lpv, L::kF | fsel);
+        set_prev(S, lnx, L::kF | fsel);
+      }
+      if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
     }
-    if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
     __syncwarp();
     nf = Lx;
     reserved -= typename L::Acc(msz);
@@ -866,7 +871,9 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           load_links<L>(S.F_lk, Lx, lpv, lnx);
         }
         __syncwarp();
-        // ---- store phase ----
+        // ---- store phase (every lane stores the same values; no location is
+        // written twice with different values within an event, so lanes that
+        // run unconverged cannot leave a stale value) ----
         uint32_t asize;
         if (split) {
           uint32_t r = fsel;                           // remainder keeps the free entry
@@ -932,21 +939,30 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           const uint32_t nsz = psz + sz + (qf ? nsz0 : 0u);
           const uint32_t nn = qf ? nnx : q;
           const uint32_t nk = make_key(acls, nsz);
-          f_store(S, P_, nk, ppos, nsz);
-          set_next(S, p, nn);
-          set_prev(S, nn, p);
-          if (qf) {                                   // drop N_: move the last entry there
-            if (N_ != Lx) {
-              if (Lx == P_) {                         // the last entry is the merged one
-                lk = nk; lsz = nsz; lnx = nn;
-              }
-              f_store(S, N_, lk, lpos, lsz);
-              store_links<L>(S.F_lk, N_, lpv, lnx);
-              set_next(S, lpv, kF | N_);
-              set_prev(S, lnx, kF | N_);
-            }
+          if (qf && N_ != Lx && Lx == P_) {
+            // the merged entry is the last one and moves into N_'s slot: write
+            // it there once (writing P_ first and then its sentinel would store
+            // two values to one location in one event)
+            f_store(S, N_, nk, ppos, nsz);
+            store_links<L>(S.F_lk, N_, lpv, nn);
+            set_next(S, lpv, kF | N_);
+            set_prev(S, nn, kF | N_);
             if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
             nf = Lx;
+          } else {
+            f_store(S, P_, nk, ppos, nsz);
+            set_next(S, p, nn);
+            set_prev(S, nn, p);
+            if (qf) {                                 // drop N_: move the last entry there
+              if (N_ != Lx) {
+                f_store(S, N_, lk, lpos, lsz);
+                store_links<L>(S.F_lk, N_, lpv, lnx);
+                set_next(S, lpv, kF | N_);
+                set_prev(S, lnx, kF | N_);
+              }
+              if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
+              nf = Lx;
+            }
           }
         } else if (qf) {
           const uint32_t nsz = nsz0 + sz;
