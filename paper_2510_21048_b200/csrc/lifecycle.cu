@@ -14,8 +14,8 @@
 //       reused while its block is open and n_ids <= max open + 31;
 //     * matching: a per-warp open-addressing hash table in global memory maps
 //       address -> top of that address's stack of open blocks (linked through
-//       the allocations' event indices), tagged with a per-trace generation so
-//       it is cleared once per call, not per trace. When the tile's addresses are distinct (the common
+//       the allocations' event indices); each trace clears and uses the
+//       first 2^ceil(log2 2n) slots of its warp's region. When the tile's addresses are distinct (the common
 //       case: __match_any_sync) every lane does its own lookup, insertions are
 //       resolved by a read phase / claim phase loop; otherwise the tile runs
 //       one instant at a time;
@@ -28,6 +28,7 @@
 // and read + 12 B wire write; hash probes and the stack links hit L2.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "xm_internal.h"
@@ -36,6 +37,7 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kWarps = 16;                // per CTA; scratch is per warp slot
+constexpr int kCtasPerSm = 4;
 
 struct Slot {                             // 16 B hash slot
   unsigned long long addr;
@@ -110,6 +112,11 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     uint32_t hb = 6;
     while ((1u << hb) < 2u * uint32_t(n) && hb < P.hbits) ++hb;
     const uint32_t hmask = (1u << hb) - 1u;
+    // clear this trace's slots (16-byte stores), so no per-call memset of the
+    // tables is needed
+    for (uint32_t h = lane; h <= hmask; h += 32)
+      reinterpret_cast<uint4*>(T)[h] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
     uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
     unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0;
     for (int base = 0; base < n; base += 32) {
@@ -305,11 +312,16 @@ Layout layout(const xm_instants* in) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
   const int64_t want_ctas = (in->n_traces + kWarps - 1) / kWarps;
-  L.ctas = uint32_t(want_ctas < sms ? (want_ctas > 0 ? want_ctas : 1) : sms);
-  L.n_slots = L.ctas * kWarps;
   uint32_t hb = 6;
   while ((1ull << hb) < 2ull * in->max_events) ++hb;
   L.hbits = hb;
+  // as many CTAs as fit (kCtasPerSm per SM) within a 2 GiB budget for the
+  // per-warp hash tables (long traces -> fewer, larger tables)
+  const int64_t per_cta = int64_t(kWarps) * int64_t(sizeof(Slot)) << hb;
+  const int64_t budget_ctas = std::max<int64_t>(1, (int64_t(2) << 30) / per_cta);
+  const int64_t cap_ctas = std::min<int64_t>(int64_t(sms) * kCtasPerSm, budget_ctas);
+  L.ctas = uint32_t(want_ctas < cap_ctas ? (want_ctas > 0 ? want_ctas : 1) : cap_ctas);
+  L.n_slots = L.ctas * kWarps;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t o = 256;                                   // header: work counter
   L.tables = o; o += al((size_t(L.n_slots) << hb) * sizeof(Slot));
@@ -349,8 +361,8 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(d_scratch);
-  // zero the header and the hash tables (generation 0 = never used)
-  cudaError_t e = cudaMemsetAsync(base, 0, L.stacks, st);
+  // zero the header (work counter); each warp clears its table per trace
+  cudaError_t e = cudaMemsetAsync(base, 0, 256, st);
   if (e != cudaSuccess) return set_error(XM_ECUDA, cudaGetErrorString(e));
   LParams P{};
   P.addr = in->addr;
