@@ -392,7 +392,8 @@ def main():
         k1_ms = float(np.median(ks))
         k1_alg = 8 * batch.n_events + 8 * (batch.n_traces + 1) + 64 * batch.n_traces
         k1_ach = k1_alg / (k1_ms / 1e3) / 1e9
-        k1 = {"kernels": "k_row_map + k_scan_tiles + k_scan_combine", "ms": k1_ms,
+        k1 = {"kernels": ("k_scan_trace (K1t)" if batch.lengths().max(initial=0) <= 65536
+                          else "k_row_map + k_scan_tiles + k_scan_combine"), "ms": k1_ms,
               "events_per_s": batch.n_events / (k1_ms / 1e3), "bound": "hbm",
               "achieved": k1_ach, "peak": peak, "unit": "GB/s", "frac": k1_ach / peak,
               "alg_bytes_per_launch": k1_alg}

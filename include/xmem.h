@@ -415,7 +415,8 @@ int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch, size_t scr
  */
 #define XM_O_OK 0
 #define XM_O_FEW_ITERATIONS 1   /* fewer iterations than analysis_iter + 1      */
-#define XM_O_TS_RANGE 2         /* a re-timed timestamp is >= 2^32 us after Ws  */
+#define XM_O_TS_RANGE 2         /* a re-timed timestamp >= 2^32 us after Ws, or */
+                                /* a block size outside (0, 2^41)              */
 typedef struct {
   const int64_t* alloc_ts;  /* [n_blocks] DEVICE, allocation time (us)                  */
   const int64_t* free_ts;   /* [n_blocks] DEVICE, deallocation time, -1 = none observed */
@@ -427,7 +428,8 @@ typedef struct {
                             /* zero_grad (-1,-1 = none), optimizer.step                */
   const int64_t* woff;      /* [n_traces+1] DEVICE, iterations of trace t              */
   int64_t n_traces, n_blocks;
-  uint32_t max_blocks;      /* largest trace (host value; sizes the scratch)           */
+  uint32_t max_blocks;      /* largest trace (host value; sizes the scratch), <= 2^23  */
+                            /* (XM_ERANGE otherwise)                                   */
 } xm_profiles;
 
 typedef struct {            /* per trace, 56 bytes                                      */

@@ -10,7 +10,8 @@
 //        optimizer-step candidates are listed (CTA-wide atomics);
 //     2. a candidate is optimizer state iff fewer than 2 x (#parameters of
 //        its size) earlier candidates have its size (the quota consumed in
-//        allocation order, SPEC D3) -- counted directly, O(C (C + P));
+//        allocation order, SPEC D3): candidates sorted by (size, block) and
+//        parameter sizes sorted (bitonic), then binary searches;
 //     3. every block: class (priority Parameter > OptState > Gradient >
 //        BatchData > Activation > Other), re-timed allocation / free, and
 //        64-bit keys (ts - Ws) << 32 | kind << 31 | block;
@@ -32,6 +33,8 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kThreads = 512;
 constexpr int kSmemKeys = 16384;          // 128 KB of keys in shared memory
+constexpr int kBlockBits = 23;            // quota keys: size << 23 | block (< 2^23 blocks,
+constexpr uint64_t kBlockMask = (1ull << kBlockBits) - 1;   // sizes < 2^41 bytes)
 enum { kParam = 0, kState, kGrad, kData, kAct, kOther };
 enum { wIt = 0, wData, wFw, wBw, wZg, wOpt };
 
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_orchestrate(OParams P) {
     // ---- 1. parameters and optimizer-step candidates ----
     for (int i = tid; i < n; i += kThreads) {
       const int64_t a = A[i];
+      if (S[i] <= 0 || (uint64_t(S[i]) >> 41)) atomicExch(&s_bad, 1u);   // sizes in (0, 2^41)
       if (F[i] == -1 && a < first) {
         psize[atomicAdd(&s_npar, 1u)] = S[i];
       } else {
@@ -134,27 +138,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_orchestrate(OParams P) {
     }
     __syncthreads();
     const uint32_t nc = s_ncand, np = s_npar;
-    // ---- 2. the quota: state iff earlier same-size candidates < 2 x same-size params ----
-    for (uint32_t c = tid; c < nc; c += kThreads) {
-      const uint32_t i = cand[c] & 0x7FFFFFFFu;
-      const int64_t sz = S[i];
-      uint32_t before = 0, pars = 0;
-      for (uint32_t d = 0; d < nc; ++d) {
-        const uint32_t j = cand[d] & 0x7FFFFFFFu;       // (other threads set bit 31)
-        before += (j < i && S[j] == sz);
-      }
-      for (uint32_t d = 0; d < np; ++d) pars += psize[d] == sz;
-      // mark: bit 31 of the candidate entry = optimizer state
-      if (before < 2 * pars) cand[c] = i | 0x80000000u;
-    }
-    __syncthreads();
-    // flag state blocks through the class output (written for every block below)
-    for (uint32_t c = tid; c < nc; c += kThreads)
-      if (cand[c] & 0x80000000u) P.cls[b0 + (cand[c] & 0x7FFFFFFFu)] = kState;
-    __syncthreads();
-    // ---- 3. classes, re-timing, keys ----
+    // ---- 2. the quota: a candidate is state iff fewer than 2 x (parameters of
+    // its size) earlier candidates have its size. Sort the candidates by
+    // (size, block) and the parameter sizes (bitonic, in the key buffer); a
+    // candidate's rank in its size run and the run length of its size among
+    // the parameters are then two binary searches. ----
     const bool big = 2 * n > kSmemKeys;
     unsigned long long* keys = big ? P.gkeys + size_t(blockIdx.x) * P.keys_cap : skeys;
+    {
+      uint32_t cpow = 1, ppow = 1;
+      while (cpow < nc) cpow <<= 1;
+      while (ppow < np) ppow <<= 1;
+      unsigned long long* ck = keys;
+      unsigned long long* pk = keys + cpow;
+      for (uint32_t c = tid; c < cpow; c += kThreads)
+        ck[c] = c < nc ? (uint64_t(S[cand[c]]) << kBlockBits) | cand[c] : ~0ull;
+      for (uint32_t q = tid; q < ppow; q += kThreads) pk[q] = q < np ? uint64_t(psize[q]) : ~0ull;
+      __syncthreads();
+      if (nc > 1) bitonic(ck, cpow);
+      if (np > 1) bitonic(pk, ppow);
+      for (uint32_t c = tid; c < nc; c += kThreads) {
+        const unsigned long long key = ck[c];
+        const uint64_t sz = key >> kBlockBits;
+        uint32_t lo = 0, hi = c;                         // first candidate of this size
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if ((ck[mid] >> kBlockBits) < sz) lo = mid + 1; else hi = mid;
+        }
+        const uint32_t rank = c - lo;
+        uint32_t a0 = 0, a1 = np;                        // parameters of this size
+        while (a0 < a1) {
+          const uint32_t mid = (a0 + a1) >> 1;
+          if (pk[mid] < sz) a0 = mid + 1; else a1 = mid;
+        }
+        uint32_t b1 = a0, b2 = np;
+        while (b1 < b2) {
+          const uint32_t mid = (b1 + b2) >> 1;
+          if (pk[mid] <= sz) b1 = mid + 1; else b2 = mid;
+        }
+        if (rank < 2 * (b1 - a0)) P.cls[b0 + uint32_t(key & kBlockMask)] = kState;
+      }
+      __syncthreads();
+    }
+    // ---- 3. classes, re-timing, keys ----
     for (int i = tid; i < n; i += kThreads) {
       const int64_t a = A[i];
       int64_t f = F[i];
@@ -359,7 +385,8 @@ extern "C" int xm_orchestrate(const xm_profiles* in, uint32_t analysis_iter, voi
   launch_counter() = 0;
   if (!in || in->n_traces < 0 || in->n_blocks < 0)
     return set_error(XM_EINVAL, "xm_orchestrate: bad arguments");
-  if (in->max_blocks > 0x7FFFFFFFu) return set_error(XM_ERANGE, "xm_orchestrate: too many blocks");
+  if (in->max_blocks > (1u << kBlockBits))
+    return set_error(XM_ERANGE, "xm_orchestrate: more than 2^23 blocks in a trace");
   if (in->n_traces == 0) return XM_OK;
   if (!in->boff || !in->win || !in->woff || (in->n_blocks > 0 && (!in->alloc_ts || !in->free_ts ||
       !in->size)) || !d_class || !d_seq || !d_rec || !d_scratch)
