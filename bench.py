@@ -183,6 +183,20 @@ def oracle_rate(batch, cores=None, passes=1):
     return ev / best, best, cores, res, ev
 
 
+def single_core_rate(batch, budget_events=4_000_000):
+    """The oracle on ONE host core (SURVEY.md §8(d) oracle timing (i)), on every
+    k-th trace up to ~budget_events."""
+    import oracle
+    k = max(1, int(np.ceil(batch.n_events / budget_events)))
+    sub = batch.subset(range(0, batch.n_traces, k))
+    t0 = time.perf_counter()
+    r = oracle.simulate_batch(sub)
+    dt = time.perf_counter() - t0
+    ev = int(r["events_done"].sum())
+    return {"value": ev / dt, "unit": UNIT, "cores": 1,
+            "sample": f"every {k}th trace: {sub.n_traces} traces, {ev} events, {dt:.2f} s"}
+
+
 def bounded_sample(batch, budget_events=60_000_000):
     """Whole workload when it is small enough, else every k-th trace."""
     if batch.n_events <= budget_events:
@@ -407,7 +421,8 @@ def main():
         sample, sdesc = bounded_sample(batch)
         rate, sec, cores, o, ev = oracle_rate(sample)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": sdesc + f"; {sec:.2f} s wall on {cores} host processes"}
+               "sample": sdesc + f"; {sec:.2f} s wall on {cores} host processes",
+               "single_core": single_core_rate(batch)}
         if not args.no_parity and sample.n_traces == batch.n_traces:
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from gpu_util import COMPARE

@@ -80,3 +80,51 @@ def test_gather_gloo_world2():
     assert (o0 == o1).all()
     vals = o0[:, :8].copy().view(np.uint64).ravel()
     assert vals.tolist() == [t * 7 + 3 for t in range(len(lengths))]
+
+
+def _oracle_worker(rank, world, port, q):
+    """Each rank replays its LPT shard of real traces (with the oracle, as a
+    stand-in for its GPU) and the per-trace records are all-gathered."""
+    import oracle
+    from workloads import fuzz, mc5
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    idx = np.arange(0, 3000, 97)                      # config-5 traces (global indices)
+    lengths = mc5.lengths(mc5.describe(idx))
+    plan = lpt_plan(lengths, world)
+    mine = plan.shards[rank]
+    b = mc5.batch(idx[mine])
+    o = oracle.simulate_batch(b)
+    rec = np.zeros((len(mine), 8), np.uint64)
+    for c, f in enumerate(["peak_allocated", "peak_allocated_blk", "peak_reserved", "final_reserved",
+                           "events_done", "status", "n_seg_alloc", "n_seg_release"]):
+        rec[:, c] = o[f]
+    local = torch.from_numpy(rec.view(np.uint8).reshape(len(mine), 64).copy())
+    out = gather_results(local, plan, rank)
+    q.put((rank, out.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_replay_gloo_equals_single_rank():
+    import oracle
+    from workloads import mc5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_oracle_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    (_, o0), (_, o1) = sorted(res, key=lambda x: x[0])
+    assert (o0 == o1).all()
+    idx = np.arange(0, 3000, 97)
+    whole = oracle.simulate_batch(mc5.batch(idx))
+    got = o0.view(np.uint64).reshape(len(idx), 8)
+    for c, f in enumerate(["peak_allocated", "peak_allocated_blk", "peak_reserved", "final_reserved",
+                           "events_done", "status", "n_seg_alloc", "n_seg_release"]):
+        assert (got[:, c] == whole[f]).all(), f
