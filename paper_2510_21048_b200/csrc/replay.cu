@@ -709,20 +709,23 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
     }
     const int64_t cur = tensor + d;
     const uint32_t w1 = (tc & 0xF0000000u) | (tc & kIdMask) | (is_alloc ? kAllocBit : 0u);
+    // a4 + the best-fit key of this lane's allocation, computed lane-parallel
+    // once per tile: class (stream, pool) and key = cls << 27 | min(s, max)
+    const uint32_t key1 = make_key(((tc >> 28) << 1) | (su <= u.small_u ? 1u : 0u), su);
 
     uint32_t j = 0;
     for (; j < cnt; ++j) {
       const uint32_t s = __shfl_sync(kFull, su, j);
       const uint32_t w = __shfl_sync(kFull, w1, j);
       const uint32_t id = w & kIdMask;
+      const uint32_t lo = __shfl_sync(kFull, key1, j);
       if (w & kAllocBit) {
         // ================= ALLOC =================
-        const uint32_t small = s <= u.small_u;                     // a4: pool
-        const uint32_t cls = ((w >> 28) << 1) | small;             // per-stream pools (Q5)
+        const uint32_t cls = lo >> kKeyBits;                       // per-stream pools (Q5)
+        const uint32_t small = cls & 1u;                           // a4: pool
         // a5: best fit = min (size, addr) over free blocks of class cls with
         // size >= s. Candidate iff key in [cls<<27 | min(s,max), cls<<27 | max];
         // equal keys are ordered by addr, loaded only on a tie.
-        const uint32_t lo = make_key(cls, s);
         const uint32_t span = (cls << kKeyBits | kKeyMax) - lo;
         uint32_t fsel = kNone32;
         uint32_t fkey_sel = 0;                          // narrow: the winner's key and
