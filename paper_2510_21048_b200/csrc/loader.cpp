@@ -8,6 +8,7 @@
 // the persistent replay kernel pulls work from, storing the traces in that
 // order. Traces are processed in parallel on host threads. None of the allocator arithmetic lives here.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -225,13 +226,17 @@ extern "C" int xm_load_traces(const int64_t* bytes, const uint32_t* tag, const i
   tr->max_ids = mi;
   tr->max_events = n_traces ? uint32_t(soff[1] - soff[0]) : 0u;
   // upload chunks for the streamed host entry point: chunk c = stored traces
-  // [chunk_end[c-1], chunk_end[c]), cut at trace boundaries near equal event
-  // counts (the first chunks hold the longest traces, which start first)
+  // [chunk_end[c-1], chunk_end[c]), cut at trace boundaries; chunk sizes grow
+  // geometrically (x1.15) so that the first, longest traces land -- and start
+  // -- early while later chunks stay few
   tr->n_chunks = 0;
   if (tr->chunk_end) {
     int64_t prev = 0;
+    const double r = 1.15, rn = std::pow(r, double(xm_internal::kUploadChunks));
     for (int c = 1; c <= xm_internal::kUploadChunks && prev < n_traces; ++c) {
-      int64_t e = int64_t(std::lower_bound(soff, soff + n_traces + 1, E * c / xm_internal::kUploadChunks) - soff);
+      const double frac = (std::pow(r, double(c)) - 1.0) / (rn - 1.0);
+      const int64_t target = int64_t(double(E) * frac);
+      int64_t e = int64_t(std::lower_bound(soff, soff + n_traces + 1, target) - soff);
       if (c == xm_internal::kUploadChunks) e = n_traces;
       if (e <= prev) continue;
       tr->chunk_end[tr->n_chunks++] = uint32_t(e);
