@@ -13,6 +13,12 @@
  * independent traces on one GPU, one warp per trace. The exact rules and
  * every reading of the paper are in DESIGN.md §Readings (Q1-Q16).
  *
+ * Beyond the replay (the rows around it): xm_expand_templates
+ * (config-5 traces generated on the device), xm_reconstruct /
+ * xm_reconstruct_wire (lifecycle reconstruction from profiler instants),
+ * xm_orchestrate / xm_orchestrate_wire (the Memory Orchestrator), and
+ * xm_metrics_batch (the paper's MRE / PEF / MCP).
+ *
  * Conventions for every entry point:
  *   - returns int: XM_OK (0) or a negative XM_E* code; never throws, never
  *     aborts. xm_last_error() returns a thread-local message for the last

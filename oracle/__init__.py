@@ -6,8 +6,17 @@ Plain CPU reference of xMem's Simulator (§3.4) written in C
 ``--impl reference`` legs may import this package. It shares no code with
 ``paper_2510_21048_b200`` (the product) and never imports it.
 
+Contents: the Simulator (``xmo.c``; allocator variants of NEXT-4 included),
+lifecycle reconstruction (``lifecycle.c``, NEXT-3; ``reconstruct`` /
+``wire_from_partner`` below), and in plain Python the Memory Orchestrator
+(``orchestrator.py``, NEXT-2) and the evaluation metrics (``metrics.py``,
+NEXT-4).
+
 Parity status: all functions pinned (tests/test_oracle_pins.py,
-tests/test_oracle_bruteforce.py); see DESIGN.md §Oracle.
+tests/test_oracle_bruteforce.py, tests/test_oracle_variants.py,
+tests/test_oracle_lifecycle.py, tests/test_oracle_orchestrator.py,
+tests/test_oracle_metrics.py, and the mutation checks in
+tests/test_oracle_mutants.py); see DESIGN.md §3.
 """
 from __future__ import annotations
 

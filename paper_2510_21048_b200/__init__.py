@@ -10,6 +10,12 @@ a hard error. PyTorch is used for device memory and streams only.
     res = simulate_batch(dev, Config())         # xm_simulate_batch -> uint8[T, 64] on device
     pk  = peaks(res)                            # xm_peaks -> dict of numpy arrays
     pk  = simulate_host(tr, Config())           # end to end with host buffers (xm_simulate_host)
+
+Widened rows, same conventions:
+    dev = expand_templates(Templates(...), tpl, b, seed, thr)   # config 5 on device (K4)
+    partner, mismatch, rec, wire = reconstruct(DeviceInstants.from_host(...))   # NEXT-3 (K5)
+    cls, seq, rec, wire = orchestrate(DeviceProfiles.from_host(...))           # NEXT-2 (K6)
+    m = metrics(runs)                                                          # NEXT-4
 """
 from __future__ import annotations
 
