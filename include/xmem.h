@@ -364,7 +364,8 @@ typedef struct {            /* per trace, 56 bytes                              
   uint64_t n_kept;          /* allocations + matched frees = replay events of the trace    */
   uint64_t n_invalid;       /* zero-byte instants                                          */
   uint32_t max_open;        /* most blocks open at once                                    */
-  uint32_t n_ids;           /* dense id space of the wire trace (<= max_open + 31)         */
+  uint32_t n_ids;           /* dense id space of the wire trace (<= max_open + 31); the    */
+                            /* replay needs <= 2^27 (xm_batch tag bits 0-26)               */
 } xm_lifecycle;
 
 size_t xm_reconstruct_scratch_bytes(const xm_instants* in);

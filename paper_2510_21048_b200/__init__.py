@@ -546,6 +546,9 @@ def reconstruct(ins: DeviceInstants, wire: bool = True, stream=None, scratch=Non
                                        p(wn), _stream_ptr(stream))
         _check(rc, "xm_reconstruct_wire")
         n_wire = int(r["n_kept"].sum()) if T else 0
+        if T and int(r["n_ids"].max()) > (1 << 27):
+            raise XMemError("xm_reconstruct: a trace keeps more than 2^27 blocks open; its wire "
+                            "trace exceeds the replay's id space (include/xmem.h XM_ID_BITS)")
         batch = DeviceBatch(wb[:max(n_wire, 0)], wt[:max(n_wire, 0)], wo, wn[:T], order, None, T,
                             n_wire, int(r["n_ids"].max()) if T else 0,
                             int(r["n_kept"].max()) if T else 0)
