@@ -360,12 +360,14 @@ def main():
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t[0])
-        h2d = 8 * batch.n_events + 4 * batch.n_events + 8 * (batch.n_traces + 1) \
+        ev_bytes = 8 if tr.packed is not None else 12        # packed or bytes + tag
+        h2d = ev_bytes * batch.n_events + 8 * (batch.n_traces + 1) \
             + 8 * batch.n_traces + (8 * batch.n_traces if has_cap else 0)
         e2e = {"value": done / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(64 * batch.n_traces), "ms_per_step": dt * 1e3,
                "api": "xm_simulate_host (pinned host traces -> device -> host results; "
-                      "upload streamed in longest-first chunks overlapping the replay)",
+                      "upload streamed in longest-first chunks overlapping the replay; "
+                      + ("8-byte packed events)" if tr.packed is not None else "12-byte events)"),
                "results_equal_device_path": bool((h_e2e == h).all())}
     clocks = sampler.stop() if sampler else None
 

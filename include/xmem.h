@@ -178,7 +178,13 @@ typedef struct {
                             /* allocated block bytes, reserved bytes}. Rows of events*/
                             /* a trace did not process (after a simulated OOM) are   */
                             /* left untouched. XM_FULL mode only.                    */
+  const uint64_t* packed;   /* optional [n_events] compact events (8 B instead of    */
+                            /* 12): bits 0-40 |request bytes|, bit 41 = allocation,   */
+                            /* bits 42-45 stream, bits 46-63 dense id (< 2^18). When  */
+                            /* non-NULL the kernels read it and ignore bytes / tag.   */
 } xm_batch;
+
+#define XM_PACKED_ID_BITS 18
 
 /* Fill *cfg with the defaults above. */
 void xm_config_default(xm_config* cfg);
@@ -210,6 +216,11 @@ int xm_traces_views(const xm_traces* tr, const int64_t** bytes, const uint32_t**
                     uint32_t* max_events);
 
 void xm_free_traces(xm_traces* tr);
+
+/* The compact event array of a packed batch (xm_batch.packed layout), built by */
+/* xm_load_traces when every trace's id space is below 2^XM_PACKED_ID_BITS;     */
+/* *packed = NULL otherwise. HOST, valid until xm_free_traces.                 */
+int xm_traces_packed(const xm_traces* tr, const uint64_t** packed);
 
 /*
  * Device scratch needed by xm_simulate_batch for this batch and config

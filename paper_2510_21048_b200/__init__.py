@@ -65,7 +65,8 @@ class _Batch(ctypes.Structure):
                 ("n_ids", ctypes.c_void_p), ("order", ctypes.c_void_p),
                 ("capacity", ctypes.c_void_p), ("n_traces", ctypes.c_int64),
                 ("n_events", ctypes.c_int64), ("max_ids", ctypes.c_uint32),
-                ("max_events", ctypes.c_uint32), ("curve", ctypes.c_void_p)]
+                ("max_events", ctypes.c_uint32), ("curve", ctypes.c_void_p),
+                ("packed", ctypes.c_void_p)]
 
 
 class _Summary(ctypes.Structure):
@@ -160,6 +161,7 @@ def lib():
         L.xm_traces_views.argtypes = [P] * 6 + [ctypes.POINTER(I64), ctypes.POINTER(I64),
                                                 ctypes.POINTER(ctypes.c_uint32),
                                                 ctypes.POINTER(ctypes.c_uint32)]
+        L.xm_traces_packed.argtypes = [P, ctypes.POINTER(P)]
         L.xm_free_traces.argtypes = [P]
         L.xm_free_traces.restype = None
         L.xm_scratch_bytes.argtypes = [ctypes.POINTER(_Batch), ctypes.POINTER(_Cfg)]
@@ -229,6 +231,9 @@ class Traces:
         # trace order[i], its events are [off[i], off[i+1]); pos[t] = i
         self.pos = np.empty(self.n_traces, np.int64)
         self.pos[self.order.astype(np.int64)] = np.arange(self.n_traces)
+        pk = ctypes.c_void_p()
+        _check(L.xm_traces_packed(handle, ctypes.byref(pk)), "xm_traces_packed")
+        self.packed = view(pk, np.uint64, self.n_events) if pk.value else None
 
     def span(self, t: int):
         """Event range [a, b) of the caller's trace t in the stored arrays
@@ -243,7 +248,9 @@ class Traces:
             self._h = None
 
     def to_device(self, device=None, capacity: Optional[np.ndarray] = None,
-                  non_blocking: bool = False) -> "DeviceBatch":
+                  non_blocking: bool = False, packed: bool = False) -> "DeviceBatch":
+        """Device copy; packed=True uploads the compact 8-byte events
+        (xm_batch.packed) instead of bytes + tag."""
         import torch
         device = torch.device(device or "cuda")
 
@@ -253,6 +260,14 @@ class Traces:
         if capacity is not None:
             cap = torch.from_numpy(np.ascontiguousarray(capacity, np.uint64).view(np.int64)).to(
                 device, non_blocking=non_blocking)
+        if packed:
+            if self.packed is None:
+                raise XMemError("no packed form: an id space exceeds 2^18")
+            db = DeviceBatch(None, None, t(self.off), t(self.n_ids.view(np.int32)),
+                             t(self.order.view(np.int32)), cap, self.n_traces, self.n_events,
+                             self.max_ids, self.max_events)
+            db.packed = t(self.packed.view(np.int64))
+            return db
         return DeviceBatch(t(self.bytes), t(self.tag.view(np.int32)), t(self.off),
                            t(self.n_ids.view(np.int32)), t(self.order.view(np.int32)), cap,
                            self.n_traces, self.n_events, self.max_ids, self.max_events)
@@ -271,13 +286,14 @@ class DeviceBatch:
     max_ids: int
     max_events: int
     _scratch: Dict = field(default_factory=dict)
+    packed: "object" = None              # optional compact events (xm_batch.packed)
 
     def c(self, curve=None) -> _Batch:
         def p(x):
             return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
         return _Batch(p(self.bytes), p(self.tag), p(self.off), p(self.n_ids), p(self.order),
                       p(self.capacity), self.n_traces, self.n_events, self.max_ids,
-                      self.max_events, p(curve))
+                      self.max_events, p(curve), p(self.packed))
 
 
 def load_traces(bytes_: np.ndarray, tag: np.ndarray, off: np.ndarray) -> Traces:

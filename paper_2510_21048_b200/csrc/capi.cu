@@ -100,7 +100,8 @@ static int check_batch(const xm_batch* b) {
   if (b->n_traces > 0x7FFFFFFFll) return set_error(XM_ERANGE, "more than 2^31-1 traces");
   if (b->n_traces > 0 && (!b->off || !b->n_ids || !b->order))
     return set_error(XM_EINVAL, "null device array in batch");
-  if (b->n_events > 0 && (!b->bytes || !b->tag)) return set_error(XM_EINVAL, "null event arrays");
+  if (b->n_events > 0 && !b->packed && (!b->bytes || !b->tag))
+    return set_error(XM_EINVAL, "null event arrays");
   return XM_OK;
 }
 
@@ -188,15 +189,20 @@ extern "C" int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_
 
 namespace {
 struct HostLayout {
-  size_t bytes, tag, off, n_ids, order, cap, out, ready, scratch, total;
+  size_t bytes, tag, packed, off, n_ids, order, cap, out, ready, scratch, total;
 };
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 HostLayout host_layout(const xm_traces_info& I, const xm_config* cfg, bool with_cap) {
   HostLayout L{};
   size_t p = 0;
-  L.bytes = p; p += al(sizeof(int64_t) * I.n_events);
-  L.tag = p; p += al(sizeof(uint32_t) * I.n_events);
+  // events: the packed 8-byte form when the loader built it, else bytes + tag
+  if (I.packed) {
+    L.packed = p; p += al(sizeof(uint64_t) * I.n_events);
+  } else {
+    L.bytes = p; p += al(sizeof(int64_t) * I.n_events);
+    L.tag = p; p += al(sizeof(uint32_t) * I.n_events);
+  }
   L.off = p; p += al(sizeof(int64_t) * (I.n_traces + 1));
   L.n_ids = p; p += al(sizeof(uint32_t) * I.n_traces);
   L.order = p; p += al(sizeof(uint32_t) * I.n_traces);
@@ -293,8 +299,12 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   if (capacity) cp(L.cap, capacity, sizeof(uint64_t) * I.n_traces, st);
   uint32_t* ready = reinterpret_cast<uint32_t*>(w + L.ready);
   if (!streamed) {
-    cp(L.bytes, I.bytes, sizeof(int64_t) * I.n_events, st);
-    cp(L.tag, I.tag, sizeof(uint32_t) * I.n_events, st);
+    if (I.packed) {
+      cp(L.packed, I.packed, sizeof(uint64_t) * I.n_events, st);
+    } else {
+      cp(L.bytes, I.bytes, sizeof(int64_t) * I.n_events, st);
+      cp(L.tag, I.tag, sizeof(uint32_t) * I.n_events, st);
+    }
   } else {
     Pipe* pp = nullptr;
     if (e == cudaSuccess) e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
@@ -312,8 +322,12 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
       if (c + 1 < I.n_chunks) ev1 = std::min<int64_t>(I.n_events, (ev1 + 31) & ~int64_t(31));
       else ev1 = I.n_events;
       if (ev1 > ev0) {
-        cp(L.bytes + sizeof(int64_t) * ev0, I.bytes + ev0, sizeof(int64_t) * (ev1 - ev0), pp->cs);
-        cp(L.tag + sizeof(uint32_t) * ev0, I.tag + ev0, sizeof(uint32_t) * (ev1 - ev0), pp->cs);
+        if (I.packed) {
+          cp(L.packed + sizeof(uint64_t) * ev0, I.packed + ev0, sizeof(uint64_t) * (ev1 - ev0), pp->cs);
+        } else {
+          cp(L.bytes + sizeof(int64_t) * ev0, I.bytes + ev0, sizeof(int64_t) * (ev1 - ev0), pp->cs);
+          cp(L.tag + sizeof(uint32_t) * ev0, I.tag + ev0, sizeof(uint32_t) * (ev1 - ev0), pp->cs);
+        }
         ev0 = ev1;
       }
       if (e != cudaSuccess) break;
@@ -330,8 +344,9 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   }
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
   xm_batch b{};
-  b.bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
-  b.tag = reinterpret_cast<const uint32_t*>(w + L.tag);
+  b.bytes = I.packed ? nullptr : reinterpret_cast<const int64_t*>(w + L.bytes);
+  b.tag = I.packed ? nullptr : reinterpret_cast<const uint32_t*>(w + L.tag);
+  b.packed = I.packed ? reinterpret_cast<const uint64_t*>(w + L.packed) : nullptr;
   b.off = reinterpret_cast<const int64_t*>(w + L.off);
   b.n_ids = reinterpret_cast<const uint32_t*>(w + L.n_ids);
   b.order = reinterpret_cast<const uint32_t*>(w + L.order);

@@ -33,6 +33,7 @@ struct xm_traces {
   uint32_t max_ids = 0, max_events = 0;
   uint32_t* chunk_end = nullptr;   // [kUploadChunks] pinned, see xm_simulate_host
   int n_chunks = 0;
+  uint64_t* packed = nullptr;      // compact events (xm_batch.packed), or null
   std::vector<void*> blocks;
   std::vector<bool> pinned;
 };
@@ -224,6 +225,28 @@ extern "C" int xm_load_traces(const int64_t* bytes, const uint32_t* tag, const i
   uint32_t mi = 0;
   for (int64_t i = 0; i < n_traces; ++i) mi = std::max(mi, tr->n_ids[i]);
   tr->max_ids = mi;
+  // compact 8-byte events for the host entry point's upload (2/3 of the bytes)
+  if (mi <= (1u << XM_PACKED_ID_BITS) && E > 0) {
+    tr->packed = (uint64_t*)host_alloc(tr, sizeof(uint64_t) * E);
+    if (tr->packed) {
+      auto pack = [&](int k) {
+        for (int64_t e = soff[bounds[k]]; e < soff[bounds[k + 1]]; ++e) {
+          const int64_t b = tr->bytes[e];
+          const uint32_t g = tr->tag[e];
+          tr->packed[e] = uint64_t(b > 0 ? b : -b) | (uint64_t(b > 0) << 41) |
+                          (uint64_t(g >> XM_STREAM_SHIFT) << 42) |
+                          (uint64_t(g & ((1u << XM_STREAM_SHIFT) - 1u)) << 46);
+        }
+      };
+      if (nth == 1) {
+        pack(0);
+      } else {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nth; ++k) th.emplace_back(pack, k);
+        for (auto& x : th) x.join();
+      }
+    }
+  }
   tr->max_events = n_traces ? uint32_t(soff[1] - soff[0]) : 0u;
   // upload chunks for the streamed host entry point: chunk c = stored traces
   // [chunk_end[c-1], chunk_end[c]), cut at trace boundaries; chunk sizes grow
@@ -265,6 +288,12 @@ extern "C" int xm_traces_views(const xm_traces* tr, const int64_t** bytes, const
   return XM_OK;
 }
 
+extern "C" int xm_traces_packed(const xm_traces* tr, const uint64_t** packed) {
+  if (!tr || !packed) return xm_internal::set_error(XM_EINVAL, "xm_traces_packed: null argument");
+  *packed = tr->packed;
+  return XM_OK;
+}
+
 extern "C" void xm_free_traces(xm_traces* tr) {
   if (!tr) return;
   for (size_t i = 0; i < tr->blocks.size(); ++i) {
@@ -279,6 +308,6 @@ namespace xm_internal {
 const xm_traces_info traces_info(const xm_traces* tr) {
   return xm_traces_info{tr->bytes,   tr->tag,      tr->off,      tr->n_ids,    tr->order,
                         tr->n_traces, tr->n_events, tr->max_ids, tr->max_events,
-                        tr->chunk_end, tr->n_chunks};
+                        tr->chunk_end, tr->n_chunks, tr->packed};
 }
 }  // namespace xm_internal

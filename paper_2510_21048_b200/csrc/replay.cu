@@ -84,6 +84,7 @@ struct HeapHdr {
 
 struct KParams {
   const int64_t* __restrict__ bytes;
+  const unsigned long long* __restrict__ packed;   // compact events (xm_batch.packed) or null
   const uint32_t* __restrict__ tag;
   const int64_t* __restrict__ off;
   const uint32_t* __restrict__ n_ids;
@@ -674,6 +675,19 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   const xm_internal::UnitConfig& u = P.u;
   const long long* __restrict__ by = reinterpret_cast<const long long*>(P.bytes) + e0;
   const uint32_t* __restrict__ tg = P.tag + e0;
+  const unsigned long long* __restrict__ pk = P.packed ? P.packed + e0 : nullptr;
+  // one event: signed request bytes and tag, from the 12-byte or the packed form
+  auto load_event = [&](uint32_t i, int64_t& b, uint32_t& t) {
+    if (pk) {
+      const unsigned long long v = __ldcg(pk + i);
+      const int64_t m = int64_t(v & ((1ull << 41) - 1));
+      b = (v >> 41) & 1ull ? m : -m;
+      t = uint32_t(v >> 46) | (uint32_t((v >> 42) & 0xFull) << 28);
+    } else {
+      b = __ldcg(by + i);
+      t = __ldcg(tg + i);
+    }
+  };
   uint64_t* const curve = kCurve ? P.curve + 3 * size_t(e0) : nullptr;
   Acc c_blk = 0, c_res = 0;               // curve: this lane's event of the tile
 
@@ -689,12 +703,12 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
 
   int64_t b_nx = 0;
   uint32_t t_nx = 0;
-  if (lane < n) { b_nx = __ldcg(by + lane); t_nx = __ldcg(tg + lane); }
+  if (lane < n) load_event(lane, b_nx, t_nx);
   for (uint32_t base = 0; base < n; base += 32) {
     const int64_t bc = b_nx;
     const uint32_t tc = t_nx;
     const uint32_t cnt = min(32u, n - base);
-    if (base + 32 + lane < n) { b_nx = __ldcg(by + base + 32 + lane); t_nx = __ldcg(tg + base + 32 + lane); }
+    if (base + 32 + lane < n) load_event(base + 32 + lane, b_nx, t_nx);
     __syncwarp();
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;
@@ -1171,6 +1185,7 @@ int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
   KParams P{};
   P.ready = ready;
   P.bytes = b->bytes;
+  P.packed = reinterpret_cast<const unsigned long long*>(b->packed);
   P.tag = b->tag;
   P.off = b->off;
   P.n_ids = b->n_ids;

@@ -81,6 +81,12 @@ __device__ __forceinline__ int64_t rounded_delta(int64_t b, uint32_t sh) {
   return (b + (b > 0 ? int64_t((1ull << sh) - 1) : 0)) >> sh;
 }
 
+// a packed event word (xm_batch.packed) -> signed request bytes
+__device__ __forceinline__ int64_t unpack_bytes(int64_t v) {
+  const int64_t m = v & ((1ll << 41) - 1);
+  return (v >> 41) & 1 ? m : -m;
+}
+
 // with the roundup_power2_divisions variant (NEXT-4): the shared a2 rule
 __device__ __forceinline__ int64_t rounded_delta(int64_t b, const xm_internal::UnitConfig& u) {
   if (!u.div_shift) return rounded_delta(b, u.unit_shift);
@@ -89,7 +95,8 @@ __device__ __forceinline__ int64_t rounded_delta(int64_t b, const xm_internal::U
 }
 
 struct SParams {
-  const int64_t* __restrict__ bytes;
+  const int64_t* __restrict__ bytes;      // signed request bytes, or the packed words
+  bool packed;                            // bytes holds xm_batch.packed words
   const int64_t* __restrict__ off;
   const uint32_t* __restrict__ order;   // caller index of each stored trace
   int64_t n_traces, n_events;
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         if (i < nvalid) {
-          run += rounded_delta(d[i], P.u);
+          run += rounded_delta(P.packed ? unpack_bytes(d[i]) : d[i], P.u);
           if (run > mx) { mx = run; arg = rel0 + i; }
         }
       }
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_tiles(SParams P) {
           cur.tr = tcur;
           run = 0;
         }
-        run += rounded_delta(d[i], P.u);
+        run += rounded_delta(P.packed ? unpack_bytes(d[i]) : d[i], P.u);
         cur.sum = run;
         if (run > cur.mx) { cur.mx = run; cur.arg = rel0 + i; }
       }
@@ -361,6 +368,7 @@ constexpr int kPerLane = 8;
 constexpr int kWarpSpan = 32 * kPerLane;
 constexpr int kStep = kTWarps * kWarpSpan;
 
+template <bool kPacked>
 __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
   __shared__ long long s_sum[kTWarps], s_mx[kTWarps];
   __shared__ int s_arg[kTWarps];
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
         const int idx = base + p0 + q - sh;             // event index in the trace
         const long long raw = (q & 1) ? cur[q >> 1].y : cur[q >> 1].x;
         if (idx >= 0 && idx < n) {
-          run += rounded_delta(raw, P.u);
+          run += rounded_delta(kPacked ? unpack_bytes(raw) : raw, P.u);
           if (run > lmx) { lmx = run; larg = idx; }
         }
       }
@@ -477,7 +485,8 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
                 xm_result* d_out, void* stream, int* n_launches) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SParams P{};
-  P.bytes = b->bytes;
+  P.packed = b->packed != nullptr;
+  P.bytes = b->packed ? reinterpret_cast<const int64_t*>(b->packed) : b->bytes;
   P.off = b->off;
   P.order = b->order;
   P.n_traces = b->n_traces;
@@ -501,7 +510,8 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * 16);
-    k_scan_trace<<<unsigned(grid), kTThreads, 0, st>>>(P);
+    if (P.packed) k_scan_trace<true><<<unsigned(grid), kTThreads, 0, st>>>(P);
+    else k_scan_trace<false><<<unsigned(grid), kTThreads, 0, st>>>(P);
     *n_launches += 1;
     return int(cudaGetLastError());
   }

@@ -23,6 +23,7 @@ struct xm_traces_info {
   uint32_t max_ids, max_events;
   const uint32_t* chunk_end;   // pinned [n_chunks]: stored-trace end of each upload chunk
   int n_chunks;
+  const uint64_t* packed;      // compact events (xm_batch.packed) or null
 };
 // upload chunks of the streamed host entry point (xm_simulate_host)
 constexpr int kUploadChunks = 24;

@@ -173,3 +173,16 @@ def test_scratch_sizing_is_host_only():
     cfg = xm.Config().c()
     n = xm.lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(cfg))
     assert n >= 256
+
+
+def test_packed_events_encode_bytes_and_tags():
+    """xm_load_traces also builds the compact 8-byte events (xm_batch.packed):
+    they decode to exactly the stored bytes and tags."""
+    c = fuzz.spec1_corpus(30, 400, salt=34)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    assert tr.packed is not None and len(tr.packed) == tr.n_events
+    v = tr.packed
+    mag = (v & np.uint64((1 << 41) - 1)).astype(np.int64)
+    b = np.where((v >> np.uint64(41)) & np.uint64(1), mag, -mag)
+    t = ((v >> np.uint64(46)) | (((v >> np.uint64(42)) & np.uint64(0xF)) << np.uint64(28))).astype(np.uint32)
+    assert (b == tr.bytes).all() and (t == tr.tag).all()

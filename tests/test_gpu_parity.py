@@ -223,3 +223,23 @@ def test_variant_config_validation():
         gpu_run(b, xm.Config(roundup_power2_divisions=3))
     with pytest.raises(xm.XMemError):
         gpu_run(b, xm.Config(reclaim_policy=7))
+
+
+def test_packed_event_format():
+    """The compact 8-byte events (xm_batch.packed, what xm_simulate_host uploads)
+    give the same results as bytes + tag, for K2 (plain, variants, curve) and K1."""
+    b = concat([fuzz.spec1_corpus(300, 800, salt=70), fuzz.capacity_corpus(100, 500, salt=71),
+                suites.config3().subset([0, 43]), hand.h7()])
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    dp = tr.to_device(capacity=b.capacity, packed=True)
+    h, _ = xm.peaks(xm.simulate_batch(dp))
+    assert_parity(b, h, oracle_run(b))
+    h2, _ = xm.peaks(xm.simulate_batch(dp, xm.Config(reclaim_policy=1, roundup_power2_divisions=4)))
+    assert_parity(b, h2, oracle_run(b, reclaim=1, div=4))
+    h3, _ = xm.peaks(xm.simulate_batch(dp, xm.Config(smem_per_warp=4096, warps_per_cta=1)))
+    assert_parity(b, h3, oracle_run(b))
+    d1 = tr.to_device(packed=True)
+    k1, _ = xm.peaks(xm.simulate_batch(d1, xm.Config(mode=1)))
+    assert_parity(b, k1, oracle_run(type(b)(b.bytes, b.tag, b.off,
+                                            np.full(b.n_traces, oracle.UNLIMITED, np.uint64))),
+                  fields=["peak_allocated", "peak_allocated_idx", "events_done"])
