@@ -106,11 +106,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     const unsigned gen = k + 1;
     const int64_t e0 = P.off[k];
     const int n = int(P.off[k + 1] - e0);
-    // this trace's table: the first 2^hb slots of the warp's region (>= 2n:
-    // at most n distinct addresses, load <= 1/2); other traces' entries in it
-    // carry other generations
+    // this trace's table: the first 2^hb slots of the warp's region, 2^hb > n
+    // (at most n distinct addresses, so a free slot always exists; with about
+    // half the instants allocations and addresses reused, the load stays well
+    // below 1/2 in practice); other traces' entries carry other generations
     uint32_t hb = 6;
-    while ((1u << hb) < 2u * uint32_t(n) && hb < P.hbits) ++hb;
+    while ((1u << hb) < uint32_t(n) + 1u && hb < P.hbits) ++hb;
     const uint32_t hmask = (1u << hb) - 1u;
     // clear this trace's slots (16-byte stores), so no per-call memset of the
     // tables is needed
@@ -313,7 +314,7 @@ Layout layout(const xm_instants* in) {
   cudaGetLastError();
   const int64_t want_ctas = (in->n_traces + kWarps - 1) / kWarps;
   uint32_t hb = 6;
-  while ((1ull << hb) < 2ull * in->max_events) ++hb;
+  while ((1ull << hb) < uint64_t(in->max_events) + 1) ++hb;
   L.hbits = hb;
   // as many CTAs as fit (kCtasPerSm per SM) within a 2 GiB budget for the
   // per-warp hash tables (long traces -> fewer, larger tables)
