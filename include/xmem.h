@@ -91,7 +91,7 @@ typedef struct {
   uint32_t smem_per_warp;      /* caps the per-CTA shared-memory heap at        */
                                /* smem_per_warp * warps_per_cta bytes (tests);  */
                                /* 0 = the whole 227 KB                          */
-  uint32_t warps_per_cta;      /* 0 = default (12)                              */
+  uint32_t warps_per_cta;      /* 0 = default (14)                              */
   /* Allocator variants (readings Q19, Q20):  */
   uint32_t roundup_power2_divisions; /* torch PYTORCH_CUDA_ALLOC_CONF          */
                                /* roundup_power2_divisions:N, one N for all sizes: */

@@ -44,6 +44,10 @@
 #include "rounding.cuh"
 #include "xm_internal.h"
 
+#ifndef XM_HEAP_RESERVE_DIV
+#define XM_HEAP_RESERVE_DIV 24  // admission keeps 1/24 of the heap for free-list growth (tuned)
+#endif
+
 #ifdef XM_DEBUG
 #include <cstdio>
 #define XM_CHECK(cond, ...)                                   \
@@ -418,7 +422,7 @@ __device__ void ticket_release(HeapHdr* h) {
 // (unless the heap would otherwise sit idle).
 __device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t reserve = total / 8;
+  const uint32_t reserve = total / XM_HEAP_RESERVE_DIV;
   uint32_t start, hw = 0, nap = 256;
   for (;;) {
     uint32_t used = 0;
@@ -1148,7 +1152,7 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   if (cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 12;
+  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 14;
   if (p.warps_per_cta > 16) p.warps_per_cta = 16;
   if (p.warps_per_cta < 1) p.warps_per_cta = 1;
   // heap: the whole per-CTA maximum unless capped (smem_per_warp x warps)

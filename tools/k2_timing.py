@@ -28,7 +28,7 @@ rate = done / np.maximum(dur, 1e-9) / 1e3
 print("per-trace ns/event quantiles", np.quantile(dur * 1e6 / np.maximum(done, 1), [0.1, 0.5, 0.9]))
 print("start times quantiles", np.quantile(st, [0, .5, .9, 1]))
 busy = dur.sum()
-W = 148 * (cfg.warps_per_cta or 12)
+W = 148 * (cfg.warps_per_cta or 14)
 print(f"warp-slot utilisation {busy / (en.max() * W) * 100:.1f}% (sum of trace durations / makespan x {W} warps)")
 for q in (0.5, 0.8, 0.9, 0.95, 1.0):
     print(f"  {q*100:.0f}% of traces done by {np.quantile(en, q):.3f} ms")
