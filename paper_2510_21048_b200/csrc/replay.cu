@@ -44,6 +44,9 @@
 #include "rounding.cuh"
 #include "xm_internal.h"
 
+#ifndef XM_F_INIT_DIV
+#define XM_F_INIT_DIV 4         // initial free-list capacity: n_ids / 4 + 64 entries
+#endif
 #ifndef XM_HEAP_RESERVE_DIV
 #define XM_HEAP_RESERVE_DIV 24  // admission keeps 1/24 of the heap for free-list growth (tuned)
 #endif
@@ -1097,7 +1100,7 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     int st = kStatusOverflow;
     // shared memory, NARROW layout: A region + an initial free list
     const uint32_t npa = uint32_t((a_bytes<Narrow>(na) + kPage - 1) / kPage);
-    const uint32_t nfc = min(round_scan(min(nf_exact, na / 4 + 64)), Narrow::kCapMax);
+    const uint32_t nfc = min(round_scan(min(nf_exact, na / XM_F_INIT_DIV + 64)), Narrow::kCapMax);
     const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc) + kPage - 1) / kPage);
     if (na <= Narrow::kMaxIdx && npa + npf <= P.heap_pages) {
       const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);

@@ -8,7 +8,7 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 b = suites.CONFIGS[wl]()
 tr = xm.load_traces(b.bytes, b.tag, b.off)
 cap = b.capacity if (b.capacity != xm.UNLIMITED).any() else None
-dev = tr.to_device("cuda", capacity=cap)
+dev = tr.to_device("cuda", capacity=cap, packed=bool(os.environ.get("PACKED")))
 for wpc in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,8,16").split(",")]:
     cfg = xm.Config(warps_per_cta=wpc)
     out = xm.simulate_batch(dev, cfg)
