@@ -333,8 +333,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kern_ms = float(t[0]), float(t[1])
 
-    # results of this rank (for parity)
+    # results of this rank (for parity); batch summary over all ranks
     h, summ = xm.peaks(out)
+    if world > 1:
+        from paper_2510_21048_b200.dist import reduce_summary
+        summ = reduce_summary(summ, device=dev)
     local_done = int(h["events_done"].astype(np.int64).sum())
     done = local_done
     if world > 1:

@@ -72,3 +72,23 @@ def reorder(full, plan: ShardPlan):
     perm = np.empty(T, np.int64)
     perm[dst] = src
     return full.index_select(0, torch.from_numpy(perm).to(full.device))
+
+
+SUM_KEYS = ("n_traces", "events_done", "n_oom", "n_overflow", "sum_peak_reserved", "n_predicted_oom")
+MAX_KEYS = ("max_peak_reserved", "max_peak_allocated")
+
+
+def reduce_summary(summ: dict, device=None, group=None) -> dict:
+    """Batch summary (xm_peaks' xm_summary as a dict) over all ranks: counters
+    summed, peaks maxed -- two small all_reduce calls."""
+    import torch
+    import torch.distributed as dist
+    dev = device if device is not None else "cpu"
+    s = torch.tensor([int(summ[k]) for k in SUM_KEYS], dtype=torch.int64, device=dev)
+    m = torch.tensor([int(summ[k]) for k in MAX_KEYS], dtype=torch.int64, device=dev)
+    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    out = dict(summ)
+    out.update({k: int(v) for k, v in zip(SUM_KEYS, s.tolist())})
+    out.update({k: int(v) for k, v in zip(MAX_KEYS, m.tolist())})
+    return out

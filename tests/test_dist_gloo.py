@@ -10,7 +10,7 @@ torch = pytest.importorskip("torch")
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_21048_b200.dist import gather_results, lpt_plan, reorder
+from paper_2510_21048_b200.dist import gather_results, lpt_plan, reduce_summary, reorder
 
 
 def test_lpt_plan_properties():
@@ -102,7 +102,12 @@ def _oracle_worker(rank, world, port, q):
         rec[:, c] = o[f]
     local = torch.from_numpy(rec.view(np.uint8).reshape(len(mine), 64).copy())
     out = gather_results(local, plan, rank)
-    q.put((rank, out.numpy().copy()))
+    summ = {"n_traces": len(mine), "events_done": int(o["events_done"].sum()),
+            "n_oom": int((o["status"] == 1).sum()), "n_overflow": 0,
+            "sum_peak_reserved": int(o["peak_reserved"].sum()), "n_predicted_oom": 0,
+            "max_peak_reserved": int(o["peak_reserved"].max()),
+            "max_peak_allocated": int(o["peak_allocated"].max())}
+    q.put((rank, out.numpy().copy(), reduce_summary(summ)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -120,10 +125,13 @@ def test_sharded_replay_gloo_equals_single_rank():
     for p in ps:
         p.join(60)
         assert p.exitcode == 0
-    (_, o0), (_, o1) = sorted(res, key=lambda x: x[0])
-    assert (o0 == o1).all()
+    (_, o0, s0), (_, o1, s1) = sorted(res, key=lambda x: x[0])
+    assert (o0 == o1).all() and s0 == s1
     idx = np.arange(0, 3000, 97)
     whole = oracle.simulate_batch(mc5.batch(idx))
+    assert s0["n_traces"] == len(idx) and s0["events_done"] == int(whole["events_done"].sum())
+    assert s0["n_oom"] == int((whole["status"] == 1).sum())
+    assert s0["max_peak_reserved"] == int(whole["peak_reserved"].max())
     got = o0.view(np.uint64).reshape(len(idx), 8)
     for c, f in enumerate(["peak_allocated", "peak_allocated_blk", "peak_reserved", "final_reserved",
                            "events_done", "status", "n_seg_alloc", "n_seg_release"]):
