@@ -537,6 +537,9 @@ def main_cfg5(args, world, rank, local):
     torch.cuda.synchronize()
     kern_ms = kt0.elapsed_time(kt1) / args.steps
     h, summ = xm.peaks(out)
+    if world > 1:
+        from paper_2510_21048_b200.dist import reduce_summary
+        summ = reduce_summary(summ, device=dev)
     local_done = int(h["events_done"].astype(np.int64).sum())
     vals = torch.tensor([ms, kern_ms, k4_ms, float(local_done)], dtype=torch.float64, device=dev)
     if world > 1:
