@@ -35,6 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), *(["-DXM_TIMING"] if TIMING else []),
                *([f"-DXM_HEAP_RESERVE_DIV={os.environ['XM_HEAP_RESERVE_DIV']}"] if os.environ.get("XM_HEAP_RESERVE_DIV") else []),
                *([f"-DXM_F_INIT_DIV={os.environ['XM_F_INIT_DIV']}"] if os.environ.get("XM_F_INIT_DIV") else []),
+               *([f"-DXM_ORCH_SMEM_KEYS={os.environ['XM_ORCH_SMEM_KEYS']}"] if os.environ.get("XM_ORCH_SMEM_KEYS") else []),
                "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src),
                "-o", obj]

@@ -16,7 +16,7 @@
 //        BatchData > Activation > Other), re-timed allocation / free, and
 //        64-bit keys (ts - Ws) << 32 | kind << 31 | block;
 //     4. bitonic sort of the keys in shared memory (global scratch for traces
-//        of more than 8192 blocks);
+//        of more than 4096 blocks; two CTAs per SM);
 //     5. warp 0 walks the sorted keys in 32-event tiles, assigns dense block
 //        ids (allocations take ids freed before the tile, else fresh ids) and
 //        stages the wire events at the trace's 2 x block offset;
@@ -32,7 +32,11 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kThreads = 512;
-constexpr int kSmemKeys = 16384;          // 128 KB of keys in shared memory
+#ifndef XM_ORCH_SMEM_KEYS
+#define XM_ORCH_SMEM_KEYS 8192    // 64 KB: two CTAs per SM (the register limit at 512 threads)
+#endif
+constexpr int kSmemKeys = XM_ORCH_SMEM_KEYS;  // keys in shared memory (8 B each)
+constexpr int kCtasPerSm = kSmemKeys > 8192 ? 1 : 2;
 constexpr int kBlockBits = 23;            // quota keys: size << 23 | block (< 2^23 blocks,
 constexpr uint64_t kBlockMask = (1ull << kBlockBits) - 1;   // sizes < 2^41 bytes)
 enum { kParam = 0, kState, kGrad, kData, kAct, kOther };
@@ -86,7 +90,7 @@ __device__ void bitonic(unsigned long long* k, uint32_t n) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_orchestrate(OParams P) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_orchestrate(OParams P) {
   extern __shared__ __align__(16) unsigned long long skeys[];
   __shared__ unsigned int s_trace, s_ncand, s_npar, s_nkeys, s_bad;
   __shared__ unsigned int s_ncls[6];
@@ -351,7 +355,8 @@ OLayout olayout(const xm_profiles* in) {
   if (xm_internal::cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  L.ctas = uint32_t(in->n_traces < sms ? (in->n_traces > 0 ? in->n_traces : 1) : sms);
+  const int64_t max_ctas = int64_t(sms) * kCtasPerSm;
+  L.ctas = uint32_t(in->n_traces < max_ctas ? (in->n_traces > 0 ? in->n_traces : 1) : max_ctas);
   const size_t mb = in->max_blocks ? in->max_blocks : 1;
   uint32_t cap = 1;
   while (cap < 2 * mb) cap <<= 1;
