@@ -44,7 +44,7 @@ def _profiles():
              ("vgg16", "rmsprop", "pos0", 200, False), ("t5_small", "adafactor", "pos1", 10, False),
              ("mobilenet_v2", "sgd", "pos1", 300, False), ("bert_base", "adamw", "pos0", 15, True)]
     p = C.batch(cells)
-    # append synthetic traces: a big one (> 8192 blocks: global-memory sort), a
+    # append synthetic traces: a big one (9000 blocks: global-memory sort), a
     # one-iteration one (status), an empty one
     extra = [_synthetic(9000, 1), _synthetic(300, 2, iters=1), _synthetic(0, 3)]
     A = [p.alloc_ts] + [e[0] for e in extra]
