@@ -36,6 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                *([f"-DXM_HEAP_RESERVE_DIV={os.environ['XM_HEAP_RESERVE_DIV']}"] if os.environ.get("XM_HEAP_RESERVE_DIV") else []),
                *([f"-DXM_F_INIT_DIV={os.environ['XM_F_INIT_DIV']}"] if os.environ.get("XM_F_INIT_DIV") else []),
                *([f"-DXM_ORCH_SMEM_KEYS={os.environ['XM_ORCH_SMEM_KEYS']}"] if os.environ.get("XM_ORCH_SMEM_KEYS") else []),
+               *([f"-DXM_PAGE={os.environ['XM_PAGE']}"] if os.environ.get("XM_PAGE") else []),
                "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src),
                "-o", obj]

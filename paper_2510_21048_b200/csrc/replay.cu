@@ -76,8 +76,11 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kStatusOk = XM_T_OK, kStatusOom = XM_T_OOM, kStatusOverflow = XM_T_OVERFLOW;
 
 // shared-memory heap geometry
-constexpr uint32_t kPage = 512;
-constexpr uint32_t kHdrBytes = 128;
+#ifndef XM_PAGE
+#define XM_PAGE 512
+#endif
+constexpr uint32_t kPage = XM_PAGE;
+constexpr uint32_t kHdrBytes = kPage >= 512 ? 128 : 256;
 constexpr uint32_t kMaxDynSmem = 232448;  // 227 KB, the sm_100 per-CTA maximum
 constexpr uint32_t kMaxPages = (kMaxDynSmem - kHdrBytes) / kPage;  // 453
 constexpr uint32_t kBitmapWords = (kMaxPages + 31) / 32;          // 15
