@@ -411,6 +411,21 @@ int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch, size_t scr
                         uint32_t* d_wire_nids, void* stream);
 
 /*
+ * Reconstruction -> orchestrator input: the blocks each reconstruction defines,
+ * as the Analyzer hands them on ("size, initial CPU-based
+ * allocation and deallocation timestamps"), in allocation order. DEVICE in:
+ * the instants `in` (plus their times d_ts[n_events], microseconds), d_partner
+ * from xm_reconstruct, d_boff[n_traces+1] = exclusive prefix sum of the
+ * reconstruction's n_blocks (trace t's blocks start at d_boff[t]). DEVICE out
+ * [sum n_blocks]: allocation time, free time (-1 = persistent), size (the
+ * allocation's bytes), stream. One launch, asynchronous. Orphan frees are
+ * dropped; a mismatched free still closes its block (reading Q22).
+ */
+int xm_blocks_from_instants(const xm_instants* in, const int64_t* d_ts, const int32_t* d_partner,
+                            const int64_t* d_boff, int64_t* d_alloc_ts, int64_t* d_free_ts,
+                            int64_t* d_size, uint8_t* d_stream, void* stream);
+
+/*
  * Memory Orchestrator (§3.3;
  * SPEC.md:151-203), the step directly before the Simulator. Input: the
  * Analyzer's blocks of each trace in allocation order (CPU timestamps in

@@ -184,6 +184,7 @@ def lib():
         L.xm_orchestrate.argtypes = [ctypes.POINTER(_Profiles), ctypes.c_uint32, P, ctypes.c_size_t,
                                      P, P, P, P]
         L.xm_orchestrate_wire.argtypes = [ctypes.POINTER(_Profiles), P, ctypes.c_size_t] + [P] * 7
+        L.xm_blocks_from_instants.argtypes = [ctypes.POINTER(_Instants)] + [P] * 8
         L.xm_expand_templates.argtypes = [ctypes.POINTER(_Tpl), P, P, P, U64, P, I64, P, P, P, P]
         L.xm_last_error.restype = ctypes.c_char_p
         L.xm_last_launch_count.restype = ctypes.c_int
@@ -645,3 +646,50 @@ def orchestrate(prof: DeviceProfiles, analysis_iter: int = 1, wire: bool = True,
         batch = DeviceBatch(wb[:n_wire], wt[:n_wire], wo, wn[:T], order, None, T, n_wire,
                             int(r["n_ids"].max()) if T else 0, int(n_ev.max()) if T else 0)
     return cls[:B], seq, r, batch
+
+
+# ---- the GPU pipeline: instants -> blocks -> orchestrated sequence -> peaks --------
+def blocks_from_instants(ins: DeviceInstants, ts, partner, rec, stream=None) -> "DeviceProfiles":
+    """xm_blocks_from_instants: the reconstruction's blocks (allocation order)
+    as an orchestrator input without windows (set .win / .woff before use)."""
+    import torch
+    dev = ins.off.device
+    nb = rec["n_blocks"].astype(np.int64) if len(rec) else np.zeros(0, np.int64)
+    boff = np.zeros(ins.n_traces + 1, np.int64)
+    boff[1:] = np.cumsum(nb)
+    B = int(boff[-1])
+    d_boff = torch.from_numpy(boff).to(dev)
+    a = torch.empty(max(B, 1), dtype=torch.int64, device=dev)
+    f = torch.empty(max(B, 1), dtype=torch.int64, device=dev)
+    z = torch.empty(max(B, 1), dtype=torch.int64, device=dev)
+    st = torch.empty(max(B, 1), dtype=torch.uint8, device=dev)
+    c = ins.c()
+
+    def p(x):
+        return ctypes.c_void_p(x.data_ptr()) if x is not None and x.numel() else None
+    rc = lib().xm_blocks_from_instants(ctypes.byref(c), p(ts), p(partner), p(d_boff), p(a), p(f),
+                                       p(z), p(st), _stream_ptr(stream))
+    _check(rc, "xm_blocks_from_instants")
+    return DeviceProfiles(a[:B], f[:B], z[:B], st[:B], d_boff, None, None, ins.n_traces, B,
+                          int(nb.max()) if len(nb) else 0)
+
+
+def estimate(ins: DeviceInstants, ts, win: np.ndarray, woff: np.ndarray, analysis_iter: int = 1,
+             cfg: Config = Config(), capacity: Optional[np.ndarray] = None, stream=None):
+    """xMem's pipeline on the GPU (Fig. 3 after profiling; SPEC.md:296
+    estimate, without the operator attribution): profiler instants -> lifecycle
+    reconstruction (K5) -> blocks -> memory orchestrator (K6) -> replay (K2) ->
+    per-trace results. win [iters, 6, 2] / woff [T+1]: the annotation windows.
+    Returns (results numpy RESULT_DTYPE in trace order, summary, details)."""
+    import torch
+    dev = ins.off.device
+    partner, mism, rec, _ = reconstruct(ins, wire=False, stream=stream)
+    prof = blocks_from_instants(ins, ts, partner, rec, stream=stream)
+    prof.win = torch.from_numpy(np.ascontiguousarray(win, np.int64).reshape(-1)).to(dev)
+    prof.woff = torch.from_numpy(np.ascontiguousarray(woff, np.int64)).to(dev)
+    cls, seq, orec, wb = orchestrate(prof, analysis_iter, stream=stream)
+    if capacity is not None:
+        wb.capacity = torch.from_numpy(np.ascontiguousarray(capacity, np.uint64).view(np.int64)).to(dev)
+    res = simulate_batch(wb, cfg, stream)
+    h, summ = peaks(res, stream=stream)
+    return h, summ, {"lifecycle": rec, "orchestrated": orec, "classes": cls, "profiles": prof}

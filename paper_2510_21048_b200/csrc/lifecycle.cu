@@ -418,3 +418,66 @@ extern "C" int xm_reconstruct_wire(const xm_instants* in, const void* d_scratch,
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct_wire: ") + cudaGetErrorString(e));
   return XM_OK;
 }
+
+// ---- reconstruction -> orchestrator input --------------------------------------
+namespace {
+
+// One warp per trace: the blocks of trace t in allocation order at
+// boff[t] + ordinal: allocation time, free time (-1 = persistent), size,
+// stream -- the Analyzer's block list for xm_orchestrate.
+__global__ void k_blocks(const int64_t* __restrict__ ts, const int64_t* __restrict__ bytes,
+                         const uint8_t* __restrict__ stream, const int64_t* __restrict__ off,
+                         const int32_t* __restrict__ partner, const int64_t* __restrict__ boff,
+                         int64_t T, int64_t* a_ts, int64_t* f_ts, int64_t* size, uint8_t* st) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = w0; t < T; t += nw) {
+    const int64_t e0 = off[t];
+    const int n = int(off[t + 1] - e0);
+    int64_t ord = boff[t];
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + int(lane);
+      const int64_t b = i < n ? bytes[e0 + i] : 0;
+      const bool al = b > 0;
+      const unsigned am = __ballot_sync(0xFFFFFFFFu, al);
+      if (al) {
+        const int64_t o = ord + __popc(am & lt);
+        const int p = partner[e0 + i];
+        a_ts[o] = ts[e0 + i];
+        f_ts[o] = p >= 0 ? ts[e0 + p] : -1;
+        size[o] = b;
+        st[o] = stream ? stream[e0 + i] : 0;
+      }
+      ord += __popc(am);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int xm_blocks_from_instants(const xm_instants* in, const int64_t* d_ts,
+                                       const int32_t* d_partner, const int64_t* d_boff,
+                                       int64_t* d_alloc_ts, int64_t* d_free_ts, int64_t* d_size,
+                                       uint8_t* d_stream, void* stream) {
+  launch_counter() = 0;
+  if (!in || in->n_traces < 0) return set_error(XM_EINVAL, "xm_blocks_from_instants: bad arguments");
+  if (in->n_traces == 0) return XM_OK;
+  if (!in->off || !d_boff || (in->n_events > 0 && (!in->bytes || !d_ts || !d_partner)) ||
+      !d_alloc_ts || !d_free_ts || !d_size || !d_stream)
+    return set_error(XM_EINVAL, "xm_blocks_from_instants: null pointer");
+  if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (in->n_traces + 7) / 8;
+  const int g = int(std::min<int64_t>(std::max<int64_t>(want, 1), int64_t(sms) * 8));
+  k_blocks<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_ts, in->bytes, in->stream, in->off, d_partner, d_boff, in->n_traces, d_alloc_ts, d_free_ts,
+      d_size, d_stream);
+  launch_counter() = 1;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("k_blocks: ") + cudaGetErrorString(e));
+  return XM_OK;
+}

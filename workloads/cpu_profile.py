@@ -130,3 +130,43 @@ def suite_cells(n: int, salt: int = 13):
         name, opt, b, zg, cap, _ = suites.mc_draw(i, salt)
         out.append((name, opt, zg, b, False))
     return out
+
+
+def to_instants(p: Profiles, salt: int = 17):
+    """The profiler's memory instants behind a Profiles batch (PAPER.md:215
+    cpu_instant_event: time, address, signed bytes): per trace, every block's
+    allocation and (if observed) deallocation, in time order (ties in block
+    order, allocation before deallocation of later blocks as generated), with
+    CPU-allocator-like addresses (a freed address is reused LIFO by the next
+    allocation of the same size, else a 64 B-aligned bump pointer).
+    Returns (ts, addr, bytes, stream, off) numpy arrays."""
+    T = p.n_traces
+    TS, AD, BY, ST, off = [], [], [], [], [0]
+    for t in range(T):
+        a, f, s, st, _ = p.trace(t)
+        ev = [(int(a[i]), 0, i, 1) for i in range(len(a))]
+        ev += [(int(f[i]), 1, i, -1) for i in range(len(a)) if f[i] >= 0]
+        ev.sort()
+        g = generator(trace_seed(t, salt))
+        bump = 0x7E0000000000 + (int(g.integers(0, 1 << 20)) << 12)
+        free_lists, where = {}, {}
+        for (ts, _, i, sign) in ev:
+            sz = int(s[i])
+            if sign > 0:
+                fl = free_lists.get(sz)
+                if fl:
+                    ad = fl.pop()
+                else:
+                    ad = bump
+                    bump += (sz + 63) // 64 * 64
+                where[i] = ad
+            else:
+                ad = where.pop(i)
+                free_lists.setdefault(sz, []).append(ad)
+            TS.append(ts)
+            AD.append(ad)
+            BY.append(sign * sz)
+            ST.append(int(st[i]))
+        off.append(len(TS))
+    return (np.asarray(TS, np.int64), np.asarray(AD, np.uint64), np.asarray(BY, np.int64),
+            np.asarray(ST, np.uint8), np.asarray(off, np.int64))
