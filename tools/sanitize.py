@@ -37,6 +37,9 @@ xm.peaks(xm.simulate_batch(wb))                                                #
 p = cpu_profile.batch([("mobilenet_v2", "adam", "pos0", 200, False), ("gpt2", "adamw", "pos1", 5, True)])
 _, _, _, ob = xm.orchestrate(xm.DeviceProfiles.from_host(p))
 xm.peaks(xm.simulate_batch(ob))                                                # K6
+ts, ad, by, st, off = cpu_profile.to_instants(p)
+h, _, _ = xm.estimate(xm.DeviceInstants.from_host(ad, by, st, off), torch.from_numpy(ts).cuda(),
+                      p.win, p.woff)                                           # pipeline
 r = np.zeros(100, xm.RUN_DTYPE)
 r["m_max"] = 8 << 30
 r["m_peak_est"] = np.arange(1, 101) << 26

@@ -1,5 +1,5 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 5 python tools/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "== $tool: exit $?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|sanitize run done|Error|error" gpurun_out/sanitize_$tool.log | head -8
+for tool in memcheck synccheck racecheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "== $tool: exit $?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|sanitize run done" gpurun_out/sanitize_$tool.log | head -4
 done
