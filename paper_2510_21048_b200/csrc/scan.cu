@@ -362,9 +362,15 @@ __global__ void k_scan_combine(SParams P) {
 // and one arg-max reduction, and warp 0 folds the warp pieces in order onto
 // the running prefix. 8 B read per event, 2 barriers per step.
 constexpr int kTraceMax = 1 << 16;
-constexpr int kTWarps = 4;
+#ifndef XM_K1_WARPS
+#define XM_K1_WARPS 4
+#endif
+#ifndef XM_K1_PER_LANE
+#define XM_K1_PER_LANE 8
+#endif
+constexpr int kTWarps = XM_K1_WARPS;
 constexpr int kTThreads = 32 * kTWarps;
-constexpr int kPerLane = 8;
+constexpr int kPerLane = XM_K1_PER_LANE;
 constexpr int kWarpSpan = 32 * kPerLane;
 constexpr int kStep = kTWarps * kWarpSpan;
 
@@ -509,7 +515,7 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * 16);
+    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * (64 / kTWarps));
     if (P.packed) k_scan_trace<true><<<unsigned(grid), kTThreads, 0, st>>>(P);
     else k_scan_trace<false><<<unsigned(grid), kTThreads, 0, st>>>(P);
     *n_launches += 1;
