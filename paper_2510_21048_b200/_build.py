@@ -38,6 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                *([f"-DXM_ORCH_SMEM_KEYS={os.environ['XM_ORCH_SMEM_KEYS']}"] if os.environ.get("XM_ORCH_SMEM_KEYS") else []),
                *([f"-DXM_PAGE={os.environ['XM_PAGE']}"] if os.environ.get("XM_PAGE") else []),
                *([f"-DXM_K1_WARPS={os.environ['XM_K1_WARPS']}"] if os.environ.get("XM_K1_WARPS") else []),
+               *([f"-DXM_MAX_NAP={os.environ['XM_MAX_NAP']}"] if os.environ.get("XM_MAX_NAP") else []),
                *([f"-DXM_K1_PER_LANE={os.environ['XM_K1_PER_LANE']}"] if os.environ.get("XM_K1_PER_LANE") else []),
                "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src),

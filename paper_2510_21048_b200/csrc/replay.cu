@@ -44,6 +44,9 @@
 #include "rounding.cuh"
 #include "xm_internal.h"
 
+#ifndef XM_MAX_NAP
+#define XM_MAX_NAP 16384        // ns: longest back-off of a warp waiting for admission
+#endif
 #ifndef XM_F_INIT_DIV
 #define XM_F_INIT_DIV 4         // initial free-list capacity: n_ids / 4 + 64 entries
 #endif
@@ -408,7 +411,7 @@ __device__ void ticket_acquire(HeapHdr* h, uint32_t* stats, int first = -1) {
     const int srv = __shfl_sync(kFull, *(volatile int*)&h->serving, 0);
     if (srv == t) break;
     __nanosleep(nap);
-    nap = min(nap * 2, 16384u);
+    nap = min(nap * 2, uint32_t(XM_MAX_NAP));
     ++tw;
   }
   if (lane == 0 && tw) atomicAdd(stats + 3, tw);
@@ -438,7 +441,7 @@ __device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t
     start = admit ? first_fit(h, total, np) : kNone32;
     if (start != kNone32 && try_claim(h, start, np)) break;
     __nanosleep(nap);
-    nap = min(nap * 2, 16384u);
+    nap = min(nap * 2, uint32_t(XM_MAX_NAP));
     ++hw;
   }
   if (lane == 0 && hw) atomicAdd(stats + 2, hw);
