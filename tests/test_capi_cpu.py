@@ -186,3 +186,19 @@ def test_packed_events_encode_bytes_and_tags():
     b = np.where((v >> np.uint64(41)) & np.uint64(1), mag, -mag)
     t = ((v >> np.uint64(46)) | (((v >> np.uint64(42)) & np.uint64(0xF)) << np.uint64(28))).astype(np.uint32)
     assert (b == tr.bytes).all() and (t == tr.tag).all()
+
+
+def test_widened_entry_points_fail_loudly_without_gpu():
+    """Every device entry point of the widened rows returns an error (never a
+    CPU fallback) when there is no CUDA device."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    L = xm.lib()
+    ins = xm._Instants(None, None, None, None, 1, 0, 0)
+    assert L.xm_reconstruct(ctypes.byref(ins), None, 0, None, None, None, None) != 0
+    assert L.xm_blocks_from_instants(ctypes.byref(ins), *([None] * 8)) != 0
+    prof = xm._Profiles(None, None, None, None, None, None, None, 1, 0, 0)
+    assert L.xm_orchestrate(ctypes.byref(prof), 1, None, 0, None, None, None, None) != 0
+    m = xm._Metrics()
+    assert L.xm_metrics_batch(None, 1, None, 0, ctypes.byref(m), None) != 0
