@@ -102,13 +102,19 @@ def main():
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1, sort_keys=True)
     lines = [f"# ncu summary, round {rnd}", "",
-             "| kernel | duration | DRAM bytes/launch | DRAM GB/s | DRAM % peak | issue active % | occupancy % | regs | warp inst |",
+             "| kernel | duration | DRAM bytes/launch | DRAM GB/s | % of measured HBM peak | issue active % | occupancy % | regs | warp inst |",
              "|---|---|---|---|---|---|---|---|---|"]
     def num(d, k):
         v = d.get(k, 0)
         return v if isinstance(v, float) else 0.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm = 6650.0                       # B200_PROFILING.md fallback
     for k, d in summ["kernels"].items():
         d = {kk: (vv if not isinstance(vv, str) or kk == "source" else 0.0) for kk, vv in d.items()}
+        d["dram_throughput_pct"] = 100.0 * d.get("dram_GBps", 0) / hbm
         lines.append(f"| {k} | {d.get('duration_ns', 0) / 1e6:.3f} ms | {d['dram_bytes_per_launch']:.4g} | "
                      f"{d.get('dram_GBps', 0):.0f} | "
                      f"{d.get('dram_throughput_pct', 0):.1f} | {d.get('issue_active_pct', 0):.1f} | "
