@@ -374,7 +374,14 @@ constexpr int kPerLane = XM_K1_PER_LANE;
 constexpr int kWarpSpan = 32 * kPerLane;
 constexpr int kStep = kTWarps * kWarpSpan;
 
-template <bool kPacked>
+// a2 for K1t: the plain 512 B rule as one shift, or the divisions variant
+template <bool kDiv>
+__device__ __forceinline__ int64_t k1_delta(int64_t b, const SParams& P) {
+  if constexpr (kDiv) return rounded_delta(b, P.u);
+  else return rounded_delta(b, P.unit_shift);
+}
+
+template <bool kPacked, bool kDiv>
 __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
   __shared__ long long s_sum[kTWarps], s_mx[kTWarps];
   __shared__ int s_arg[kTWarps];
@@ -410,13 +417,22 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
       load(nxt, base + kStep);
       long long run = 0, lmx = kNeg;
       int larg = -1;
+      if ((base > 0 || sh == 0) && base + kStep <= m) {    // every position valid
 #pragma unroll
-      for (int q = 0; q < kPerLane; ++q) {
-        const int idx = base + p0 + q - sh;             // event index in the trace
-        const long long raw = (q & 1) ? cur[q >> 1].y : cur[q >> 1].x;
-        if (idx >= 0 && idx < n) {
-          run += rounded_delta(kPacked ? unpack_bytes(raw) : raw, P.u);
-          if (run > lmx) { lmx = run; larg = idx; }
+        for (int q = 0; q < kPerLane; ++q) {
+          const long long raw = (q & 1) ? cur[q >> 1].y : cur[q >> 1].x;
+          run += k1_delta<kDiv>(kPacked ? unpack_bytes(raw) : raw, P);
+          if (run > lmx) { lmx = run; larg = base + p0 + q - sh; }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kPerLane; ++q) {
+          const int idx = base + p0 + q - sh;           // event index in the trace
+          const long long raw = (q & 1) ? cur[q >> 1].y : cur[q >> 1].x;
+          if (idx >= 0 && idx < n) {
+            run += k1_delta<kDiv>(kPacked ? unpack_bytes(raw) : raw, P);
+            if (run > lmx) { lmx = run; larg = idx; }
+          }
         }
       }
       long long ex = run;                     // exclusive scan of the lane sums
@@ -516,8 +532,14 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * (64 / kTWarps));
-    if (P.packed) k_scan_trace<true><<<unsigned(grid), kTThreads, 0, st>>>(P);
-    else k_scan_trace<false><<<unsigned(grid), kTThreads, 0, st>>>(P);
+    const bool dv = u.div_shift != 0;
+    if (P.packed) {
+      if (dv) k_scan_trace<true, true><<<unsigned(grid), kTThreads, 0, st>>>(P);
+      else k_scan_trace<true, false><<<unsigned(grid), kTThreads, 0, st>>>(P);
+    } else {
+      if (dv) k_scan_trace<false, true><<<unsigned(grid), kTThreads, 0, st>>>(P);
+      else k_scan_trace<false, false><<<unsigned(grid), kTThreads, 0, st>>>(P);
+    }
     *n_launches += 1;
     return int(cudaGetLastError());
   }
