@@ -675,11 +675,15 @@ def blocks_from_instants(ins: DeviceInstants, ts, partner, rec, stream=None) -> 
 
 
 def estimate(ins: DeviceInstants, ts, win: np.ndarray, woff: np.ndarray, analysis_iter: int = 1,
-             cfg: Config = Config(), capacity: Optional[np.ndarray] = None, stream=None):
+             cfg: Config = Config(), capacity: Optional[np.ndarray] = None, stream=None,
+             curve: bool = False):
     """xMem's pipeline on the GPU (Fig. 3 after profiling; SPEC.md:296
     estimate, without the operator attribution): profiler instants -> lifecycle
     reconstruction (K5) -> blocks -> memory orchestrator (K6) -> replay (K2) ->
     per-trace results. win [iters, 6, 2] / woff [T+1]: the annotation windows.
+    curve=True adds the memory-usage curve of the re-timed sequences (P:205
+    "an optional detailed memory usage curve"; rows in the wire batch's stored
+    order: details["wire"].off / .order locate trace t).
     Returns (results numpy RESULT_DTYPE in trace order, summary, details)."""
     import torch
     dev = ins.off.device
@@ -690,6 +694,10 @@ def estimate(ins: DeviceInstants, ts, win: np.ndarray, woff: np.ndarray, analysi
     cls, seq, orec, wb = orchestrate(prof, analysis_iter, stream=stream)
     if capacity is not None:
         wb.capacity = torch.from_numpy(np.ascontiguousarray(capacity, np.uint64).view(np.int64)).to(dev)
-    res = simulate_batch(wb, cfg, stream)
+    cv = None
+    if curve:
+        cv = torch.zeros((wb.n_events, 3), dtype=torch.int64, device=dev)
+    res = simulate_batch(wb, cfg, stream, curve=cv)
     h, summ = peaks(res, stream=stream)
-    return h, summ, {"lifecycle": rec, "orchestrated": orec, "classes": cls, "profiles": prof}
+    return h, summ, {"lifecycle": rec, "orchestrated": orec, "classes": cls, "profiles": prof,
+                     "wire": wb, "curve": cv}

@@ -67,3 +67,31 @@ def test_estimate_pipeline_matches_oracle_chain(capacity):
             assert int(h[k][t]) == exp, (p.names[t], k, int(h[k][t]), exp)
     if capacity is not None:
         assert summ["n_oom"] > 0
+
+
+def test_estimate_curve_matches_oracle_curve():
+    """The pipeline's optional memory-usage curve equals the
+    oracle's curve of the same re-timed sequence, event by event."""
+    p = C.batch(CELLS[:3])
+    ts, ad, by, st, off = C.to_instants(p)
+    d = xm.DeviceInstants.from_host(ad, by, st, off)
+    h, _, det = xm.estimate(d, torch.from_numpy(ts).cuda(), p.win, p.woff, curve=True)
+    wb = det["wire"]
+    cv = det["curve"].cpu().numpy().view(np.uint64)
+    woff = wb.off.cpu().numpy()
+    order = wb.order.cpu().numpy().view(np.uint32)
+    pos = np.empty(p.n_traces, np.int64)
+    pos[order] = np.arange(p.n_traces)
+    for t in range(p.n_traces):
+        z0, z1 = int(off[t]), int(off[t + 1])
+        W = p.win[p.woff[t]:p.woff[t + 1]]
+        part, _, _ = oracle.reconstruct(ad[z0:z1], by[z0:z1])
+        al = np.flatnonzero(by[z0:z1] > 0)
+        a = ts[z0:z1][al]
+        f = np.where(part[al] >= 0, ts[z0:z1][np.maximum(part[al], 0)], -1)
+        s = by[z0:z1][al]
+        _, ev = O.orchestrate(a, f, s, W)
+        wbb, wtt = O.wire(ev, s, st[z0:z1][al])
+        r, oc = oracle.simulate_trace(wbb, wtt, curve=True)
+        q = pos[t]
+        assert (cv[woff[q]:woff[q + 1]] == oc).all(), t
