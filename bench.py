@@ -255,6 +255,29 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- our arm
+def _device(local):
+    """cuda:LOCAL_RANK. XM_BENCH_DEVICE=k pins every rank to GPU k -- a
+    debugging aid only, to run the N>1 code path on a one-GPU box (with
+    XM_BENCH_BACKEND=gloo; NCCL refuses two ranks on one GPU)."""
+    import torch
+    k = int(os.environ.get("XM_BENCH_DEVICE", local))
+    torch.cuda.set_device(k)
+    return torch.device("cuda", k)
+
+
+def _cdev(dev):
+    """Device of the small all-reduce tensors: host memory under gloo."""
+    import torch.distributed as dist
+    return "cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else dev
+
+
+def _init_dist(dev):
+    import torch.distributed as dist
+    backend = os.environ.get("XM_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
 def main():
     args = parse()
     world, rank, local = dist_env()
@@ -270,10 +293,9 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: CUDA device required (no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = _device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
 
     batch, plan, desc, total_ev, total_tr = workload(args.workload, world, rank)
     tr = xm.load_traces(batch.bytes, batch.tag, batch.off)
@@ -329,7 +351,7 @@ def main():
     torch.cuda.synchronize()
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kevs]))
     if world > 1:
-        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=_cdev(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kern_ms = float(t[0]), float(t[1])
 
@@ -341,7 +363,7 @@ def main():
     local_done = int(h["events_done"].astype(np.int64).sum())
     done = local_done
     if world > 1:
-        t = torch.tensor([local_done], dtype=torch.int64, device=dev)
+        t = torch.tensor([local_done], dtype=torch.int64, device=_cdev(dev))
         dist.all_reduce(t)
         done = int(t[0])
     value = done / (ms / 1e3)
@@ -360,7 +382,7 @@ def main():
             h_e2e, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
         dt = (time.perf_counter() - t0) / args.steps
         if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            t = torch.tensor([dt], dtype=torch.float64, device=_cdev(dev))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t[0])
         ev_bytes = 8 if tr.packed is not None else 12        # packed or bytes + tag
@@ -480,10 +502,9 @@ def main_cfg5(args, world, rank, local):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: CUDA device required (no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = _device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
     n = args.cfg5_traces
     d_all = mc5.describe(np.arange(n))
     L = mc5.lengths(d_all)
@@ -541,7 +562,7 @@ def main_cfg5(args, world, rank, local):
         from paper_2510_21048_b200.dist import reduce_summary
         summ = reduce_summary(summ, device=dev)
     local_done = int(h["events_done"].astype(np.int64).sum())
-    vals = torch.tensor([ms, kern_ms, k4_ms, float(local_done)], dtype=torch.float64, device=dev)
+    vals = torch.tensor([ms, kern_ms, k4_ms, float(local_done)], dtype=torch.float64, device=_cdev(dev))
     if world > 1:
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -568,7 +589,7 @@ def main_cfg5(args, world, rank, local):
             del db2
         dt = (time.perf_counter() - tt) / reps
         if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            t = torch.tensor([dt], dtype=torch.float64, device=_cdev(dev))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t[0])
         T = len(mine)

@@ -54,11 +54,13 @@ def gather_results(local, plan: ShardPlan, rank: int, group=None):
     W = plan.world
     M = plan.max_shard
     width = local.shape[1] if local.dim() == 2 else 64
-    pad = torch.zeros((M, width), dtype=torch.uint8, device=local.device)
-    pad[: local.shape[0]] = local
-    full = torch.empty((W * M, width), dtype=torch.uint8, device=local.device)
+    # gloo (CPU tests, debugging) gathers host tensors; NCCL the device ones
+    dev = "cpu" if dist.get_backend(group) == "gloo" else local.device
+    pad = torch.zeros((M, width), dtype=torch.uint8, device=dev)
+    pad[: local.shape[0]] = local.to(dev)
+    full = torch.empty((W * M, width), dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(full, pad, group=group)
-    return reorder(full, plan)
+    return reorder(full, plan).to(local.device)
 
 
 def reorder(full, plan: ShardPlan):
@@ -83,7 +85,7 @@ def reduce_summary(summ: dict, device=None, group=None) -> dict:
     summed, peaks maxed -- two small all_reduce calls."""
     import torch
     import torch.distributed as dist
-    dev = device if device is not None else "cpu"
+    dev = device if device is not None and dist.get_backend(group) != "gloo" else "cpu"
     s = torch.tensor([int(summ[k]) for k in SUM_KEYS], dtype=torch.int64, device=dev)
     m = torch.tensor([int(summ[k]) for k in MAX_KEYS], dtype=torch.int64, device=dev)
     dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
