@@ -17,8 +17,9 @@
 //       the allocations' event indices); each trace clears and uses the
 //       first 2^ceil(log2 2n) slots of its warp's region. When the tile's addresses are distinct (the common
 //       case: __match_any_sync) every lane does its own lookup, insertions are
-//       resolved by a read phase / claim phase loop; otherwise the tile runs
-//       one instant at a time;
+//       resolved by a read phase / claim phase loop; instants sharing an
+//       address inside a tile are applied in rounds (round r: every
+//       address's r-th instant);
 //     * per instant: partner (alloc <-> free, -1 persistent / orphan),
 //       mismatch flag; kept events are written compacted within the trace at
 //       its input offset (staging), ids of matched blocks go back on the stack;
@@ -67,29 +68,6 @@ struct LParams {
 
 __device__ __forceinline__ uint32_t hash_addr(uint64_t a, uint32_t bits) {
   return uint32_t((a * 0x9E3779B97F4A7C15ull) >> (64 - bits));
-}
-
-// One instant, done by one lane: the sequential definition (probe, insert if
-// absent, push or pop). Used when addresses repeat inside a tile.
-__device__ __forceinline__ void op_serial(const LParams& P, Slot* T, uint32_t hmask,
-                                          uint32_t hbits, unsigned gen, int64_t e0, int li,
-                                          uint64_t a, int64_t b, bool& matched, int& blk) {
-  uint32_t h = hash_addr(a, hbits);
-  for (;;) {
-    if (T[h].gen != gen) break;
-    if (T[h].addr == a) break;
-    h = (h + 1) & hmask;
-  }
-  const bool found = T[h].gen == gen;
-  if (b > 0) {
-    if (!found) { T[h].addr = a; T[h].gen = gen; T[h].top = -1; }
-    P.below[e0 + li] = T[h].top;
-    T[h].top = li;
-  } else if (found && T[h].top >= 0) {
-    blk = T[h].top;
-    T[h].top = P.below[e0 + blk];
-    matched = true;
-  }
 }
 
 __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
@@ -143,13 +121,19 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       // ---- matching (LIFO per address) ----
       bool matched = false;
       int blk = -1;
+      // Lanes with the same address form a group; its instants must be
+      // applied in time order, different addresses touch different keys. So
+      // round r applies every group's r-th instant at once (one round when
+      // the tile's addresses are distinct, the common case).
       const unsigned grp = __match_any_sync(kFull, a);
-      const bool repeat = __any_sync(kFull, valid && __popc(grp) > 1);
-      if (!repeat) {
+      const uint32_t my_rank = __popc(grp & lt);
+      const uint32_t rounds = __reduce_max_sync(kFull, valid ? uint32_t(__popc(grp)) : 0u);
+      for (uint32_t r = 0; r < rounds; ++r) {
+        const bool act = valid && b != 0 && my_rank == r;
         // read phase: find my key or the first free slot of my probe sequence
         uint32_t h = hash_addr(a, hb);
         bool found = false;
-        if (valid) {
+        if (act) {
           for (;;) {
             if (T[h].gen != gen) break;
             if (T[h].addr == a) { found = true; break; }
@@ -158,7 +142,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
         }
         // claim phase for allocations at new addresses: lanes aiming at the
         // same free slot -> the lowest wins, the others probe on
-        bool pend = is_alloc && !found;
+        bool pend = act && is_alloc && !found;
         while (__any_sync(kFull, pend)) {
           const unsigned same = __match_any_sync(kFull, pend ? h : 0xFFFFFFFFu);
           const bool win = pend && (__ffs(same) - 1) == int(lane);
@@ -175,20 +159,17 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
           pend = pend && !win;
         }
         __syncwarp();
-        if (is_alloc) {
-          P.below[e0 + li] = T[h].top;
-          T[h].top = li;
-        } else if (is_free && found && T[h].top >= 0) {
-          blk = T[h].top;
-          T[h].top = P.below[e0 + blk];
-          matched = true;
+        if (act) {
+          if (is_alloc) {
+            P.below[e0 + li] = T[h].top;
+            T[h].top = li;
+          } else if (found && T[h].top >= 0) {
+            blk = T[h].top;
+            T[h].top = P.below[e0 + blk];
+            matched = true;
+          }
         }
-      } else {
-        const int cnt = min(32, n - base);
-        for (int j = 0; j < cnt; ++j) {
-          if (int(lane) == j && b != 0) op_serial(P, T, hmask, hb, gen, e0, li, a, b, matched, blk);
-          __syncwarp();
-        }
+        __syncwarp();
       }
       __syncwarp();
       // ---- per-instant outputs ----
