@@ -373,27 +373,49 @@ def main():
     if not args.no_e2e:
         ws = None
         capn = np.ascontiguousarray(batch.capacity, np.uint64) if has_cap else None
-        for _ in range(2):
-            _, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            h_e2e, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
-        dt = (time.perf_counter() - t0) / args.steps
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=_cdev(dev))
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t[0])
+
+        def e2e_ms(mode):
+            """Mean wall time of xm_simulate_host with event input `mode`
+            (XM_HOST_INPUT, capi.cu); None = the library default."""
+            nonlocal ws
+            old_mode = os.environ.pop("XM_HOST_INPUT", None)
+            if mode:
+                os.environ["XM_HOST_INPUT"] = mode
+            try:
+                for _ in range(2):
+                    _, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
+                if world > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                for _ in range(args.steps):
+                    hh, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
+                dt = (time.perf_counter() - t0) / args.steps
+            finally:
+                os.environ.pop("XM_HOST_INPUT", None)
+                if old_mode is not None:
+                    os.environ["XM_HOST_INPUT"] = old_mode
+            if world > 1:
+                t = torch.tensor([dt], dtype=torch.float64, device=_cdev(dev))
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t[0])
+            return dt, hh
+
+        dt, h_e2e = e2e_ms(None)
+        dt_stream, h_stream = e2e_ms("stream")
         ev_bytes = 8 if tr.packed is not None else 12        # packed or bytes + tag
         h2d = ev_bytes * batch.n_events + 8 * (batch.n_traces + 1) \
             + 8 * batch.n_traces + (8 * batch.n_traces if has_cap else 0)
+        direct = tr.packed is not None and not os.environ.get("XM_NO_STREAM") \
+            and os.environ.get("XM_HOST_INPUT", "direct") == "direct"
         e2e = {"value": done / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(64 * batch.n_traces), "ms_per_step": dt * 1e3,
                "api": "xm_simulate_host (pinned host traces -> device -> host results; "
-                      "upload streamed in longest-first chunks overlapping the replay; "
+                      + ("events read by the replaying warps straight from the page-locked "
+                         "host array over PCIe, no staging copy; " if direct else
+                         "upload streamed in longest-first chunks overlapping the replay; ")
                       + ("8-byte packed events)" if tr.packed is not None else "12-byte events)"),
-               "results_equal_device_path": bool((h_e2e == h).all())}
+               "stream_copy_ms_per_step": dt_stream * 1e3,
+               "results_equal_device_path": bool((h_e2e == h).all() and (h_stream == h).all())}
     clocks = sampler.stop() if sampler else None
 
     # ---- roofline of the dominant kernel (k_replay): algorithmic bytes / launch time

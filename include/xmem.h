@@ -254,14 +254,25 @@ int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_summary* h_
              uint64_t capacity_for_eq1, void* stream);
 
 /*
- * End-to-end entry point with HOST buffers: copies the packed batch to the
- * DEVICE workspace d_ws (>= xm_host_ws_bytes()), replays it, copies the
+ * End-to-end entry point with HOST buffers: moves the batch's events from
+ * host memory to the replay, replays it using the DEVICE workspace d_ws
+ * (>= xm_host_ws_bytes(); the metadata always goes there), copies the
  * results to h_out[n_traces] (HOST, caller order) and synchronises `stream`.
  *   capacity: HOST [n_traces] per-trace capacities (caller order) or NULL.
- * In XM_FULL mode the event upload is streamed: chunks of whole traces, in
- * stored (longest-first) order, go over a library-owned copy stream while the
- * replay kernel already runs on `stream`, each trace starting once its chunk
- * is resident (env XM_NO_STREAM=1 copies everything first, for comparison).
+ * Event input in XM_FULL mode (env XM_HOST_INPUT overrides the default):
+ *   direct  (default when the packed array is page-locked and device-mapped,
+ *           i.e. the batch was loaded with CUDA available): each replaying
+ *           warp loads its trace's 8-byte events IN PLACE from the host array
+ *           over PCIe, two 32-event tiles ahead of the replay; nothing is
+ *           staged in HBM. The host array must stay alive and unchanged until
+ *           the call returns (it does: the call is synchronous).
+ *   stream  (the fallback): chunks of whole traces, in stored order, are
+ *           copied into d_ws on a library-owned copy stream while the replay
+ *           kernel already runs on `stream`, each trace starting once its
+ *           chunk is resident.
+ *   copy    (or XM_NO_STREAM=1; always for XM_ALLOCATED_ONLY): everything is
+ *           copied before the launch.
+ * All three give identical results.
  */
 size_t xm_host_ws_bytes(const xm_traces* tr, const xm_config* cfg);
 int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_config* cfg,

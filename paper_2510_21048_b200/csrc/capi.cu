@@ -292,13 +292,31 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   auto cp = [&](size_t o, const void* src, size_t n, cudaStream_t s) {
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, s);
   };
-  const bool streamed = cfg->mode == XM_FULL && I.n_chunks > 0 && !std::getenv("XM_NO_STREAM");
+  // event input (include/xmem.h): DIRECT (the default when the packed host
+  // array is device-mapped) = the replaying warps load the events in place
+  // from host memory over PCIe, nothing staged in HBM; STREAM = chunked copies
+  // on a copy stream overlapping the replay; COPY = everything copied first.
+  // XM_HOST_INPUT=direct|stream|copy overrides; XM_NO_STREAM=1 = copy.
+  const char* hin = std::getenv("XM_HOST_INPUT");
+  auto is = [&](const char* m) { return hin && !std::strcmp(hin, m); };
+  const bool want_copy = std::getenv("XM_NO_STREAM") || is("copy");
+  const uint64_t* h_direct = nullptr;        // device-usable pointer of I.packed
+  if (cfg->mode == XM_FULL && I.packed && I.n_events > 0 && !want_copy && !is("stream")) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, const_cast<uint64_t*>(I.packed), 0) == cudaSuccess)
+      h_direct = static_cast<const uint64_t*>(dp);
+    else
+      cudaGetLastError();        // not page-locked (loaded without CUDA): stream instead
+  }
+  const bool streamed = !h_direct && cfg->mode == XM_FULL && I.n_chunks > 0 && !want_copy;
   cp(L.off, I.off, sizeof(int64_t) * (I.n_traces + 1), st);
   cp(L.n_ids, I.n_ids, sizeof(uint32_t) * I.n_traces, st);
   cp(L.order, I.order, sizeof(uint32_t) * I.n_traces, st);
   if (capacity) cp(L.cap, capacity, sizeof(uint64_t) * I.n_traces, st);
   uint32_t* ready = reinterpret_cast<uint32_t*>(w + L.ready);
-  if (!streamed) {
+  if (h_direct) {
+    // DIRECT: nothing staged (h2d traffic = the events, read by the kernel)
+  } else if (!streamed) {
     if (I.packed) {
       cp(L.packed, I.packed, sizeof(uint64_t) * I.n_events, st);
     } else {
@@ -346,7 +364,7 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   xm_batch b{};
   b.bytes = I.packed ? nullptr : reinterpret_cast<const int64_t*>(w + L.bytes);
   b.tag = I.packed ? nullptr : reinterpret_cast<const uint32_t*>(w + L.tag);
-  b.packed = I.packed ? reinterpret_cast<const uint64_t*>(w + L.packed) : nullptr;
+  b.packed = h_direct ? h_direct : I.packed ? reinterpret_cast<const uint64_t*>(w + L.packed) : nullptr;
   b.off = reinterpret_cast<const int64_t*>(w + L.off);
   b.n_ids = reinterpret_cast<const uint32_t*>(w + L.n_ids);
   b.order = reinterpret_cast<const uint32_t*>(w + L.order);

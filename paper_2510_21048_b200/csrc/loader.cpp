@@ -43,7 +43,7 @@ namespace {
 void* host_alloc(xm_traces* tr, size_t n) {
   if (n == 0) n = 8;
   void* p = nullptr;
-  if (xm_internal::cuda_usable() && cudaHostAlloc(&p, n, cudaHostAllocDefault) == cudaSuccess) {
+  if (xm_internal::cuda_usable() && cudaHostAlloc(&p, n, cudaHostAllocMapped) == cudaSuccess) {
     tr->blocks.push_back(p);
     tr->pinned.push_back(true);
     return p;

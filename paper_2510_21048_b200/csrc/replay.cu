@@ -690,16 +690,14 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   const uint32_t* __restrict__ tg = P.tag + e0;
   const unsigned long long* __restrict__ pk = P.packed ? P.packed + e0 : nullptr;
   // one event: signed request bytes and tag, from the 12-byte or the packed form
+  auto unpack = [](unsigned long long v, int64_t& b, uint32_t& t) {
+    const int64_t m = int64_t(v & ((1ull << 41) - 1));
+    b = (v >> 41) & 1ull ? m : -m;
+    t = uint32_t(v >> 46) | (uint32_t((v >> 42) & 0xFull) << 28);
+  };
   auto load_event = [&](uint32_t i, int64_t& b, uint32_t& t) {
-    if (pk) {
-      const unsigned long long v = __ldcg(pk + i);
-      const int64_t m = int64_t(v & ((1ull << 41) - 1));
-      b = (v >> 41) & 1ull ? m : -m;
-      t = uint32_t(v >> 46) | (uint32_t((v >> 42) & 0xFull) << 28);
-    } else {
-      b = __ldcg(by + i);
-      t = __ldcg(tg + i);
-    }
+    b = __ldcg(by + i);
+    t = __ldcg(tg + i);
   };
   uint64_t* const curve = kCurve ? P.curve + 3 * size_t(e0) : nullptr;
   Acc c_blk = 0, c_res = 0;               // curve: this lane's event of the tile
@@ -714,14 +712,32 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   int status = kStatusOk;
   uint32_t done_total = 0;
 
+  // events are loaded ahead of the replay: the packed form two tiles ahead
+  // (raw words; the events may be read straight from host memory over PCIe,
+  // xm_simulate_host's direct input, so the lead covers that latency), the
+  // 12-byte form one tile ahead
   int64_t b_nx = 0;
   uint32_t t_nx = 0;
-  if (lane < n) load_event(lane, b_nx, t_nx);
+  unsigned long long q1 = 0, q2 = 0;
+  if (pk) {
+    if (lane < n) q1 = __ldcg(pk + lane);
+    if (32 + lane < n) q2 = __ldcg(pk + 32 + lane);
+  } else if (lane < n) {
+    load_event(lane, b_nx, t_nx);
+  }
   for (uint32_t base = 0; base < n; base += 32) {
-    const int64_t bc = b_nx;
-    const uint32_t tc = t_nx;
+    int64_t bc;
+    uint32_t tc;
     const uint32_t cnt = min(32u, n - base);
-    if (base + 32 + lane < n) load_event(base + 32 + lane, b_nx, t_nx);
+    if (pk) {
+      unpack(q1, bc, tc);
+      q1 = q2;
+      if (base + 64 + lane < n) q2 = __ldcg(pk + base + 64 + lane);
+    } else {
+      bc = b_nx;
+      tc = t_nx;
+      if (base + 32 + lane < n) load_event(base + 32 + lane, b_nx, t_nx);
+    }
     __syncwarp();
     // ---- a2: round-up of this lane's event (PAPER.md:256 (i)) ----
     const bool is_alloc = bc > 0;

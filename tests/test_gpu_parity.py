@@ -109,9 +109,17 @@ def test_config4_full_suite():
     assert (h["status"] == 2).sum() == 0
 
 
-def test_host_entry_point_matches_device_path():
-    b = concat([fuzz.capacity_corpus(100, 400, salt=9), suites.config1()])
+@pytest.mark.parametrize("mode", ["default", "direct", "stream", "copy"])
+def test_host_entry_point_matches_device_path(mode, monkeypatch):
+    """xm_simulate_host with each event-input mode (capi.cu: the events read
+    in place from the page-locked host array by the replaying warps, chunked
+    copies under the replay, one copy first) gives the device path's results,
+    which are oracle-checked."""
+    if mode != "default":
+        monkeypatch.setenv("XM_HOST_INPUT", mode)
+    b = concat([fuzz.capacity_corpus(100, 400, salt=9), suites.config1(), suites.config3()])
     tr = xm.load_traces(b.bytes, b.tag, b.off)
+    assert tr.packed is not None
     cap = b.capacity
     h_host, _ = xm.simulate_host(tr, xm.Config(), capacity=cap)
     h_dev, _ = gpu_run(b)
