@@ -152,6 +152,54 @@ def test_allocated_only_mode_long_traces():
     assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
 
 
+def _stepped_traces():
+    """Traces around multiples of K1t's step (1024 events: 4 warps x 32 lanes x
+    8) up to the trace-per-CTA limit (65536), with first-argmax ties across
+    steps and peaks on step boundaries."""
+    tb = TraceBuilder()
+    rng = np.random.default_rng(21)
+    bid = 0
+    for n in [4095, 4096, 4097, 8191, 8192, 8193, 12289, 20000, 40000, 65536]:
+        live = []
+        for _ in range(n):
+            if live and rng.random() < 0.47:
+                tb.free(live.pop(int(rng.integers(0, len(live)))))
+            else:
+                tb.alloc(bid, int(rng.integers(1, 1 << 21)))
+                live.append(bid)
+                bid += 1
+        tb.end_trace()
+    # the peak reached early and again, exactly, many times later (also at the
+    # last event of a step and the first of the next): the first must win
+    for first in [100, 4095, 4096]:
+        ids = []
+        for i in range(first + 1):
+            tb.alloc(bid, 512)
+            ids.append(bid)
+            bid += 1
+        k = 0
+        while len(ids) > 1 and k < 5000:
+            tb.free(ids.pop())
+            tb.alloc(bid, 512)
+            ids.append(bid)
+            bid += 1
+            k += 1
+        for i in ids:
+            tb.free(i)
+        tb.end_trace()
+    return tb.build()
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_allocated_only_mode_stepped_traces(packed):
+    b = concat([_stepped_traces(), fuzz.spec1_corpus(100, 900, salt=13), suites.config1()])
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    dev = tr.to_device(packed=packed)
+    h, _ = xm.peaks(xm.simulate_batch(dev, xm.Config(mode=1)))
+    o = oracle_run(b)
+    assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
+
+
 def test_determinism():
     b = fuzz.capacity_corpus(200, 500, salt=11)
     h1, _ = gpu_run(b)
