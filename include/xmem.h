@@ -59,6 +59,12 @@ extern "C" {
 #define XM_FULL 0            /* full allocator replay (K2)                     */
 #define XM_RECLAIM_ALL 0
 #define XM_RECLAIM_LARGEST_FIRST 1
+
+/* xm_config.host_input: how xm_simulate_host moves the events (see there) */
+#define XM_HOST_INPUT_AUTO 0      /* direct when the packed array is mapped, else stream */
+#define XM_HOST_INPUT_DIRECT 1
+#define XM_HOST_INPUT_STREAM 2
+#define XM_HOST_INPUT_COPY 3
 #define XM_ALLOCATED_ONLY 1  /* only peak_allocated / _idx via the segmented   */
                              /* prefix-scan/max (K1). Exact only with unlimited */
                              /* capacity, which it requires (else XM_EINVAL).   */
@@ -104,6 +110,8 @@ typedef struct {
                                /* XM_RECLAIM_LARGEST_FIRST (SPEC.md:283 D3: fully  */
                                /* free segments largest first, ties lowest address,*/
                                /* only until the request fits)                     */
+  uint32_t host_input;         /* XM_HOST_INPUT_* (xm_simulate_host only);        */
+                               /* default AUTO                                     */
 } xm_config;
 
 /*
@@ -259,18 +267,19 @@ int xm_peaks(const xm_result* d_res, int64_t n, xm_result* h_out, xm_summary* h_
  * (>= xm_host_ws_bytes(); the metadata always goes there), copies the
  * results to h_out[n_traces] (HOST, caller order) and synchronises `stream`.
  *   capacity: HOST [n_traces] per-trace capacities (caller order) or NULL.
- * Event input in XM_FULL mode (env XM_HOST_INPUT overrides the default):
- *   direct  (default when the packed array is page-locked and device-mapped,
+ * Event input in XM_FULL mode, cfg->host_input (env XM_HOST_INPUT=direct|
+ * stream|copy overrides it, for tooling):
+ *   direct  (AUTO's choice when the packed array is page-locked and mapped,
  *           i.e. the batch was loaded with CUDA available): each replaying
  *           warp loads its trace's 8-byte events IN PLACE from the host array
  *           over PCIe, two 32-event tiles ahead of the replay; nothing is
  *           staged in HBM. The host array must stay alive and unchanged until
  *           the call returns (it does: the call is synchronous).
- *   stream  (the fallback): chunks of whole traces, in stored order, are
+ *   stream  (AUTO's fallback; DIRECT's too when the array is not mapped): chunks of whole traces, in stored order, are
  *           copied into d_ws on a library-owned copy stream while the replay
  *           kernel already runs on `stream`, each trace starting once its
  *           chunk is resident.
- *   copy    (or XM_NO_STREAM=1; always for XM_ALLOCATED_ONLY): everything is
+ *   copy    (also env XM_NO_STREAM=1; always for XM_ALLOCATED_ONLY): everything is
  *           copied before the launch.
  * All three give identical results.
  */

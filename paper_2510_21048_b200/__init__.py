@@ -57,7 +57,7 @@ class _Cfg(ctypes.Structure):
                 ("capacity", ctypes.c_uint64), ("large_split_strict", ctypes.c_uint32),
                 ("mode", ctypes.c_uint32), ("smem_per_warp", ctypes.c_uint32),
                 ("warps_per_cta", ctypes.c_uint32), ("roundup_power2_divisions", ctypes.c_uint32),
-                ("reclaim_policy", ctypes.c_uint32)]
+                ("reclaim_policy", ctypes.c_uint32), ("host_input", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -136,12 +136,13 @@ class Config:
     warps_per_cta: int = 0
     roundup_power2_divisions: int = 0     # NEXT-4 variant: torch knob (0/1 = off)
     reclaim_policy: int = 0               # 0 torch release-all; 1 SPEC.md:283 D3
+    host_input: int = 0                   # xm_simulate_host: 0 auto, 1 direct, 2 stream, 3 copy
 
     def c(self) -> _Cfg:
         return _Cfg(self.min_block, self.small_size, self.small_buffer, self.large_buffer,
                     self.min_large_alloc, self.round_large, self.capacity,
                     self.large_split_strict, self.mode, self.smem_per_warp, self.warps_per_cta,
-                    self.roundup_power2_divisions, self.reclaim_policy)
+                    self.roundup_power2_divisions, self.reclaim_policy, self.host_input)
 
 
 _lib = None

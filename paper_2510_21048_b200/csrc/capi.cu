@@ -55,6 +55,7 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
     return set_error(XM_EINVAL, "xm_config: roundup_power2_divisions must be a power of two <= 64");
   if (c->reclaim_policy != XM_RECLAIM_ALL && c->reclaim_policy != XM_RECLAIM_LARGEST_FIRST)
     return set_error(XM_EINVAL, "xm_config: unknown reclaim_policy");
+  if (c->host_input > XM_HOST_INPUT_COPY) return set_error(XM_EINVAL, "xm_config: unknown host_input");
   int sh = 0;
   while ((1ull << sh) < m) ++sh;
   u->unit_shift = uint32_t(sh);
@@ -296,12 +297,20 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   // array is device-mapped) = the replaying warps load the events in place
   // from host memory over PCIe, nothing staged in HBM; STREAM = chunked copies
   // on a copy stream overlapping the replay; COPY = everything copied first.
-  // XM_HOST_INPUT=direct|stream|copy overrides; XM_NO_STREAM=1 = copy.
-  const char* hin = std::getenv("XM_HOST_INPUT");
-  auto is = [&](const char* m) { return hin && !std::strcmp(hin, m); };
-  const bool want_copy = std::getenv("XM_NO_STREAM") || is("copy");
+  // cfg->host_input chooses; env XM_HOST_INPUT=direct|stream|copy overrides,
+  // XM_NO_STREAM=1 = copy.
+  uint32_t hin = cfg->host_input;
+  if (const char* v = std::getenv("XM_HOST_INPUT")) {
+    if (!std::strcmp(v, "direct")) hin = XM_HOST_INPUT_DIRECT;
+    else if (!std::strcmp(v, "stream")) hin = XM_HOST_INPUT_STREAM;
+    else if (!std::strcmp(v, "copy")) hin = XM_HOST_INPUT_COPY;
+  }
+  if (std::getenv("XM_NO_STREAM")) hin = XM_HOST_INPUT_COPY;
+  if (hin > XM_HOST_INPUT_COPY) return set_error(XM_EINVAL, "xm_config: unknown host_input");
+  const bool want_copy = hin == XM_HOST_INPUT_COPY;
   const uint64_t* h_direct = nullptr;        // device-usable pointer of I.packed
-  if (cfg->mode == XM_FULL && I.packed && I.n_events > 0 && !want_copy && !is("stream")) {
+  if (cfg->mode == XM_FULL && I.packed && I.n_events > 0 &&
+      (hin == XM_HOST_INPUT_AUTO || hin == XM_HOST_INPUT_DIRECT)) {
     void* dp = nullptr;
     if (cudaHostGetDevicePointer(&dp, const_cast<uint64_t*>(I.packed), 0) == cudaSuccess)
       h_direct = static_cast<const uint64_t*>(dp);

@@ -109,21 +109,31 @@ def test_config4_full_suite():
     assert (h["status"] == 2).sum() == 0
 
 
-@pytest.mark.parametrize("mode", ["default", "direct", "stream", "copy"])
+@pytest.mark.parametrize("mode", ["auto", "direct", "stream", "copy", "env-stream", "env-no-stream"])
 def test_host_entry_point_matches_device_path(mode, monkeypatch):
-    """xm_simulate_host with each event-input mode (capi.cu: the events read
-    in place from the page-locked host array by the replaying warps, chunked
-    copies under the replay, one copy first) gives the device path's results,
-    which are oracle-checked."""
-    if mode != "default":
-        monkeypatch.setenv("XM_HOST_INPUT", mode)
+    """xm_simulate_host with each event-input mode (xm_config.host_input, or
+    the env override: the events read in place from the page-locked host array
+    by the replaying warps, chunked copies under the replay, one copy first)
+    gives the device path's results, which are oracle-checked."""
+    cfg = xm.Config(host_input={"direct": 1, "stream": 2, "copy": 3}.get(mode, 0))
+    if mode == "env-stream":
+        monkeypatch.setenv("XM_HOST_INPUT", "stream")
+    if mode == "env-no-stream":
+        monkeypatch.setenv("XM_NO_STREAM", "1")
     b = concat([fuzz.capacity_corpus(100, 400, salt=9), suites.config1(), suites.config3()])
     tr = xm.load_traces(b.bytes, b.tag, b.off)
     assert tr.packed is not None
     cap = b.capacity
-    h_host, _ = xm.simulate_host(tr, xm.Config(), capacity=cap)
+    h_host, _ = xm.simulate_host(tr, cfg, capacity=cap)
     h_dev, _ = gpu_run(b)
     assert (h_host == h_dev).all()
+
+
+def test_host_input_rejects_unknown_mode():
+    b = suites.config1()
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    with pytest.raises(xm.XMemError):
+        xm.simulate_host(tr, xm.Config(host_input=7))
 
 
 def test_allocated_only_mode():
