@@ -18,7 +18,10 @@ curve = torch.zeros((b.n_events, 3), dtype=torch.int64, device="cuda")
 xm.peaks(xm.simulate_batch(dev, curve=curve))                                  # K2 + curve
 xm.peaks(xm.simulate_batch(dev, xm.Config(reclaim_policy=1, roundup_power2_divisions=4)))
 xm.peaks(xm.simulate_batch(dev, xm.Config(smem_per_warp=4096, warps_per_cta=1)))  # wide arena
-xm.simulate_host(tr, xm.Config(), capacity=b.capacity)                         # streamed e2e
+xm.simulate_host(tr, xm.Config(), capacity=b.capacity)                         # e2e, direct input
+xm.simulate_host(tr, xm.Config(host_input=2), capacity=b.capacity)             # e2e, streamed copies
+dev_pk = tr.to_device(capacity=b.capacity, packed=True)
+xm.peaks(xm.simulate_batch(dev_pk))                                            # K2, packed events
 dev1 = tr.to_device()
 xm.peaks(xm.simulate_batch(dev1, xm.Config(mode=1)))                           # K1t
 tb = fuzz.spec1_corpus(1, 1000, salt=5)
