@@ -15,7 +15,10 @@
 //     * matching: a per-warp open-addressing hash table in global memory maps
 //       address -> top of that address's stack of open blocks (linked through
 //       the allocations' event indices); each trace clears and uses the
-//       first 2^ceil(log2 2n) slots of its warp's region. When the tile's addresses are distinct (the common
+//       first 2^ceil(log2 (n+1)) slots of its warp's region. Each allocation
+//       writes one 16-byte record (stack link, dense id | stream, request
+//       bytes), so a matching free reads everything it needs about its
+//       allocation from one sector. When the tile's addresses are distinct (the common
 //       case: __match_any_sync) every lane does its own lookup, insertions are
 //       resolved by a read phase / claim phase loop; instants sharing an
 //       address inside a tile are applied in rounds (round r: every
@@ -25,8 +28,10 @@
 //       its input offset (staging), ids of matched blocks go back on the stack;
 //   k_wire_offsets  one CTA: exclusive scan of the kept counts -> wire offsets;
 //   k_wire_compact  one warp per trace: staging -> dense wire arrays, n_ids.
-// HBM: 17 B/instant read, 5 B written (partner, mismatch) + 12 B staging write
-// and read + 12 B wire write; hash probes and the stack links hit L2.
+// HBM (algorithmic): 17 B/instant read, 5 B written (partner, mismatch) + 12 B
+// staging write and read + 12 B wire write. Measured DRAM traffic is ~5x that
+// (round 1 ncu): the random per-instant sectors (hash probes, records, the
+// partner write of a matched allocation) mostly miss L2.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,6 +51,12 @@ struct Slot {                             // 16 B hash slot
   int top;                                // local index of the top open block, -1 none
 };
 
+struct __align__(16) ARec {                 // what a matching free needs, in one sector
+  int below;                              // the address's previous open allocation (-1)
+  uint32_t tag;                           // dense id | stream << 28
+  long long bytes;                        // the allocation's request bytes
+};
+
 struct LParams {
   const uint64_t* __restrict__ addr;
   const int64_t* __restrict__ bytes;
@@ -56,8 +67,8 @@ struct LParams {
   Slot* tables;                           // [n_slots][1 << hbits]
   uint32_t* idstacks;                     // [n_slots][max_events]
   uint32_t max_events;
-  int* below;                             // [n_events] stack link of an allocation
-  uint32_t* id_of;                        // [n_events] dense id of an allocation
+  ARec* arec;                             // [n_events] per allocation: stack link,
+                                          // dense id | stream << 28, request bytes
   int64_t* st_bytes;                      // [n_events] staging (trace-compacted wire)
   uint32_t* st_tag;
   int32_t* partner;
@@ -109,9 +120,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       const unsigned am = __ballot_sync(kFull, is_alloc);
       const uint32_t na = __popc(am), ka = __popc(am & lt);
       const uint32_t take = min(na, top);
+      uint32_t my_tag = 0;                  // an allocation's dense id | stream << 28
       if (is_alloc) {
         const uint32_t id = ka < take ? ids[top - 1 - ka] : fresh + (ka - take);
-        P.id_of[e0 + li] = id;
+        my_tag = id | (s << 28);
         P.partner[e0 + li] = -1;
         P.mismatch[e0 + li] = 0;
       }
@@ -121,6 +133,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       // ---- matching (LIFO per address) ----
       bool matched = false;
       int blk = -1;
+      uint32_t blk_tag = 0;                 // the matched allocation's record
+      long long blk_bytes = 0;
       // Lanes with the same address form a group; its instants must be
       // applied in time order, different addresses touch different keys. So
       // round r applies every group's r-th instant at once (one round when
@@ -161,11 +175,18 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
         __syncwarp();
         if (act) {
           if (is_alloc) {
-            P.below[e0 + li] = T[h].top;
+            // one 16-byte store / load per record
+            const unsigned long long ub = static_cast<unsigned long long>(b);
+            reinterpret_cast<int4*>(P.arec)[e0 + li] =
+                make_int4(T[h].top, int(my_tag), int(uint32_t(ub)), int(uint32_t(ub >> 32)));
             T[h].top = li;
           } else if (found && T[h].top >= 0) {
             blk = T[h].top;
-            T[h].top = P.below[e0 + blk];
+            const int4 r = reinterpret_cast<const int4*>(P.arec)[e0 + blk];
+            T[h].top = r.x;
+            blk_tag = uint32_t(r.y);
+            blk_bytes = static_cast<long long>((static_cast<unsigned long long>(uint32_t(r.w)) << 32) |
+                                               uint32_t(r.z));
             matched = true;
           }
         }
@@ -178,7 +199,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
         P.partner[e0 + li] = matched ? blk : -1;
         if (matched) {
           P.partner[e0 + blk] = li;
-          mism = P.bytes[e0 + blk] != -b;
+          mism = blk_bytes != -b;
         }
         P.mismatch[e0 + li] = mism ? 1 : 0;
       } else if (valid && b == 0) {
@@ -188,7 +209,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       __syncwarp();
       // ---- matched blocks' ids go back on the stack ----
       const unsigned mm = __ballot_sync(kFull, matched);
-      if (matched) ids[top + __popc(mm & lt)] = P.id_of[e0 + blk];
+      if (matched) ids[top + __popc(mm & lt)] = blk_tag & 0x0FFFFFFFu;
       top += __popc(mm);
       // ---- staging: kept events, compacted within the trace ----
       const bool kept = is_alloc || matched;
@@ -197,11 +218,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
         const int64_t dst = e0 + int64_t(n_kept) + __popc(km & lt);
         if (is_alloc) {
           P.st_bytes[dst] = b;
-          P.st_tag[dst] = P.id_of[e0 + li] | (s << 28);
+          P.st_tag[dst] = my_tag;
         } else {
-          const uint32_t sb = P.stream ? P.stream[e0 + blk] : 0u;
-          P.st_bytes[dst] = -P.bytes[e0 + blk];          // the block's size
-          P.st_tag[dst] = P.id_of[e0 + blk] | (sb << 28);
+          P.st_bytes[dst] = -blk_bytes;                  // the block's size
+          P.st_tag[dst] = blk_tag;                       // its id and stream
         }
       }
       // ---- open count (max open = the minimal id space) ----
@@ -284,7 +304,7 @@ __global__ void k_wire_compact(const int64_t* __restrict__ off, const int64_t* _
 
 struct Layout {
   uint32_t hbits, n_slots, ctas;
-  size_t tables, stacks, below, id_of, st_bytes, st_tag, total;
+  size_t tables, stacks, arec, st_bytes, st_tag, total;
 };
 
 Layout layout(const xm_instants* in) {
@@ -309,8 +329,7 @@ Layout layout(const xm_instants* in) {
   L.tables = o; o += al((size_t(L.n_slots) << hb) * sizeof(Slot));
   L.stacks = o; o += al(size_t(L.n_slots) * (in->max_events ? in->max_events : 1) * 4);
   const size_t E = size_t(in->n_events > 0 ? in->n_events : 1);
-  L.below = o; o += al(E * 4);
-  L.id_of = o; o += al(E * 4);
+  L.arec = o; o += al(E * sizeof(ARec));
   L.st_bytes = o; o += al(E * 8);
   L.st_tag = o; o += al(E * 4);
   L.total = o;
@@ -356,8 +375,7 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   P.tables = reinterpret_cast<Slot*>(base + L.tables);
   P.idstacks = reinterpret_cast<uint32_t*>(base + L.stacks);
   P.max_events = in->max_events ? in->max_events : 1;
-  P.below = reinterpret_cast<int*>(base + L.below);
-  P.id_of = reinterpret_cast<uint32_t*>(base + L.id_of);
+  P.arec = reinterpret_cast<ARec*>(base + L.arec);
   P.st_bytes = reinterpret_cast<int64_t*>(base + L.st_bytes);
   P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
   P.partner = d_partner;
