@@ -443,14 +443,18 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
       }
       const long long wsum = __shfl_sync(kFull, ex, 31);
       ex -= run;
-      long long c = lmx == kNeg ? kNeg : ex + lmx;
-      int ca = larg;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {          // first argmax of the warp
-        const long long m2 = __shfl_xor_sync(kFull, c, o);
-        const int a2 = __shfl_xor_sync(kFull, ca, o);
-        if (m2 > c || (m2 == c && a2 < ca && m2 != kNeg)) { c = m2; ca = a2; }
-      }
+      // first argmax of the warp: lanes hold increasing index ranges, so it
+      // is the lowest lane with the maximum; the maximum by two 32-bit
+      // reductions of the order-preserving unsigned image (kNeg -> 0)
+      const unsigned long long ukey =
+          static_cast<unsigned long long>(lmx == kNeg ? kNeg : ex + lmx) ^ 0x8000000000000000ull;
+      const unsigned khi = unsigned(ukey >> 32), klo = unsigned(ukey);
+      const unsigned mh = __reduce_max_sync(kFull, khi);
+      const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
+      const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
+      const int ca = __shfl_sync(kFull, larg, src);
+      const long long c =
+          static_cast<long long>(((static_cast<unsigned long long>(mh) << 32) | ml) ^ 0x8000000000000000ull);
       if (lane == 0) { s_sum[w] = wsum; s_mx[w] = c; s_arg[w] = ca; }
       __syncthreads();
       if (w == 0) {                           // fold the warp pieces in order
@@ -464,16 +468,16 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
           if (lane >= o) pe += y;
         }
         pe -= ps;
-        long long cc = pm == kNeg ? kNeg : carry + pe + pm;
-        int cca = pa;
-#pragma unroll
-        for (int o = kTWarps / 2; o; o >>= 1) {
-          const long long m2 = __shfl_xor_sync(kFull, cc, o);
-          const int a2 = __shfl_xor_sync(kFull, cca, o);
-          if (m2 > cc || (m2 == cc && a2 < cca && m2 != kNeg)) { cc = m2; cca = a2; }
-        }
-        cc = __shfl_sync(kFull, cc, 0);
-        cca = __shfl_sync(kFull, cca, 0);
+        // first argmax over the warp pieces (lowest lane among ties), as above
+        const unsigned long long uk =
+            static_cast<unsigned long long>(pm == kNeg ? kNeg : carry + pe + pm) ^ 0x8000000000000000ull;
+        const unsigned fhi = unsigned(uk >> 32), flo = unsigned(uk);
+        const unsigned fmh = __reduce_max_sync(kFull, fhi);
+        const unsigned fml = __reduce_max_sync(kFull, fhi == fmh ? flo : 0u);
+        const int fsrc = __ffs(__ballot_sync(kFull, fhi == fmh && flo == fml)) - 1;
+        const int cca = __shfl_sync(kFull, pa, fsrc);
+        const long long cc =
+            static_cast<long long>(((static_cast<unsigned long long>(fmh) << 32) | fml) ^ 0x8000000000000000ull);
         if (cc != kNeg && cc > best) { best = cc; barg = cca; }
         carry += __shfl_sync(kFull, pe + ps, kTWarps - 1);
       }
