@@ -253,11 +253,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_orchestrate(OParams P)
     // ---- 5. outputs: sequence, dense ids, staged wire events ----
     unsigned long long* seq = P.seq + 2 * b0;
     for (uint32_t i = tid; i < nk; i += kThreads) seq[i] = keys[i];
+    __syncthreads();                                    // warp 0 rewrites keys[] below
+    int64_t* ob = P.st_bytes + 2 * b0;
+    uint32_t* ot = P.st_tag + 2 * b0;
     if (warp == 0) {
       const unsigned lt = (1u << lane) - 1u;
       uint32_t top = 0, fresh = 0;
-      int64_t* ob = P.st_bytes + 2 * b0;
-      uint32_t* ot = P.st_tag + 2 * b0;
+      // the serial part only assigns the dense ids (kept in the high half of
+      // each key); the block sizes and streams are gathered by the whole CTA
+      // afterwards, off the serial chain
       for (uint32_t base = 0; base < nk; base += 32) {
         const uint32_t j = base + lane;
         const bool v = j < nk;
@@ -279,11 +283,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_orchestrate(OParams P)
         const unsigned fm = __ballot_sync(kFull, fr);
         if (fr) ids[top + __popc(fm & lt)] = id;
         top += __popc(fm);
-        if (v) {
-          const uint32_t st = P.stream ? P.stream[b0 + blk] : 0u;
-          ob[j] = al ? S[blk] : -S[blk];
-          ot[j] = id | (st << 28);
-        }
+        if (v) keys[j] = (static_cast<unsigned long long>(id) << 32) | (key & 0xFFFFFFFFull);
         __syncwarp();
       }
       if (lane == 0) {
@@ -295,6 +295,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_orchestrate(OParams P)
         for (int c = 0; c < 6; ++c) R.n_class[c] = s_ncls[c];
         P.rec[t] = R;
       }
+    }
+    __syncthreads();
+    // staged wire events: (size, dense id | stream << 28) of each sequence entry
+    for (uint32_t j = tid; j < nk; j += kThreads) {
+      const unsigned long long key = keys[j];
+      const uint32_t blk = uint32_t(key & 0x7FFFFFFFu);
+      const bool al = (key >> 31) & 1ull;
+      const uint32_t st = P.stream ? P.stream[b0 + blk] : 0u;
+      ob[j] = al ? S[blk] : -S[blk];
+      ot[j] = uint32_t(key >> 32) | (st << 28);
     }
     __syncthreads();
   }
