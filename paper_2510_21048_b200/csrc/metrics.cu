@@ -6,9 +6,11 @@
 //   k_metrics_map  one thread per run: C1, C2, M_save, the selected relative
 //                  error (as its IEEE-754 bit pattern: errors are >= 0, so the
 //                  bits order like the values); CTA-reduced sums -> atomics.
-//   k_select       one CTA: radix select (8 passes of 8 bits, shared-memory
-//                  histograms) of the k-th and (k+1)-th smallest error keys
-//                  -> the median (mean of the central pair for even counts).
+//   k_select_hist  grid-wide: histogram of the next 8-bit digit of the error
+//   k_select_pick  keys matching the digits chosen so far; one warp picks the
+//                  digit holding each wanted rank (8 passes) -> the k-th and
+//                  (k+1)-th smallest keys -> the median (mean of the central
+//                  pair for even counts) and the finished record.
 // HBM: 40 B/run read, 8 B/run written + 8 passes x 8 B/run re-read (L2).
 #include <cuda_runtime.h>
 
@@ -20,7 +22,8 @@
 namespace {
 
 constexpr int kMapThreads = 256;
-constexpr int kSelThreads = 1024;
+constexpr int kHistThreads = 512;
+constexpr size_t kHdr = 4096;          // Acc, SelState, result record; keys follow
 
 static_assert(sizeof(xm_metrics) <= 128, "scratch layout");
 
@@ -80,45 +83,58 @@ __global__ void __launch_bounds__(kMapThreads) k_metrics_map(const xm_run* __res
 }
 
 // The two central order statistics of the selected keys by 8-bit MSD radix
-// select (8 passes), then the finished metrics record (thread 0).
-__global__ void __launch_bounds__(kSelThreads) k_select(const uint64_t* __restrict__ keys, int64_t n,
-                                                        const Acc* acc, uint64_t* out,
-                                                        xm_metrics* res) {
-  __shared__ unsigned int hist[256];
-  __shared__ uint64_t s_prefix;
-  __shared__ unsigned long long s_rank;
-  const unsigned long long m = acc->n_sel;
-  for (int j = 0; j < 2 && m > 0; ++j) {
-    unsigned long long rank = (m - 1) / 2 + (j == 1 && (m % 2 == 0) ? 1 : 0);
-    uint64_t prefix = 0, mask = 0;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
-      __syncthreads();
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint64_t k = keys[i];
-        if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 0xFF], 1u);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long acc_c = 0;
-        int d = 0;
-        for (; d < 256; ++d) {
-          if (acc_c + hist[d] > rank) break;
-          acc_c += hist[d];
-        }
-        s_prefix = prefix | (uint64_t(d) << shift);
-        s_rank = rank - acc_c;
-      }
-      __syncthreads();
-      prefix = s_prefix;
-      rank = s_rank;
-      mask |= 0xFFull << shift;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[j] = prefix;
-    __syncthreads();
+// select, 8 passes; each pass is a grid-wide histogram of the next digit over
+// the keys that match the digits chosen so far (per-CTA shared-memory
+// histograms merged with one atomic per bin), then one small kernel picks the
+// digit that holds each wanted rank. Both order statistics (the k-th and
+// (k+1)-th smallest, for the median of an even count) are selected at once.
+struct SelState {                 // scratch, zeroed per call
+  uint64_t prefix[2];             // digits chosen so far (the selected keys' high bits)
+  uint64_t mask;                  // the bits chosen so far
+  unsigned long long rank[2];     // rank still to skip inside the current prefix
+  unsigned int hist[2][256];
+};
+
+__global__ void __launch_bounds__(kHistThreads) k_select_hist(const uint64_t* __restrict__ keys,
+                                                              int64_t n, int shift, SelState* S) {
+  __shared__ unsigned int h[2][256];
+  for (int b = threadIdx.x; b < 512; b += blockDim.x) (&h[0][0])[b] = 0;
+  __syncthreads();
+  const uint64_t mask = S->mask, p0 = S->prefix[0], p1 = S->prefix[1];
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = __ldg(keys + i);
+    const unsigned d = unsigned(k >> shift) & 0xFFu;
+    if ((k & mask) == p0) atomicAdd(&h[0][d], 1u);
+    if ((k & mask) == p1) atomicAdd(&h[1][d], 1u);
   }
-  if (threadIdx.x == 0) {
+  __syncthreads();
+  for (int b = threadIdx.x; b < 512; b += blockDim.x) {
+    const unsigned v = (&h[0][0])[b];
+    if (v) atomicAdd(&(&S->hist[0][0])[b], v);
+  }
+}
+
+// one warp: lane j < 2 picks the digit holding rank[j]; the histograms are
+// cleared for the next pass; after the last pass, the metrics record
+__global__ void k_select_pick(int shift, SelState* S, const Acc* acc, int64_t n, xm_metrics* res) {
+  const unsigned long long m = acc->n_sel;
+  const int j = threadIdx.x;
+  if (j < 2 && m > 0) {
+    unsigned long long rank = shift == 56 ? (m - 1) / 2 + (j == 1 && (m % 2 == 0) ? 1 : 0) : S->rank[j];
+    unsigned long long c = 0;
+    int d = 0;
+    for (; d < 255; ++d) {
+      if (c + S->hist[j][d] > rank) break;
+      c += S->hist[j][d];
+    }
+    S->prefix[j] |= uint64_t(d) << shift;
+    S->rank[j] = rank - c;
+  }
+  __syncwarp();
+  for (int b = threadIdx.x; b < 512; b += blockDim.x) (&S->hist[0][0])[b] = 0;
+  if (j == 0) S->mask |= 0xFFull << shift;
+  if (shift == 0 && j == 0) {
     const double nn = double(n);
     xm_metrics r;
     r.n = uint64_t(n);
@@ -126,8 +142,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const uint64_t* __restri
     r.sum_c1 = acc->c1;
     r.sum_c2 = acc->c2;
     r.sum_save = (long long)acc->save;
-    const double a = __longlong_as_double((long long)out[0]);
-    const double b = __longlong_as_double((long long)out[1]);
+    const double a = __longlong_as_double((long long)S->prefix[0]);
+    const double b = __longlong_as_double((long long)S->prefix[1]);
     r.mre = m == 0 ? __longlong_as_double(0x7FF8000000000000ll) : ((m % 2) ? a : (a + b) / 2.0);
     r.pef1 = double(uint64_t(n) - acc->c1) / nn;               // Eq. failed-estimation-probability
     r.pef2 = double(uint64_t(n) - acc->c2) / nn;
@@ -141,7 +157,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const uint64_t* __restri
 using namespace xm_internal;
 
 extern "C" size_t xm_metrics_scratch_bytes(int64_t n_runs) {
-  return 256 + size_t(n_runs > 0 ? n_runs : 0) * 8;
+  return kHdr + size_t(n_runs > 0 ? n_runs : 0) * 8;
 }
 
 extern "C" int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch,
@@ -154,10 +170,13 @@ extern "C" int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch
   if (scratch_bytes < xm_metrics_scratch_bytes(n)) return set_error(XM_ENOMEM, "scratch too small");
   if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  Acc* acc = static_cast<Acc*>(d_scratch);
-  uint64_t* sel = reinterpret_cast<uint64_t*>(static_cast<char*>(d_scratch) + 64);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(static_cast<char*>(d_scratch) + 256);
-  cudaError_t e = cudaMemsetAsync(d_scratch, 0, 256, st);
+  char* base = static_cast<char*>(d_scratch);
+  Acc* acc = reinterpret_cast<Acc*>(base);
+  xm_metrics* d_res = reinterpret_cast<xm_metrics*>(base + 128);
+  SelState* sel = reinterpret_cast<SelState*>(base + 256);
+  static_assert(256 + sizeof(SelState) <= kHdr, "metrics scratch header");
+  uint64_t* keys = reinterpret_cast<uint64_t*>(base + kHdr);
+  cudaError_t e = cudaMemsetAsync(d_scratch, 0, kHdr, st);
   if (e != cudaSuccess) return set_error(XM_ECUDA, cudaGetErrorString(e));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -165,9 +184,13 @@ extern "C" int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch
   const int64_t want = (n + kMapThreads - 1) / kMapThreads;
   const int grid = int(want < int64_t(sms) * 8 ? want : int64_t(sms) * 8);
   k_metrics_map<<<grid, kMapThreads, 0, st>>>(d_runs, n, keys, acc);
-  xm_metrics* d_res = reinterpret_cast<xm_metrics*>(static_cast<char*>(d_scratch) + 128);
-  k_select<<<1, kSelThreads, 0, st>>>(keys, n, acc, sel, d_res);
-  launch_counter() = 2;
+  const int64_t hwant = (n + kHistThreads * 4 - 1) / (kHistThreads * 4);
+  const int hgrid = int(hwant < int64_t(sms) * 2 ? (hwant > 0 ? hwant : 1) : int64_t(sms) * 2);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k_select_hist<<<hgrid, kHistThreads, 0, st>>>(keys, n, shift, sel);
+    k_select_pick<<<1, 32, 0, st>>>(shift, sel, acc, n, d_res);
+  }
+  launch_counter() = 1 + 2 * 8;
   Acc h{};
   if ((e = cudaMemcpyAsync(&h, acc, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(h_out, d_res, sizeof(*h_out), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
