@@ -129,6 +129,23 @@ def test_host_entry_point_matches_device_path(mode, monkeypatch):
     assert (h_host == h_dev).all()
 
 
+def test_host_entry_point_without_packed_form():
+    """An id space of 2^18 or more has no packed form: xm_simulate_host falls
+    back to streaming the 12-byte events (bytes + tag), oracle-checked."""
+    tb = TraceBuilder()
+    n = (1 << 18) + 40
+    for i in range(n):
+        tb.alloc(i, 512 * (1 + i % 7))
+    for i in range(n):
+        tb.free(i)
+    tb.end_trace()
+    b = concat([tb.build(), suites.config1()])
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    assert tr.packed is None
+    h_host, _ = xm.simulate_host(tr, xm.Config())
+    assert_parity(b, h_host, oracle_run(b))
+
+
 def test_host_input_rejects_unknown_mode():
     b = suites.config1()
     tr = xm.load_traces(b.bytes, b.tag, b.off)
