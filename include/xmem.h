@@ -380,7 +380,8 @@ int xm_metrics_batch(const xm_run* d_runs, int64_t n, void* d_scratch, size_t sc
 typedef struct {
   const uint64_t* addr;     /* [n_events] DEVICE: the instant's address                   */
   const int64_t* bytes;     /* [n_events] DEVICE: +size allocation, -size deallocation;    */
-                            /* 0 is invalid (counted in n_invalid, otherwise ignored)      */
+                            /* 0 or |bytes| >= XM_MAX_REQUEST is invalid (counted in     */
+                            /* n_invalid, otherwise ignored: never reaches the replay)    */
   const uint8_t* stream;    /* [n_events] DEVICE stream (0..15) or NULL (all 0)            */
   const int64_t* off;       /* [n_traces+1] DEVICE: trace t = instants [off[t], off[t+1])  */
   int64_t n_traces, n_events;
@@ -393,7 +394,7 @@ typedef struct {            /* per trace, 56 bytes                              
   uint64_t n_mismatch;      /* matched frees whose |bytes| differs from the block's size   */
   uint64_t n_persistent;    /* blocks never closed                                         */
   uint64_t n_kept;          /* allocations + matched frees = replay events of the trace    */
-  uint64_t n_invalid;       /* zero-byte instants                                          */
+  uint64_t n_invalid;       /* zero-byte or out-of-range (>= XM_MAX_REQUEST) instants       */
   uint32_t max_open;        /* most blocks open at once                                    */
   uint32_t n_ids;           /* dense id space of the wire trace (<= max_open + 31); the    */
                             /* replay needs <= 2^27 (xm_batch tag bits 0-26)               */
@@ -469,7 +470,7 @@ int xm_blocks_from_instants(const xm_instants* in, const int64_t* d_ts, const in
 #define XM_O_OK 0
 #define XM_O_FEW_ITERATIONS 1   /* fewer iterations than analysis_iter + 1      */
 #define XM_O_TS_RANGE 2         /* a re-timed timestamp >= 2^32 us after Ws, or */
-                                /* a block size outside (0, 2^41)              */
+                                /* a block size outside (0, XM_MAX_REQUEST)    */
 typedef struct {
   const int64_t* alloc_ts;  /* [n_blocks] DEVICE, allocation time (us)                  */
   const int64_t* free_ts;   /* [n_blocks] DEVICE, deallocation time, -1 = none observed */

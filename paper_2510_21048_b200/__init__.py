@@ -34,6 +34,7 @@ __all__ = ["Config", "Traces", "DeviceBatch", "load_traces", "simulate_batch", "
 UNLIMITED = 0xFFFFFFFFFFFFFFFF
 XM_FULL, XM_ALLOCATED_ONLY = 0, 1
 STATUS = {0: "ok", 1: "oom", 2: "overflow"}
+XM_O_OK, XM_O_FEW_ITERATIONS, XM_O_TS_RANGE = 0, 1, 2      # xm_orchestrated.status
 
 # numpy view of xm_result (64 B, include/xmem.h)
 RESULT_DTYPE = np.dtype([
@@ -693,6 +694,15 @@ def estimate(ins: DeviceInstants, ts, win: np.ndarray, woff: np.ndarray, analysi
     prof.win = torch.from_numpy(np.ascontiguousarray(win, np.int64).reshape(-1)).to(dev)
     prof.woff = torch.from_numpy(np.ascontiguousarray(woff, np.int64)).to(dev)
     cls, seq, orec, wb = orchestrate(prof, analysis_iter, stream=stream)
+    bad = np.flatnonzero(orec["status"] != XM_O_OK) if len(orec) else np.zeros(0, np.int64)
+    if len(bad):
+        # SPEC.md:300-304 (insufficient iterations is an error) and the
+        # orchestrator's range checks: such a trace has no valid re-timed
+        # sequence, so it must not be replayed as if it were empty
+        t = int(bad[0])
+        raise XMemError(f"estimate: {len(bad)} trace(s) not orchestrated; first trace {t} "
+                        f"status {int(orec['status'][t])} "
+                        f"({'fewer than analysis_iter + 1 iterations' if orec['status'][t] == XM_O_FEW_ITERATIONS else 'timestamp or size out of range'})")
     if capacity is not None:
         wb.capacity = torch.from_numpy(np.ascontiguousarray(capacity, np.uint64).view(np.int64)).to(dev)
     cv = None

@@ -48,6 +48,11 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
       return set_error(XM_EINVAL, "xm_config: sizes must be non-zero multiples of min_block");
   if (c->small_buffer < c->small_size || c->large_buffer <= c->small_size)
     return set_error(XM_EINVAL, "xm_config: segment sizes must cover the small threshold");
+  // SPEC.md:211-213 / torch's constants: small_size < min_large_alloc <=
+  // large_buffer, so a request between them fits its large_buffer segment
+  // (otherwise the remainder bsize - s underflows) and narrow keys never saturate
+  if (c->min_large_alloc <= c->small_size || c->min_large_alloc > c->large_buffer)
+    return set_error(XM_EINVAL, "xm_config: need small_size < min_large_alloc <= large_buffer");
   if (c->mode != XM_FULL && c->mode != XM_ALLOCATED_ONLY)
     return set_error(XM_EINVAL, "xm_config: unknown mode");
   const uint32_t dv = c->roundup_power2_divisions;
@@ -117,10 +122,10 @@ static int simulate(const xm_batch* b, const xm_config* cfg, void* d_scratch, si
                     xm_result* d_out, void* stream, const uint32_t* ready) {
   launch_counter() = 0;
   if (!cfg) return set_error(XM_EINVAL, "null config");
-  int rc = check_batch(b);
-  if (rc) return rc;
   UnitConfig u;
-  if ((rc = make_unit_config(cfg, &u))) return rc;
+  int rc = make_unit_config(cfg, &u);
+  if (rc) return rc;
+  if ((rc = check_batch(b))) return rc;
   if (b->n_traces == 0) return XM_OK;
   if (!d_out || !d_scratch) return set_error(XM_EINVAL, "null output or scratch");
   if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");

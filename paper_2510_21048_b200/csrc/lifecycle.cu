@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       const int li = base + int(lane);
       const bool valid = li < n;
       const uint64_t a = valid ? P.addr[e0 + li] : ~0ull - lane;
-      const int64_t b = valid ? P.bytes[e0 + li] : 0;
+      int64_t b = valid ? P.bytes[e0 + li] : 0;
+      // |bytes| >= XM_MAX_REQUEST is out of the replay's range: invalid like 0
+      if (b >= int64_t(XM_MAX_REQUEST) || b <= -int64_t(XM_MAX_REQUEST)) b = 0;
       const uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
       const bool is_alloc = b > 0, is_free = b < 0;
       // ---- dense ids for this tile's allocations (ids freed before the tile) ----

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_orchestrate(OParams P)
     // ---- 1. parameters and optimizer-step candidates ----
     for (int i = tid; i < n; i += kThreads) {
       const int64_t a = A[i];
-      if (S[i] <= 0 || (uint64_t(S[i]) >> 41)) atomicExch(&s_bad, 1u);   // sizes in (0, 2^41)
+      if (S[i] <= 0 || uint64_t(S[i]) >= XM_MAX_REQUEST) atomicExch(&s_bad, 1u);   // sizes in (0, 2^40): the replay's bound
       if (F[i] == -1 && a < first) {
         psize[atomicAdd(&s_npar, 1u)] = S[i];
       } else {

@@ -50,6 +50,9 @@
 #ifndef XM_F_INIT_DIV
 #define XM_F_INIT_DIV 4         // initial free-list capacity: n_ids / 4 + 64 entries
 #endif
+#ifndef XM_ARENA_BUDGET
+#define XM_ARENA_BUDGET (4ull << 30)   // bytes of global arena slots (overflow path), see plan_replay
+#endif
 #ifndef XM_HEAP_RESERVE_DIV
 #define XM_HEAP_RESERVE_DIV 24  // admission keeps 1/24 of the heap for free-list growth (tuned)
 #endif
@@ -76,6 +79,7 @@ constexpr uint32_t kAllocBit = 0x08000000u;
 constexpr uint32_t kKeyBits = 27;
 constexpr uint32_t kKeyMax = (1u << kKeyBits) - 1u;
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr size_t kArenaBudget = XM_ARENA_BUDGET;
 constexpr int kStatusOk = XM_T_OK, kStatusOom = XM_T_OOM, kStatusOverflow = XM_T_OVERFLOW;
 
 // shared-memory heap geometry
@@ -1196,9 +1200,15 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   p.arena_ids = b->max_ids;
   p.arena_free = b->max_events + 1;
   p.arena_per_warp = (align16(a_bytes<Wide>(p.arena_ids)) + f_bytes<Wide>(p.arena_free) + 255) & ~size_t(255);
+  // Slots: at most one per warp and 64, and within a byte budget
+  // (XM_ARENA_BUDGET, default 4 GiB): every slot is sized for the batch's
+  // longest trace, so one very long trace must not make the scratch
+  // unallocatable. Fewer slots only serialise overflowing traces
+  // (arena_claim waits for a free one); at least one always exists.
   const int64_t tw = int64_t(p.ctas) * p.warps_per_cta;
-  const uint32_t n_arena = uint32_t(std::min<int64_t>(std::min<int64_t>(tw, 64),
-                                                      std::max<int64_t>(1, b->n_traces)));
+  const int64_t by_budget = std::max<int64_t>(1, int64_t(kArenaBudget / p.arena_per_warp));
+  const uint32_t n_arena = uint32_t(std::min<int64_t>(
+      std::min<int64_t>(std::min<int64_t>(tw, 64), by_budget), std::max<int64_t>(1, b->n_traces)));
   p.n_arena = n_arena;
   p.scratch_bytes = 256 + size_t(n_arena) * p.arena_per_warp;
 #ifdef XM_TIMING

@@ -202,3 +202,32 @@ def test_widened_entry_points_fail_loudly_without_gpu():
     assert L.xm_orchestrate(ctypes.byref(prof), 1, None, 0, None, None, None, None) != 0
     m = xm._Metrics()
     assert L.xm_metrics_batch(None, 1, None, 0, ctypes.byref(m), None) != 0
+
+
+@pytest.mark.parametrize("field,value", [("min_large_alloc", 1 << 20),      # == small_size
+                                         ("min_large_alloc", 22 << 20),     # > large_buffer
+                                         ("large_buffer", 8 << 20)])        # < min_large_alloc
+def test_config_rejects_inconsistent_thresholds(field, value):
+    """small_size < min_large_alloc <= large_buffer (SPEC.md:211-213, torch's
+    constants): otherwise a request between them would get a segment smaller
+    than itself. Checked before any device work, so testable on CPU."""
+    c = hand.h1(512, 3)
+    tr = xm.load_traces(c.bytes, c.tag, c.off)
+    b = xm._Batch(None, None, None, None, None, None, tr.n_traces, tr.n_events, tr.max_ids,
+                  tr.max_events)
+    cfg = xm.Config()
+    setattr(cfg, field, value)
+    cc = cfg.c()
+    rc = xm.lib().xm_simulate_batch(ctypes.byref(b), ctypes.byref(cc), None, 0, None, None)
+    assert rc == -1, rc                                          # XM_EINVAL
+    assert b"min_large_alloc" in xm.lib().xm_last_error()
+
+
+def test_arena_scratch_is_bounded_for_one_huge_trace():
+    """every overflow arena slot is sized for the longest trace, so
+    the slot count is capped by a byte budget (4 GiB) instead of one per warp."""
+    b = xm._Batch(None, None, None, None, None, None, 5000, 60_000_000, 2_000_000, 50_000_000)
+    cc = xm.Config().c()
+    n = xm.lib().xm_scratch_bytes(ctypes.byref(b), ctypes.byref(cc))
+    per_slot = 50_000_001 * 24 + 2_000_000 * 20
+    assert per_slot <= n <= max(4 << 30, per_slot) + (1 << 20)

@@ -122,3 +122,20 @@ def test_reconstruct_config4_shaped():
     ins = instants.from_batch(b.subset(idx), salt=4, p_orphan=0.001, p_mismatch=0.001,
                               p_lost=0.002)
     _check(ins)
+
+
+def test_out_of_range_instants_are_invalid():
+    """an instant with |bytes| >= 2^40 (XM_MAX_REQUEST, the replay's
+    bound) is counted in n_invalid and ignored like a zero-byte one, so it can
+    never reach k_replay's 32-bit unit arithmetic."""
+    A = np.uint64
+    big = 1 << 40
+    ins = instants.Instants(np.array([5, 6, 6, 5], A), np.array([4096, big, -big, -4096], np.int64),
+                            np.zeros(4, np.uint8), np.array([0, 4], np.int64))
+    d = xm.DeviceInstants.from_host(ins.addr, ins.bytes, ins.stream, ins.off)
+    partner, mism, rec, wb = xm.reconstruct(d)
+    assert int(rec["n_invalid"][0]) == 2 and int(rec["n_blocks"][0]) == 1
+    assert int(rec["n_kept"][0]) == 2 and int(rec["n_orphan"][0]) == 0
+    p = partner.cpu().numpy()
+    assert p[0] == 3 and p[3] == 0 and p[1] == -1 and p[2] == -1
+    assert wb.bytes[:wb.n_events].cpu().numpy().tolist() == [4096, -4096]

@@ -95,3 +95,15 @@ def test_estimate_curve_matches_oracle_curve():
         r, oc = oracle.simulate_trace(wbb, wtt, curve=True)
         q = pos[t]
         assert (cv[woff[q]:woff[q + 1]] == oc).all(), t
+
+
+def test_estimate_rejects_traces_without_enough_iterations():
+    """a trace with fewer than analysis_iter + 1 iterations has no
+    analysis window (an error). estimate() raises instead of
+    replaying the empty sequence K6 leaves for it as a 0-byte peak."""
+    p = C.batch(CELLS[:2])
+    ts, ad, by, st, off = C.to_instants(p)
+    d = xm.DeviceInstants.from_host(ad, by, st, off)
+    n_iter = int(np.diff(p.woff).min())
+    with pytest.raises(xm.XMemError, match="fewer than analysis_iter"):
+        xm.estimate(d, torch.from_numpy(ts).cuda(), p.win, p.woff, analysis_iter=n_iter)

@@ -11,7 +11,10 @@ cap = b.capacity if (b.capacity != xm.UNLIMITED).any() else None
 cfg = xm.Config()
 ws = None
 ref = None
-for m in (sys.argv[1:] or os.environ.get("XM_E2E_MODES", "hybrid").split()):
+MODES = ("direct", "stream", "copy")    # xm_simulate_host event inputs (capi.cu)
+for m in (sys.argv[1:] or os.environ.get("XM_E2E_MODES", "direct stream copy").split()):
+    if m not in MODES:
+        raise SystemExit(f"unknown host-input mode {m!r}; one of {MODES}")
     os.environ["XM_HOST_INPUT"] = m
     for _ in range(3):
         h, ws = xm.simulate_host(tr, cfg, capacity=cap, workspace=ws)
@@ -21,6 +24,5 @@ for m in (sys.argv[1:] or os.environ.get("XM_E2E_MODES", "hybrid").split()):
         t0 = time.perf_counter()
         h, ws = xm.simulate_host(tr, cfg, capacity=cap, workspace=ws)
         ts.append(time.perf_counter() - t0)
-    print(f"{m:7s} direct_traces={os.environ.get('XM_DIRECT_TRACES', 'auto'):5s} "
-          f"median {np.median(ts) * 1e3:.3f} ms  min {min(ts) * 1e3:.3f} ms  same={(h == ref).all()}",
+    print(f"{m:7s} median {np.median(ts) * 1e3:.3f} ms  min {min(ts) * 1e3:.3f} ms  same={(h == ref).all()}",
           flush=True)
