@@ -168,19 +168,30 @@ def ncu_issue(kernel="k_replay"):
 
 
 # ---------------------------------------------------------------- cpu oracle
-def oracle_rate(batch, cores=None, passes=1):
-    """The oracle as it stands (oracle/xmo.c), traces spread over host processes."""
-    import oracle
-    cores = cores or len(os.sched_getaffinity(0))
-    best = None
-    res = None
-    for _ in range(passes):
-        t0 = time.perf_counter()
-        res = oracle.simulate_batch_parallel(batch, workers=cores)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
+def _oracle_pool():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_pool
+    return oracle_pool
+
+
+def oracle_rate(batch, passes=1):
+    """The oracle as it stands (oracle/xmo.c) on every host core: forked workers
+    inherit the batch (nothing pickled but chunk numbers) and time only the
+    simulate call; the rate divides by the busiest worker's simulate time
+    (SURVEY.md §8(d) "timing only simulate"). Returns (rate, detail, results)."""
+    op = _oracle_pool()
+    with op.Pool(batch) as pool:
+        best = None
+        for _ in range(passes):
+            res, wall, busiest, total = pool.run()
+            if best is None or busiest < best[1]:
+                best = (wall, busiest, total)
+        cores = pool.workers
+    wall, busiest, total = best
     ev = int(res["events_done"].sum())
-    return ev / best, best, cores, res, ev
+    return ev / busiest, {"cores": cores, "wall_s": wall, "busiest_worker_simulate_s": busiest,
+                          "simulate_s_all_workers": total, "events": ev,
+                          "wall_value": ev / wall, "cpu_model": op.cpu_model()}, res
 
 
 def single_core_rate(batch, budget_events=4_000_000):
@@ -226,17 +237,19 @@ def run_reference(args, world, rank):
         from workloads import suites
         b = suites.pool_batch(range(total_tr))
     sample, sdesc = bounded_sample(b, 30_000_000)
-    cores = len(os.sched_getaffinity(0))
-    import oracle
-    for _ in range(args.warmup):
-        oracle.simulate_batch_parallel(sample, workers=cores)
+    op = _oracle_pool()
     times = []
+    busiest = []
     ev = 0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        r = oracle.simulate_batch_parallel(sample, workers=cores)
-        times.append(time.perf_counter() - t0)
-        ev = int(r["events_done"].sum())
+    with op.Pool(sample) as pool:           # forked once; every step re-runs the oracle
+        cores = pool.workers
+        for _ in range(args.warmup):
+            pool.run()
+        for _ in range(args.steps):
+            r, wall, busy, _ = pool.run()
+            times.append(wall)
+            busiest.append(busy)
+            ev = int(r["events_done"].sum())
     ms = 1e3 * float(np.mean(times))
     value = ev / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -247,7 +260,11 @@ def run_reference(args, world, rank):
             "config": {"workload": desc, "sample": sdesc, "n_traces": total_tr,
                        "n_events": total_ev},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": sdesc},
+                             "sample": sdesc, "cpu_model": op.cpu_model(),
+                             "timing": "wall time of one pass of forked workers (inputs inherited "
+                                       "at fork, results returned); busiest worker's simulate-only "
+                                       "rate in simulate_only_value",
+                             "simulate_only_value": ev / float(np.mean(busiest))},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -374,21 +391,28 @@ def main():
         ws = None
         capn = np.ascontiguousarray(batch.capacity, np.uint64) if has_cap else None
 
-        def e2e_ms(mode):
+        def e2e_ms(mode, from_raw=False):
             """Mean wall time of xm_simulate_host with event input `mode`
-            (XM_HOST_INPUT, capi.cu); None = the library default."""
+            (XM_HOST_INPUT, capi.cu; None = the library default). from_raw:
+            every step starts from the caller's raw arrays, i.e. includes
+            xm_load_traces (validation S:231/S:249/S:258, dense renumbering,
+            LPT order, page-locked packing; SURVEY.md §8(d) end-to-end)."""
             nonlocal ws
             old_mode = os.environ.pop("XM_HOST_INPUT", None)
             if mode:
                 os.environ["XM_HOST_INPUT"] = mode
+
+            def one():
+                t_ = xm.load_traces(batch.bytes, batch.tag, batch.off) if from_raw else tr
+                return xm.simulate_host(t_, cfg, capacity=capn, workspace=ws)
             try:
                 for _ in range(2):
-                    _, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
+                    _, ws = one()
                 if world > 1:
                     dist.barrier()
                 t0 = time.perf_counter()
                 for _ in range(args.steps):
-                    hh, ws = xm.simulate_host(tr, cfg, capacity=capn, workspace=ws)
+                    hh, ws = one()
                 dt = (time.perf_counter() - t0) / args.steps
             finally:
                 os.environ.pop("XM_HOST_INPUT", None)
@@ -400,6 +424,7 @@ def main():
                 dt = float(t[0])
             return dt, hh
 
+        dt_raw, h_raw = e2e_ms(None, from_raw=True)
         dt, h_e2e = e2e_ms(None)
         dt_stream, h_stream = e2e_ms("stream")
         ev_bytes = 8 if tr.packed is not None else 12        # packed or bytes + tag
@@ -407,15 +432,19 @@ def main():
             + 8 * batch.n_traces + (8 * batch.n_traces if has_cap else 0)
         direct = tr.packed is not None and not os.environ.get("XM_NO_STREAM") \
             and os.environ.get("XM_HOST_INPUT", "direct") == "direct"
-        e2e = {"value": done / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(64 * batch.n_traces), "ms_per_step": dt * 1e3,
-               "api": "xm_simulate_host (pinned host traces -> device -> host results; "
+        e2e = {"value": done / dt_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(64 * batch.n_traces), "ms_per_step": dt_raw * 1e3,
+               "api": "xm_load_traces (caller's raw host arrays: validation, dense ids, LPT "
+                      "order, page-locked packing) + xm_simulate_host, every step",
+               "pinned_handle": {"value": done / dt, "ms_per_step": dt * 1e3},
+               "pinned_handle_api": "xm_simulate_host on an already loaded handle (pinned host traces -> device -> host results; "
                       + ("events read by the replaying warps straight from the page-locked "
                          "host array over PCIe, no staging copy; " if direct else
                          "upload streamed in longest-first chunks overlapping the replay; ")
                       + ("8-byte packed events)" if tr.packed is not None else "12-byte events)"),
                "stream_copy_ms_per_step": dt_stream * 1e3,
-               "results_equal_device_path": bool((h_e2e == h).all() and (h_stream == h).all())}
+               "results_equal_device_path": bool((h_e2e == h).all() and (h_stream == h).all()
+                                                 and (h_raw == h).all())}
     clocks = sampler.stop() if sampler else None
 
     # ---- roofline of the dominant kernel (k_replay): algorithmic bytes / launch time
@@ -468,9 +497,11 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample, sdesc = bounded_sample(batch)
-        rate, sec, cores, o, ev = oracle_rate(sample)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": sdesc + f"; {sec:.2f} s wall on {cores} host processes",
+        rate, det, o = oracle_rate(sample)
+        cpu = {"value": rate, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+               "sample": sdesc + f"; busiest of {det['cores']} forked workers simulated for "
+                                 f"{det['busiest_worker_simulate_s']:.2f} s",
+               "cpu_model": det["cpu_model"], "wall_value": det["wall_value"],
                "single_core": single_core_rate(batch)}
         if not args.no_parity and sample.n_traces == batch.n_traces:
             sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -634,25 +665,34 @@ def main_cfg5(args, world, rank, local):
           "frac": 12 * n_ev_local / (k4_ms / 1e3) / 1e9 / peak,
           "alg_bytes_per_launch": 12 * n_ev_local}
     cpu = parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_parity:
+        # EVERY trace (north_star: bit-exact "for every trace versus the CPU
+        # oracle"): forked workers rebuild their chunks on the host
+        # (workloads/mc5gen.c, the documented recipe), replay them with the
+        # oracle and compare all 13 fields with the GPU's results
+        op = _oracle_pool()
+        s = op.parity_mc5(np.arange(n), h)
+        parity = {"traces": s["traces"], "fields": s["fields"],
+                  "mismatched_values": s["mismatched_values"],
+                  "mismatched_by_field": s["mismatched_by_field"],
+                  "first_mismatch_trace": s["first_mismatch_trace"],
+                  "sample": f"all {n} traces, host-built independently of K4",
+                  "oracle_oom_traces": s["oracle_oom_traces"], "wall_s": s["wall_s"]}
+        cpu = {"value": s["oracle_events"] / s["oracle_simulate_s_max_worker"], "unit": UNIT,
+               "cores": s["workers"], "kind": "oracle", "cpu_model": op.cpu_model(),
+               "sample": f"all {n} traces ({s['oracle_events']} replayed events); busiest of "
+                         f"{s['workers']} forked workers simulated for "
+                         f"{s['oracle_simulate_s_max_worker']:.1f} s (host trace generation "
+                         f"excluded)",
+               "wall_s_incl_generation_and_compare": s["wall_s"]}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         k = max(1, int(np.ceil(n_ev_local / 25_000_000)))
         sub = np.arange(0, n, k)
-        hb = mc5.batch(sub)
-        rate, sec, cores, o, ev = oracle_rate(hb)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"every {k}th trace: {hb.n_traces} traces ({hb.n_events} events); "
-                         f"{sec:.2f} s wall on {cores} host processes"}
-        if not args.no_parity:
-            sys.path.insert(0, os.path.join(ROOT, "tests"))
-            from gpu_util import COMPARE
-            mism = 0
-            for f in COMPARE:
-                exp = o[f].astype(np.uint64)
-                if f == "n_free_blocks_end":
-                    exp = np.minimum(exp, 65535)
-                mism += int((h[f][sub].astype(np.uint64) != exp).sum())
-            parity = {"traces": int(len(sub)), "fields": len(COMPARE), "mismatched_values": mism,
-                      "sample": f"every {k}th of {n} traces"}
+        hb = mc5.batch_fast(sub)
+        rate, det, o = oracle_rate(hb)
+        cpu = {"value": rate, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+               "cpu_model": det["cpu_model"],
+               "sample": f"every {k}th trace: {hb.n_traces} traces ({hb.n_events} events)"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

@@ -12,7 +12,9 @@
  * addr) opens a block; a deallocation (-bytes at addr) closes the most
  * recently opened still-open block at that address (D1, LIFO per address);
  * none open -> orphan free (tallied, SPEC D4); |bytes| != the block's size ->
- * mismatch (tallied; the block is closed with its own size).
+ * mismatch (tallied; the block is closed with its own size). S:107's "whose
+ * size matches" clause is read as in DESIGN.md Q22: the LIFO top closes
+ * whatever its size (otherwise S:107's own mismatch clause could never fire).
  *
  * Plain sequential C: a per-address stack of open blocks (linked through the
  * alloc events' indices) found through an open-addressing hash map.

@@ -16,7 +16,9 @@ Readings (Q21): MRE selects runs with OOM_jd1 = 0 and uses
 error_jde2 when OOM_jde2 = 0, else error_jde1 (Eq. median-error; a run whose
 round 2 was not run counts as OOM_jde2 != 0); the even-count median is the
 mean of the central pair (SPEC D1); a record with round-2 fields although
-not C1 = 1 and OOM_jd1 = 0 is invalid (SPEC D2, P:385 gating).
+not C1 = 1 and OOM_jd1 = 0 is invalid (SPEC D2, P:385 gating). M_save's
+OOM penalty is the equation's -M_max ("-M_max
+otherwise"), not P:439's prose "the M̂peak ... is deducted" (Q21).
 
 Parity status: pinned (tests/test_oracle_metrics.py: SPEC.md worked examples
 and properties).

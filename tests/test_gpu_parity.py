@@ -90,6 +90,39 @@ def test_edge_cases():
     _check(tb.build())
 
 
+def test_wide_layout_saturated_keys():
+    """Free blocks of >= 2^27 units (64 GiB): the WIDE layout's best-fit key
+    saturates, so the winner is chosen by the exact (size, addr) compare
+    (replay.cu best_fit_exact). Covers distinct saturated sizes, equal
+    saturated sizes in different segments (lowest address wins, reading Q4),
+    a request whose candidates mix saturated and exact keys, reclamation of a
+    saturated segment, and frees that merge into saturated blocks."""
+    G = 1 << 30
+    tb = TraceBuilder()
+    # distinct saturated sizes, listed larger-first in the free list
+    tb.alloc(0, 70 * G).alloc(1, 66 * G).free(0).free(1).alloc(2, 65 * G).alloc(3, 69 * G)
+    tb.free(2).alloc(4, 66 * G - 4096).free(3).free(4).alloc(5, 67 * G).end_trace()
+    # equal saturated sizes in different segments: lowest address wins
+    tb.alloc(0, 68 * G).alloc(1, 68 * G).free(1).free(0).alloc(2, 67 * G).alloc(3, 67 * G)
+    tb.free(2).free(3).alloc(4, 68 * G).end_trace()
+    # mixed: an exact key (1 GiB) beats the saturated one; then only saturated fit
+    tb.alloc(0, 70 * G).alloc(1, G).free(0).free(1).alloc(2, 512 << 20).alloc(3, 2 * G)
+    tb.alloc(4, 3 * G).free(3).alloc(5, 600 << 20).free(2).free(4).free(5).end_trace()
+    # reclamation with a saturated whole-segment free block (capacity 200 GiB)
+    tb.alloc(0, 100 * G).free(0).alloc(1, 150 * G).alloc(2, 40 * G).free(1).alloc(3, 120 * G)
+    tb.end_trace(capacity=200 * G)
+    # splits of saturated blocks into many pieces, then coalescing back
+    tb.alloc(0, 80 * G).free(0)
+    for i in range(1, 9):
+        tb.alloc(i, 9 * G + 512 * i)
+    for i in (2, 4, 6, 8, 1, 3, 5, 7):
+        tb.free(i)
+    tb.alloc(9, 79 * G).end_trace()
+    b = tb.build()
+    h = _check(b)
+    assert (h["status"][:3] == 0).all() and h["n_seg_release"][3] > 0
+
+
 def test_config1_mlp():
     _check(suites.config1())
 

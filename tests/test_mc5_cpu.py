@@ -71,3 +71,17 @@ def test_expand_fails_loudly_without_gpu():
     rc = xm.lib().xm_expand_templates(ctypes.byref(t), None, None, None, 0, None, 1,
                                       None, None, None, None)
     assert rc != 0
+
+
+def test_c_recipe_equals_numpy_recipe():
+    """workloads/mc5gen.c (used for parity on all 1M config-5 traces) builds
+    exactly the traces of the documented numpy recipe."""
+    idx = np.r_[np.arange(0, 1_000_000, 2011), np.arange(999_000, 999_050)]
+    a = mc5.batch(idx)
+    b = mc5.batch_fast(idx)
+    assert (a.off == b.off).all() and (a.capacity == b.capacity).all()
+    assert (a.bytes == b.bytes).all() and (a.tag == b.tag).all()
+    # the swap rule fired (the recipe is not the identity)
+    fixed, per, tag, tpl_off, _ = mc5.template_pool()
+    assert any((b.tag[b.off[t]:b.off[t + 1]] != tag[tpl_off[k]:tpl_off[k + 1]]).any()
+               for t, k in enumerate(mc5.describe(idx)["tpl"][:50]))

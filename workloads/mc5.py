@@ -201,3 +201,59 @@ def batch(idx, salt: int = SALT) -> Batch:
     return Batch(np.concatenate([it[0] for it in items]) if items else np.zeros(0, np.int64),
                  np.concatenate([it[1] for it in items]) if items else np.zeros(0, np.uint32),
                  off, d["capacity"].astype(np.uint64), names)
+
+
+# ---- the same recipe in C (workloads/mc5gen.c), for full-size host parity ------
+_HERE = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+_GEN_SRC = _HERE + "/mc5gen.c"
+_GEN_LIB = _HERE + "/libmc5gen.so"
+_gen = None
+
+
+def build_gen(force: bool = False) -> str:
+    import os
+    import subprocess
+    if force or not os.path.exists(_GEN_LIB) or os.path.getmtime(_GEN_LIB) < os.path.getmtime(_GEN_SRC):
+        tmp = _GEN_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o", tmp, _GEN_SRC])
+        os.replace(tmp, _GEN_LIB)
+    return _GEN_LIB
+
+
+def _genlib():
+    global _gen
+    if _gen is None:
+        import ctypes
+        build_gen()
+        L = ctypes.CDLL(_GEN_LIB)
+        P = ctypes.c_void_p
+        L.mc5_instantiate.argtypes = [P, P, P, P, P, P, P, ctypes.c_int64, ctypes.c_uint64, P, P, P]
+        L.mc5_instantiate.restype = ctypes.c_int
+        _gen = L
+    return _gen
+
+
+def batch_fast(idx, salt: int = SALT) -> Batch:
+    """batch(idx) built by the C form of the recipe (byte-identical to batch();
+    tests/test_mc5_cpu.py), ~100x faster: the host side of config-5 parity on
+    every one of the 1M traces."""
+    import ctypes
+    idx = np.asarray(idx, np.int64)
+    d = describe(idx, salt)
+    fixed, per, tag, tpl_off, _ = template_pool()
+    n = np.diff(tpl_off)[d["tpl"]]
+    off = np.zeros(len(idx) + 1, np.int64)
+    off[1:] = np.cumsum(n)
+    ob = np.empty(int(off[-1]), np.int64)
+    ot = np.empty(int(off[-1]), np.uint32)
+    tp = np.ascontiguousarray(d["tpl"], np.uint32)
+    bb = np.ascontiguousarray(d["b"], np.uint32)
+    sd = np.ascontiguousarray(d["seed"], np.uint64)
+
+    def p(a):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    rc = _genlib().mc5_instantiate(p(fixed), p(per), p(tag), p(tpl_off), p(tp), p(bb), p(sd),
+                                   len(idx), SWAP_THRESHOLD, p(off), p(ob), p(ot))
+    if rc:
+        raise RuntimeError("mc5_instantiate: span mismatch")
+    return Batch(ob, ot, off, d["capacity"].astype(np.uint64), [])
