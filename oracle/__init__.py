@@ -58,7 +58,8 @@ class _Cfg(ctypes.Structure):
                 ("min_large_alloc", ctypes.c_uint64), ("round_large", ctypes.c_uint64),
                 ("capacity", ctypes.c_uint64), ("large_split_strict", ctypes.c_int32),
                 ("roundup_power2_divisions", ctypes.c_int32), ("reclaim_policy", ctypes.c_int32),
-                ("_pad", ctypes.c_int32)]
+                ("_pad", ctypes.c_int32), ("max_split_size", ctypes.c_uint64),
+                ("max_non_split_rounding", ctypes.c_uint64), ("gc_threshold", ctypes.c_double)]
 
 
 @dataclass
@@ -74,12 +75,16 @@ class Config:
     large_split_strict: int = 1
     roundup_power2_divisions: int = 0    # NEXT-4 variant (torch knob); 0/1 = off
     reclaim_policy: int = 0              # 0 torch release-all (Q3); 1 SPEC.md:283 D3
+    max_split_size: int = UNLIMITED      # torch max_split_size_mb:N -> N MiB (Q26); off
+    max_non_split_rounding: int = 20 * MiB   # torch max_non_split_rounding_mb (Q26)
+    gc_threshold: float = 0.0            # torch garbage_collection_threshold (Q27); off
 
     def c(self) -> _Cfg:
         return _Cfg(self.min_block, self.small_size, self.small_buffer, self.large_buffer,
                     self.min_large_alloc, self.round_large, self.capacity,
                     self.large_split_strict, self.roundup_power2_divisions,
-                    self.reclaim_policy, 0)
+                    self.reclaim_policy, 0, self.max_split_size, self.max_non_split_rounding,
+                    self.gc_threshold)
 
 
 def build(force: bool = False) -> str:

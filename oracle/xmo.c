@@ -27,6 +27,7 @@
  *   Q5 per-stream pools: stream is an exact-match filter
  *   Q6 array order is replay order, Q7 first index reaching a peak
  *   Q9 OOM stops the trace; Q10 refuse iff reserved + size > capacity
+ *   Q19, Q20, Q26, Q27 allocator variants (NEXT-4), off by default
  *
  * Parity status: every function below is pinned by tests/test_oracle_*.py
  * (SPEC worked examples, paper examples, closed forms H1-H7, invariants
@@ -69,6 +70,12 @@ typedef struct {
   int32_t  reclaim_policy;           /* 0: torch release all cached segments (reading Q3);     */
                                      /* 1: SPEC.md:283 D3 largest first until capacity suffices */
   int32_t  _pad;
+  /* NEXT-4 variants, torch PYTORCH_CUDA_ALLOC_CONF knobs (PAPER.md:257 defers to
+   * the PyTorch allocator; readings Q26, Q27):                                  */
+  uint64_t max_split_size;           /* max_split_size_mb:N -> N MiB; UINT64_MAX = off  */
+  uint64_t max_non_split_rounding;   /* max_non_split_rounding_mb (default 20 MiB)      */
+  double   gc_threshold;             /* garbage_collection_threshold:x, 0 = off; acts   */
+                                     /* only with a finite capacity ("set_fraction")     */
 } xmo_config;
 
 /* ------------------------------------------------------------------------ */
@@ -126,6 +133,7 @@ typedef struct {
   int64_t prev, next;   /* address-order neighbours in the same segment, -1 = none */
   int64_t seg;
   int32_t stream, small, allocated, alive;
+  uint64_t gc_base;     /* its pool's free-block-search count when it entered the free index */
 } Block;
 
 typedef struct {
@@ -143,6 +151,7 @@ typedef struct {
   uint64_t next_base;
   uint64_t reserved, alloc_blk, alloc_tensor;
   int64_t live_segs;
+  uint64_t searches[2];                /* free-block searches per pool [large, small] (GC ages) */
 } State;
 
 static int grow(void** p, int64_t* cap, int64_t need, size_t elem) {
@@ -180,7 +189,21 @@ static int64_t new_block(State* S) {
 static int free_index_add(State* S, int64_t b) {
   if (grow((void**)&S->fr, &S->capfr, S->nfr + 1, sizeof(int64_t))) return XMO_E_NOMEM;
   S->fr[S->nfr++] = b;
+  /* torch BlockPool::insert_into_blocks: gc_count_base = the pool's
+   * get_free_blocks_call_count, so the block's age counts from now */
+  S->blk[b].gc_base = S->searches[S->blk[b].small];
   return 0;
+}
+
+/* Return a whole-segment free block's segment to the device (torch
+ * release_block). The caller removes it from the free index. */
+static void release_segment_of(State* S, Block* b, uint64_t* out) {
+  Segment* g = &S->seg[b->seg];
+  g->alive = 0;
+  S->reserved -= g->size;
+  S->live_segs -= 1;
+  out[F_NSEG_RELEASE] += 1;
+  b->alive = 0;
 }
 
 static void free_index_remove(State* S, int64_t b) {
@@ -234,6 +257,104 @@ static void release_largest_first(State* S, uint64_t need, uint64_t capacity, ui
     b->alive = 0;
     S->fr[best] = S->fr[S->nfr - 1];
     S->nfr--;
+  }
+}
+
+/* Variant (NEXT-4, reading Q26): torch release_available_cached_blocks, run
+ * only when max_split_size is set, when the device refuses a new segment and
+ * before release_cached. key = max(s, max_split_size). In the request's pool
+ * and stream, the smallest free block with size >= key (lowest address on a
+ * tie) is released if there is one; otherwise the free blocks of that pool
+ * and stream with size >= max_split_size are released from the largest down
+ * (torch walks its (stream, size, address) set backwards: equal sizes go
+ * highest address first) until at least key bytes are released. Blocks of
+ * max_split_size or more are never split, so each is a whole segment (checked:
+ * XMO_E_INVARIANT otherwise). Returns 1 when it released the one block or at
+ * least key bytes (torch then retries the device), 0 otherwise (torch goes on
+ * to release_cached straight away; the releases made stand), <0 on error. */
+static int release_available(State* S, const xmo_config* c, uint64_t s, int small, int32_t stream,
+                             uint64_t* out) {
+  if (c->max_split_size == UINT64_MAX) return 0;
+  uint64_t key = s < c->max_split_size ? c->max_split_size : s;
+  int64_t best = -1;
+  for (int64_t k = 0; k < S->nfr; ++k) {
+    Block* B = &S->blk[S->fr[k]];
+    if (B->small != small || B->stream != stream || B->size < key) continue;
+    if (best < 0 || B->size < S->blk[S->fr[best]].size ||
+        (B->size == S->blk[S->fr[best]].size && B->addr < S->blk[S->fr[best]].addr))
+      best = k;
+  }
+  if (best >= 0) {
+    Block* B = &S->blk[S->fr[best]];
+    if (B->prev >= 0 || B->next >= 0) return XMO_E_INVARIANT;
+    release_segment_of(S, B, out);
+    S->fr[best] = S->fr[S->nfr - 1];
+    S->nfr--;
+    return 1;
+  }
+  uint64_t released = 0;
+  while (released < key) {
+    int64_t top = -1;                     /* largest (size, addr) below key */
+    for (int64_t k = 0; k < S->nfr; ++k) {
+      Block* B = &S->blk[S->fr[k]];
+      if (B->small != small || B->stream != stream) continue;
+      if (top < 0 || B->size > S->blk[S->fr[top]].size ||
+          (B->size == S->blk[S->fr[top]].size && B->addr > S->blk[S->fr[top]].addr))
+        top = k;
+    }
+    if (top < 0) break;
+    Block* B = &S->blk[S->fr[top]];
+    if (B->size < c->max_split_size) break;
+    if (B->prev >= 0 || B->next >= 0) return XMO_E_INVARIANT;
+    released += B->size;
+    release_segment_of(S, B, out);
+    S->fr[top] = S->fr[S->nfr - 1];
+    S->nfr--;
+  }
+  return released >= key ? 1 : 0;
+}
+
+/* Variant (NEXT-4, reading Q27): torch garbage_collect_cached_blocks, run on
+ * every free-block search that found nothing while garbage_collection_threshold
+ * is set and the capacity is finite. Acts only when reserved exceeds
+ * threshold * capacity; then, over the LARGE pool's whole-segment free blocks
+ * (all streams), repeatedly: the mean age (double(total age) / count) is the
+ * bar, and every block at least that old is released (in one pass, without
+ * stopping at the target), until reserved has dropped by the excess or a pass
+ * releases nothing. Age = large-pool searches since the block entered the free
+ * index (torch gc_count). */
+static void garbage_collect(State* S, const xmo_config* c, uint64_t* out) {
+  uint64_t gc_bytes = (uint64_t)(c->gc_threshold * (double)c->capacity);
+  if (S->reserved <= gc_bytes) return;
+  uint64_t target = S->reserved - gc_bytes, reclaimed = 0, total_age = 0;
+  int64_t freeable = 0;
+  for (int64_t k = 0; k < S->nfr; ++k) {
+    Block* B = &S->blk[S->fr[k]];
+    if (B->small || B->prev >= 0 || B->next >= 0) continue;
+    total_age += S->searches[0] - B->gc_base;
+    freeable++;
+  }
+  if (freeable == 0) return;
+  int freed = 1;
+  while (reclaimed < target && freed && freeable > 0) {
+    double age_threshold = (double)total_age / (double)freeable;
+    freed = 0;
+    int64_t k = 0;
+    while (k < S->nfr) {
+      Block* B = &S->blk[S->fr[k]];
+      uint64_t age = S->searches[0] - B->gc_base;
+      if (!B->small && B->prev < 0 && B->next < 0 && (double)age >= age_threshold) {
+        freed = 1;
+        reclaimed += B->size;
+        total_age -= age;
+        freeable--;
+        release_segment_of(S, B, out);
+        S->fr[k] = S->fr[S->nfr - 1];
+        S->nfr--;
+      } else {
+        ++k;
+      }
+    }
   }
 }
 
@@ -322,6 +443,10 @@ int xmo_simulate(const int64_t* bytes, const uint32_t* tag, int64_t n,
       uint64_t s = xmo_round_size(req, &cc);
       int small = xmo_is_small(s, &cc);
 
+      /* torch get_free_block counts its calls per pool while GC is on */
+      int gc_on = cc.gc_threshold > 0.0 && cc.capacity != UINT64_MAX;
+      if (gc_on) S.searches[small] += 1;
+
       /* best fit: min (size, addr) over free blocks of this pool and stream */
       int64_t best = -1;
       for (int64_t k = 0; k < S.nfr; ++k) {
@@ -332,19 +457,36 @@ int xmo_simulate(const int64_t* bytes, const uint32_t* tag, int64_t n,
           best = S.fr[k];
       }
 
+      /* max_split_size variant (reading Q26; torch get_free_block): "Do not
+       * return an oversized block" -- for a request below max_split_size, a
+       * best fit of max_split_size or more; for a larger request, a best fit
+       * of s + max_non_split_rounding or more. Nothing else is searched. */
+      if (best >= 0) {
+        uint64_t bs = S.blk[best].size;
+        if (s < cc.max_split_size && bs >= cc.max_split_size) best = -1;
+        else if (s >= cc.max_split_size && bs >= s + cc.max_non_split_rounding) best = -1;
+      }
+
       int64_t b;
       if (best >= 0) {
         free_index_remove(&S, best);
         b = best;
       } else {
+        if (gc_on) garbage_collect(&S, &cc, out);     /* GC variant (Q27)      */
         /* New segment from the device level (PAPER.md:259 (iv) "New segments
          * are requested from the GPU only if this cache is insufficient"). */
         uint64_t a = xmo_segment_size(s, &cc);
         if (S.reserved + a > cc.capacity) {           /* device refuses (Q10) */
-          if (cc.reclaim_policy == 1)
+          if (cc.reclaim_policy == 1) {
             release_largest_first(&S, a, cc.capacity, out);  /* SPEC D3 variant */
-          else
-            release_cached(&S, out);                  /* reclaim (Q3)          */
+          } else {
+            /* torch: alloc_block || (release_available && alloc_block) ||
+             * (release_cached && alloc_block) */
+            int e = release_available(&S, &cc, s, small, stream, out);   /* Q26 */
+            if (e < 0) { rc = e; goto done; }
+            if (e == 0 || S.reserved + a > cc.capacity)
+              release_cached(&S, out);                /* reclaim (Q3)          */
+          }
           if (S.reserved + a > cc.capacity) {         /* retry refused: OOM    */
             status = XMO_T_OOM;                       /* PAPER.md:260 (v)      */
             break;
@@ -366,9 +508,11 @@ int xmo_simulate(const int64_t* bytes, const uint32_t* tag, int64_t n,
         sl = map_find(&S, id, 1);  /* (arena realloc does not move the map) */
       }
 
-      /* split: the request takes the low end, the remainder stays free */
+      /* split: the request takes the low end, the remainder stays free; with
+       * max_split_size set a large-pool request of that size or more is never
+       * split (torch should_split: size < max_split_size && remaining > ...) */
       uint64_t rem = S.blk[b].size - s;
-      if (xmo_should_split(small, rem, &cc)) {
+      if (xmo_should_split(small, rem, &cc) && (small || s < cc.max_split_size)) {
         int64_t r = new_block(&S);
         if (r < 0) { rc = XMO_E_NOMEM; goto done; }
         Block* B = &S.blk[b];

@@ -62,10 +62,30 @@ class Seg:
             yield (a, self.base + self.size - a)
 
 
-def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, reclaim=0):
+def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, reclaim=0,
+             msplit=None, nsr=20 * MiB, gc=0.0):
     """bases: optional segment base addresses in creation order (e.g. the real
-    cudaMalloc addresses torch got); default = bump addresses (reading Q4)."""
+    cudaMalloc addresses torch got); default = bump addresses (reading Q4).
+    msplit / nsr / gc: torch's max_split_size (bytes), max_non_split_rounding
+    and garbage_collection_threshold knobs (NEXT-4, readings Q26/Q27), stated
+    here on gaps: a free block's AGE is the number of large-pool searches since
+    a gap with exactly its bounds appeared."""
     segs = []
+    gc_on = gc > 0.0 and capacity != UNLIMITED
+    searches = {False: 0, True: 0}               # per pool (small flag)
+    birth = {}                                   # (base, start, len) -> searches then
+
+    def gaps_now():
+        return {(g.base, a, L): g for g in segs for (a, L) in g.gaps()}
+
+    def age(g):
+        return searches[False] - birth[(g.base, g.base, g.size)]
+
+    def drop(g):
+        nonlocal reserved
+        segs.remove(g)
+        reserved -= g.size
+        out["n_seg_release"] += 1
     where = {}     # id -> (seg, start, end, s, request)
     nxt = 0
     reserved = blk = tensor = 0
@@ -81,6 +101,8 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, re
         if nb > 0:
             s = rnd(nb, div=div)
             small = s <= MiB
+            if gc_on:
+                searches[small] += 1
             best = None
             for g in segs:
                 if g.stream != st or g.small != small:
@@ -88,8 +110,48 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, re
                 for (a, L) in g.gaps():
                     if L >= s and (best is None or (L, a) < (best[0], best[1])):
                         best = (L, a, g)
+            if best is not None and msplit is not None:
+                # an oversized best fit is refused (and nothing else is tried)
+                if (s < msplit and best[0] >= msplit) or (s >= msplit and best[0] >= s + nsr):
+                    best = None
+            if best is None and gc_on:
+                bar = int(gc * float(capacity))
+                if reserved > bar:
+                    target, got = reserved - bar, 0
+                    empty = [g for g in segs if not g.small and not g.ext]
+                    ages = sum(age(g) for g in empty)
+                    n_ok, freed_any = len(empty), True
+                    while empty and got < target and freed_any and n_ok > 0:
+                        mean = ages / n_ok
+                        old = [g for g in empty if age(g) >= mean]
+                        freed_any = bool(old)
+                        for g in old:
+                            got += g.size
+                            ages -= age(g)
+                            n_ok -= 1
+                            empty.remove(g)
+                            drop(g)
             if best is None:
                 need = seg_size(s)
+                refit = True       # torch: a failed release_available goes straight on
+                if reserved + need > capacity and reclaim == 0 and msplit is not None:
+                    key = max(s, msplit)
+                    mine = [(L, a, g) for g in segs if g.stream == st and g.small == small
+                            for (a, L) in g.gaps()]
+                    fit = [x for x in mine if x[0] >= key]
+                    if fit:
+                        L, a, g = min(fit, key=lambda x: (x[0], x[1]))
+                        assert not g.ext, "an oversize free block is a whole segment"
+                        drop(g)
+                    else:
+                        got = 0
+                        for L, a, g in sorted(mine, key=lambda x: (x[0], x[1]), reverse=True):
+                            if got >= key or L < msplit:
+                                break
+                            assert not g.ext, "an oversize free block is a whole segment"
+                            got += L
+                            drop(g)
+                        refit = got >= key
                 if reserved + need > capacity and reclaim == 1:
                     # SPEC.md:283 D3: empty segments, largest first (then lowest
                     # base), only until the request fits
@@ -102,7 +164,7 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, re
                     if reserved + need > capacity:
                         out["status"] = 1
                         break
-                elif reserved + need > capacity:
+                elif reserved + need > capacity or not refit:
                     keep = []
                     for g in segs:
                         if g.ext:
@@ -125,7 +187,8 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, re
                 out["max_live_segments"] = max(out["max_live_segments"], len(segs))
                 best = (need, g.base, g)
             L, a, g = best
-            take = s if split_ok(small, L - s, strict) else L
+            no_split = msplit is not None and not small and s >= msplit
+            take = s if split_ok(small, L - s, strict) and not no_split else L
             bisect.insort(g.ext, (a, a + take, bid))
             where[bid] = (g, a, a + take, s)
             blk += take
@@ -142,6 +205,9 @@ def simulate(bytes_, tag, capacity=UNLIMITED, strict=True, bases=None, div=0, re
         if reserved > out["peak_reserved"]:
             out["peak_reserved"], out["peak_reserved_idx"] = reserved, i
         curve.append((tensor, blk, reserved))
+        if gc_on:
+            now = gaps_now()
+            birth = {k: birth.get(k, searches[g.small]) for k, g in now.items()}
     else:
         i = len(bytes_)
     out["events_done"] = i

@@ -37,8 +37,8 @@ MUTANTS = [
     ("best fit: tie by high addr", "B->addr < S.blk[best].addr", "B->addr > S.blk[best].addr"),
     ("capacity: >=", "if (S.reserved + a > cc.capacity) {           /* device refuses",
      "if (S.reserved + a >= cc.capacity) {           /* device refuses"),
-    ("no reclamation", "release_cached(&S, out);                  /* reclaim",
-     "/* release_cached */;                  /* reclaim"),
+    ("no reclamation", "release_cached(&S, out);                /* reclaim",
+     "/* release_cached */;                /* reclaim"),
     ("no merge prev", "if (p >= 0 && !S.blk[p].allocated) {", "if (0) {"),
     ("no merge next", "if (q >= 0 && !S.blk[q].allocated) {", "if (0) {"),
     ("split remainder at low end", "R->addr = B->addr + s;", "R->addr = B->addr;"),
@@ -155,6 +155,77 @@ def test_variant_mutant_rejected(name, old, new):
         assert _variant_pins_reject(_build(src, d)) is None
         L = _build(src.replace(old, new, 1), d + "/m")
         assert _variant_pins_reject(L) is not None, f"pins did not catch mutant: {name}"
+
+
+# ---- torch knobs max_split_size / garbage_collection_threshold (Q26, Q27) -------
+KNOB_MUTANTS = [
+    ("msplit: small request takes an oversize block",
+     "if (s < cc.max_split_size && bs >= cc.max_split_size) best = -1;", "if (0) best = -1;"),
+    ("msplit: no non-split rounding bound",
+     "else if (s >= cc.max_split_size && bs >= s + cc.max_non_split_rounding) best = -1;", ""),
+    ("msplit: oversize requests split", "&& (small || s < cc.max_split_size)", "&& (1)"),
+    ("release_available: largest fitting block",
+     "if (best < 0 || B->size < S->blk[S->fr[best]].size ||",
+     "if (best < 0 || B->size > S->blk[S->fr[best]].size ||"),
+    ("release_available: a failed walk still retries", "return released >= key ? 1 : 0;", "return 1;"),
+    ("release_available: never", "int e = release_available(&S, &cc, s, small, stream, out);",
+     "int e = 0;"),
+    ("GC: strictly older than the mean", "(double)age >= age_threshold", "(double)age > age_threshold"),
+    ("GC: small pool counted", "if (B->small || B->prev >= 0 || B->next >= 0) continue;",
+     "if (B->prev >= 0 || B->next >= 0) continue;"),
+    ("GC: one pass only", "while (reclaimed < target && freed && freeable > 0) {",
+     "while (reclaimed < target && freed && freeable > 0 && !reclaimed) {"),
+    ("GC: bar from reserved", "(uint64_t)(c->gc_threshold * (double)c->capacity)",
+     "(uint64_t)(c->gc_threshold * (double)S->reserved)"),
+    ("GC: age never reset", "  S->blk[b].gc_base = S->searches[S->blk[b].small];\n", ""),
+]
+
+
+def _knob_pins_reject(L):
+    import test_oracle_variants as V
+    M = 1 << 20
+    hand_cases = [  # (events, capacity, msplit, gc, expected fields) from the H9-H12 docstrings
+        (lambda t: t.alloc(0, 100 * M).free(0).alloc(1, 90 * M).free(1).alloc(2, 30 * M)
+         .alloc(3, 70 * M), oracle.UNLIMITED, 64 * M, 0.0, {"peak_reserved": 200 * M}),
+        (lambda t: t.alloc(0, 100 * M).alloc(1, 30 * M).alloc(2, M).free(0).free(1).free(2)
+         .alloc(3, 70 * M), 180 * M, 64 * M, 0.0, {"n_seg_release": 1, "final_reserved": 102 * M}),
+        (lambda t: t.alloc(0, 66 * M).alloc(1, 70 * M).alloc(2, 30 * M).free(0).free(1).free(2)
+         .alloc(3, 120 * M), 200 * M, 64 * M, 0.0, {"n_seg_release": 2, "final_reserved": 150 * M}),
+        (lambda t: t.alloc(0, 66 * M).alloc(1, 70 * M).alloc(2, 30 * M).free(0).free(1).free(2)
+         .alloc(3, 150 * M), 200 * M, 64 * M, 0.0, {"n_seg_release": 3}),
+        (lambda t: t.alloc(0, 200 * M).alloc(1, 150 * M).alloc(2, 120 * M).alloc(3, 60 * M).free(0)
+         .free(2).alloc(4, 110 * M).free(4).alloc(5, 100 * M).free(5).alloc(6, 300 * M),
+         1000 * M, None, 0.5, {"peak_reserved": 630 * M, "n_seg_release": 1}),
+    ]
+    for k, (ev, cap, ms, gc, exp) in enumerate(hand_cases):
+        by, tg = V._one(ev, cap)
+        cfg = oracle.Config(gc_threshold=gc, **({"max_split_size": ms} if ms else {}))
+        rc, r, _ = _run(L, by, tg, cap, cfg)
+        if rc or any(r[f] != v for f, v in exp.items()):
+            return f"hand H{9 + k}"
+    for ms, gc, corpus in ((24 * M, 0.0, fuzz.spec1_corpus(50, 300, salt=94)),
+                           (24 * M, 0.0, fuzz.capacity_corpus(60, 300, salt=95)),
+                           (None, 0.5, fuzz.capacity_corpus(60, 300, salt=96)),
+                           (None, 0.3, fuzz.capacity_corpus(60, 300, salt=97))):
+        cfg = oracle.Config(gc_threshold=gc, **({"max_split_size": ms} if ms else {}))
+        for t in range(corpus.n_traces):
+            by, tg = corpus.trace(t)
+            cap = int(corpus.capacity[t])
+            rc, r, _ = _run(L, by, tg, cap, cfg)
+            bb, _ = bruteforce.simulate(by, tg, cap, msplit=ms, gc=gc)
+            if rc or any(r[k] != v for k, v in bb.items()):
+                return f"bruteforce msplit={ms} gc={gc} trace {t}"
+    return None
+
+
+@pytest.mark.parametrize("name,old,new", KNOB_MUTANTS, ids=[m[0] for m in KNOB_MUTANTS])
+def test_knob_mutant_rejected(name, old, new):
+    src = open(SRC).read()
+    assert src.count(old) >= 1, f"mutation site missing: {name}"
+    with tempfile.TemporaryDirectory() as d:
+        assert _knob_pins_reject(_build(src, d)) is None
+        L = _build(src.replace(old, new, 1), d + "/m")
+        assert _knob_pins_reject(L) is not None, f"pins did not catch mutant: {name}"
 
 
 # ---- NEXT-3 lifecycle oracle (oracle/lifecycle.c) -------------------------------
