@@ -112,6 +112,26 @@ typedef struct {
                                /* only until the request fits)                     */
   uint32_t host_input;         /* XM_HOST_INPUT_* (xm_simulate_host only);        */
                                /* default AUTO                                     */
+  uint32_t _pad0;
+  /* torch PYTORCH_CUDA_ALLOC_CONF knobs (NEXT-4; readings Q26, Q27;    */
+  /* PAPER.md:257 defers the allocator rules to PyTorch):                          */
+  uint64_t max_split_size;     /* max_split_size_mb:N = N MiB; XM_UNLIMITED (the   */
+                               /* default) = off. When set: a free block of at     */
+                               /* least this size is not handed to a smaller       */
+                               /* request, nor one of >= s + max_non_split_rounding*/
+                               /* to a request s >= it; such requests are never   */
+                               /* split; and before releasing every cached segment */
+                               /* (reading Q3) torch's release_available_cached_   */
+                               /* blocks runs. A multiple of min_block, > 0.       */
+  uint64_t max_non_split_rounding; /* max_non_split_rounding_mb (default 20 MiB)   */
+  double garbage_collection_threshold; /* in (0, 1): every free-block search that  */
+                               /* finds nothing first runs torch's garbage_collect_*/
+                               /* cached_blocks when reserved > threshold x the    */
+                               /* trace's capacity (finite capacities only; torch  */
+                               /* needs set_per_process_memory_fraction): whole    */
+                               /* large-pool cached segments at least as old as the*/
+                               /* mean age are released, pass after pass. 0 = off  */
+                               /* (default); XM_EINVAL outside [0, 1).             */
 } xm_config;
 
 /*

@@ -58,7 +58,10 @@ class _Cfg(ctypes.Structure):
                 ("capacity", ctypes.c_uint64), ("large_split_strict", ctypes.c_uint32),
                 ("mode", ctypes.c_uint32), ("smem_per_warp", ctypes.c_uint32),
                 ("warps_per_cta", ctypes.c_uint32), ("roundup_power2_divisions", ctypes.c_uint32),
-                ("reclaim_policy", ctypes.c_uint32), ("host_input", ctypes.c_uint32)]
+                ("reclaim_policy", ctypes.c_uint32), ("host_input", ctypes.c_uint32),
+                ("_pad0", ctypes.c_uint32), ("max_split_size", ctypes.c_uint64),
+                ("max_non_split_rounding", ctypes.c_uint64),
+                ("garbage_collection_threshold", ctypes.c_double)]
 
 
 class _Batch(ctypes.Structure):
@@ -138,12 +141,18 @@ class Config:
     roundup_power2_divisions: int = 0     # NEXT-4 variant: torch knob (0/1 = off)
     reclaim_policy: int = 0               # 0 torch release-all; 1 SPEC.md:283 D3
     host_input: int = 0                   # xm_simulate_host: 0 auto, 1 direct, 2 stream, 3 copy
+    _pad0: int = 0
+    max_split_size: int = UNLIMITED       # torch max_split_size_mb:N -> N << 20 (Q26); off
+    max_non_split_rounding: int = 20 << 20   # torch max_non_split_rounding_mb (Q26)
+    garbage_collection_threshold: float = 0.0    # torch knob (Q27); 0 = off
 
     def c(self) -> _Cfg:
         return _Cfg(self.min_block, self.small_size, self.small_buffer, self.large_buffer,
                     self.min_large_alloc, self.round_large, self.capacity,
                     self.large_split_strict, self.mode, self.smem_per_warp, self.warps_per_cta,
-                    self.roundup_power2_divisions, self.reclaim_policy, self.host_input)
+                    self.roundup_power2_divisions, self.reclaim_policy, self.host_input, 0,
+                    self.max_split_size, self.max_non_split_rounding,
+                    self.garbage_collection_threshold)
 
 
 _lib = None

@@ -61,6 +61,13 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
   if (c->reclaim_policy != XM_RECLAIM_ALL && c->reclaim_policy != XM_RECLAIM_LARGEST_FIRST)
     return set_error(XM_EINVAL, "xm_config: unknown reclaim_policy");
   if (c->host_input > XM_HOST_INPUT_COPY) return set_error(XM_EINVAL, "xm_config: unknown host_input");
+  if (c->max_split_size != XM_UNLIMITED &&
+      (c->max_split_size == 0 || c->max_split_size % m || c->max_split_size / m > 0x7FFFFFFFull))
+    return set_error(XM_EINVAL, "xm_config: max_split_size must be a non-zero multiple of min_block");
+  if (c->max_non_split_rounding % m || c->max_non_split_rounding / m > 0x7FFFFFFFull)
+    return set_error(XM_EINVAL, "xm_config: max_non_split_rounding must be a multiple of min_block");
+  if (!(c->garbage_collection_threshold >= 0.0 && c->garbage_collection_threshold < 1.0))
+    return set_error(XM_EINVAL, "xm_config: garbage_collection_threshold must be in [0, 1)");
   int sh = 0;
   while ((1ull << sh) < m) ++sh;
   u->unit_shift = uint32_t(sh);
@@ -73,6 +80,9 @@ int make_unit_config(const xm_config* c, UnitConfig* u) {
   u->div_shift = 0;
   while (dv > 1 && (1u << u->div_shift) < dv) ++u->div_shift;
   u->reclaim_d3 = c->reclaim_policy == XM_RECLAIM_LARGEST_FIRST ? 1u : 0u;
+  u->msplit_u = c->max_split_size == XM_UNLIMITED ? 0xFFFFFFFFu : uint32_t(c->max_split_size / m);
+  u->nsr_u = uint32_t(c->max_non_split_rounding / m);
+  u->gc_threshold = c->garbage_collection_threshold;
   return XM_OK;
 }
 
@@ -94,6 +104,9 @@ extern "C" void xm_config_default(xm_config* c) {
   c->capacity = XM_UNLIMITED;
   c->large_split_strict = 1;
   c->mode = XM_FULL;
+  c->max_split_size = XM_UNLIMITED;
+  c->max_non_split_rounding = 20ull << 20;
+  c->garbage_collection_threshold = 0.0;
 }
 
 extern "C" const char* xm_last_error(void) { return g_err.c_str(); }

@@ -186,13 +186,17 @@ struct State {
   uint32_t* F_key;           // Wide: key
   uint32_t* F_size;          // Wide: size (narrow: the key's low 27 bits)
   typename L::Link* F_lk;    // [2 * nf]
+  uint32_t* F_age;           // GC variant only (else null): the pool's search count
+                             // when the entry's block entered the free list
   uint32_t cap_f;
 };
 
 template <class L>
 __host__ __device__ inline size_t a_bytes(uint32_t na) { return size_t(na) * L::kABytes + 32; }
 template <class L>
-__host__ __device__ inline size_t f_bytes(uint32_t nf) { return size_t(nf) * L::kFBytes + 16; }
+__host__ __device__ inline size_t f_bytes(uint32_t nf, bool age = false) {
+  return size_t(nf) * (L::kFBytes + (age ? 4 : 0)) + 16;
+}
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -210,17 +214,18 @@ __device__ __forceinline__ void carve_a(State<L>& S, unsigned char* p, uint32_t 
 }
 
 template <class L>
-__device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t nf) {
+__device__ __forceinline__ void carve_f(State<L>& S, unsigned char* p, uint32_t nf, bool age) {
   using K = typename L::Link;
   if constexpr (L::kPacked) {
     S.F_kp = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
-    S.F_lk = reinterpret_cast<K*>(p);
+    S.F_lk = reinterpret_cast<K*>(p); p += size_t(nf) * 4;
   } else {
     S.F_pos = reinterpret_cast<uint64_t*>(p); p += size_t(nf) * 8;
     S.F_lk = reinterpret_cast<K*>(p); p += size_t(nf) * 8;
     S.F_key = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
-    S.F_size = reinterpret_cast<uint32_t*>(p);
+    S.F_size = reinterpret_cast<uint32_t*>(p); p += size_t(nf) * 4;
   }
+  S.F_age = age ? reinterpret_cast<uint32_t*>(p) : nullptr;
   S.cap_f = nf;
 }
 
@@ -504,7 +509,8 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   if (G.fstart == kNone32 || S.cap_f >= L::kCapMax) return false;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t ncap = min(S.cap_f * 2 + kScanBlock, L::kCapMax);
-  const uint32_t np = uint32_t((f_bytes<L>(ncap) + kPage - 1) / kPage);
+  const bool age = S.F_age != nullptr;
+  const uint32_t np = uint32_t((f_bytes<L>(ncap, age) + kPage - 1) / kPage);
   if (np > G.total) return false;
   // Bounded wait (~2 ms): running traces finish and free pages long before a
   // trace here could be restarted elsewhere; only when every resident trace is
@@ -518,8 +524,9 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   }
   if (st == kNone32) return false;
   State<L> T = S;
-  carve_f(T, G.pages + size_t(st) * kPage, ncap);
+  carve_f(T, G.pages + size_t(st) * kPage, ncap, age);
   for (uint32_t f = lane; f < nf; f += 32) {
+    if (age) T.F_age[f] = S.F_age[f];
     if constexpr (L::kPacked) {
       T.F_kp[f] = S.F_kp[f];
       reinterpret_cast<uint32_t*>(T.F_lk)[f] = reinterpret_cast<const uint32_t*>(S.F_lk)[f];
@@ -541,36 +548,39 @@ __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   return true;
 }
 
-// Reclamation (reading Q3; PAPER.md:259 (iv) "Cached blocks persist until the
-// framework allocator needs more memory, but the device indicates an OOM
-// error"): release every free block that spans a whole segment, in all pools
-// and streams. Warp-parallel stable compaction of the free list (lanes write
-// distinct entries; barriers separate the reads of each chunk from its writes).
-template <class L>
-__device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typename L::Acc& reserved,
-                                        uint32_t& n_release, uint32_t& live_segs) {
+// Warp-parallel stable compaction of the free list that drops every entry
+// `drop(key, size, prev, next, age)` selects (lanes write distinct entries;
+// barriers separate the reads of each chunk from its writes). Dropped entries
+// must be whole segments (no neighbours). Returns their count; *units and *ages
+// get their summed sizes and ages.
+template <class L, class Drop>
+__device__ __forceinline__ uint32_t drop_where(const State<L>& S, uint32_t& nf, Drop drop,
+                                               uint64_t* units, uint64_t* ages) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t newn = 0, cnt = 0;
-  uint64_t freed = 0;
+  uint64_t freed = 0, aged = 0;
   for (uint32_t base = 0; base < nf; base += 32) {
     const uint32_t f = base + lane;
     const bool valid = f < nf;
-    uint32_t k = 0, sz = 0, pv = L::kNone, nx = L::kNone;
+    uint32_t k = 0, sz = 0, pv = L::kNone, nx = L::kNone, ag = 0;
     uint64_t pos = 0;
     if (valid) {
       f_load(S, f, k, pos, sz);
       load_links<L>(S.F_lk, f, pv, nx);
+      if (S.F_age) ag = S.F_age[f];
     }
-    const bool whole = valid && pv == L::kNone && nx == L::kNone;
-    const bool keep = valid && !whole;
+    const bool gone = valid && drop(k, sz, pv, nx, ag);
+    const bool keep = valid && !gone;
     const unsigned km = __ballot_sync(kFull, keep);
-    const unsigned wm = __ballot_sync(kFull, whole);
-    const uint64_t fs = warp_sum_u64(whole ? uint64_t(sz) : 0ull);
+    const unsigned wm = __ballot_sync(kFull, gone);
+    const uint64_t fs = warp_sum_u64(gone ? uint64_t(sz) : 0ull);
+    const uint64_t fa = warp_sum_u64(gone ? uint64_t(ag) : 0ull);
     const uint32_t dst = newn + __popc(km & ((1u << lane) - 1u));
     __syncwarp();
     if (keep && dst != f) {
       f_store(S, dst, k, pos, sz);
       store_links<L>(S.F_lk, dst, pv, nx);
+      if (S.F_age) S.F_age[dst] = ag;
       set_next(S, pv, L::kF | dst);
       set_prev(S, nx, L::kF | dst);
     }
@@ -578,13 +588,179 @@ __device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typenam
     newn += __popc(km);
     cnt += __popc(wm);
     freed += fs;
+    aged += fa;
   }
   fill_sentinels(S, newn, nf);
   __syncwarp();
   nf = newn;
-  reserved -= typename L::Acc(freed);
+  *units = freed;
+  *ages = aged;
+  return cnt;
+}
+
+// Reclamation (reading Q3; PAPER.md:259 (iv) "Cached blocks persist until the
+// framework allocator needs more memory, but the device indicates an OOM
+// error"): release every free block that spans a whole segment, in all pools
+// and streams.
+template <class L>
+__device__ __forceinline__ void reclaim(const State<L>& S, uint32_t& nf, typename L::Acc& reserved,
+                                        uint32_t& n_release, uint32_t& live_segs) {
+  uint64_t units, ages;
+  const uint32_t cnt = drop_where(
+      S, nf, [](uint32_t, uint32_t, uint32_t pv, uint32_t nx, uint32_t) {
+        return pv == L::kNone && nx == L::kNone;
+      }, &units, &ages);
+  reserved -= typename L::Acc(units);
   n_release += cnt;
   live_segs -= cnt;
+}
+
+// Variant (NEXT-4, reading Q27; torch garbage_collect_cached_blocks): when
+// reserved exceeds the GC bar (threshold x capacity, in bytes), release the
+// LARGE-pool whole-segment free blocks at least as old as the mean age,
+// pass after pass, until the excess is gone or a pass releases nothing. Age =
+// large-pool searches since the entry entered the free list (F_age). The
+// mean is taken in double as torch does (double(total) / double(count)).
+template <class L>
+__device__ void gc_collect(const State<L>& S, uint32_t& nf, typename L::Acc& reserved,
+                           uint32_t& n_release, uint32_t& live_segs, uint32_t now,
+                           uint64_t bar_bytes, uint32_t shift) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t res_b = uint64_t(reserved) << shift;
+  if (res_b <= bar_bytes) return;
+  const uint64_t target = res_b - bar_bytes;
+  uint64_t tot = 0;
+  uint32_t cnt = 0;
+  for (uint32_t f = lane; f < nf; f += 32) {
+    uint32_t k, sz, pv, nx;
+    uint64_t pos;
+    f_load(S, f, k, pos, sz);
+    load_links<L>(S.F_lk, f, pv, nx);
+    if (!((k >> kKeyBits) & 1u) && pv == L::kNone && nx == L::kNone) {
+      tot += now - S.F_age[f];
+      ++cnt;
+    }
+  }
+  tot = warp_sum_u64(tot);
+  cnt = __reduce_add_sync(kFull, cnt);
+  uint64_t got = 0;
+  bool freed = true;
+  while (got < target && freed && cnt > 0) {
+    const double bar = double(tot) / double(cnt);
+    uint64_t units, ages;
+    const uint32_t nrel = drop_where(
+        S, nf, [now, bar](uint32_t k, uint32_t, uint32_t pv, uint32_t nx, uint32_t ag) {
+          return !((k >> kKeyBits) & 1u) && pv == L::kNone && nx == L::kNone &&
+                 double(now - ag) >= bar;
+        }, &units, &ages);
+    freed = nrel > 0;
+    got += units << shift;
+    tot -= uint64_t(nrel) * now - ages;          // sum of (now - age) over the dropped
+    cnt -= nrel;
+    reserved -= typename L::Acc(units);
+    n_release += nrel;
+    live_segs -= nrel;
+  }
+}
+
+// Warp arg-min (want_max: arg-max) of (size, addr) over the free entries of
+// class cls with size >= lo; kNone32 if none. Rare paths only.
+template <class L>
+__device__ uint32_t f_arg(const State<L>& S, uint32_t nf, uint32_t cls, uint32_t lo, bool want_max,
+                          uint32_t& bsz) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t best = kNone32, sz_b = 0;
+  uint64_t pos_b = 0;
+  for (uint32_t f = lane; f < nf; f += 32) {
+    uint32_t k, sz;
+    uint64_t pos;
+    f_load(S, f, k, pos, sz);
+    if ((k >> kKeyBits) != cls || sz < lo) continue;
+    const bool better = best == kNone32 ||
+        (want_max ? (sz > sz_b || (sz == sz_b && pos > pos_b)) : (sz < sz_b || (sz == sz_b && pos < pos_b)));
+    if (better) { best = f; sz_b = sz; pos_b = pos; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint32_t ob = __shfl_xor_sync(kFull, best, o);
+    const uint32_t os = __shfl_xor_sync(kFull, sz_b, o);
+    const uint64_t op = __shfl_xor_sync(kFull, pos_b, o);
+    const bool take = ob != kNone32 &&
+        (best == kNone32 || (want_max ? (os > sz_b || (os == sz_b && op > pos_b))
+                                      : (os < sz_b || (os == sz_b && op < pos_b))));
+    if (take) { best = ob; sz_b = os; pos_b = op; }
+  }
+  bsz = sz_b;
+  return best;
+}
+
+// Drop free entry fsel, a whole segment (the last entry moves into its slot).
+// False if it is not a whole segment (the caller reports XM_T_OVERFLOW).
+template <class L>
+__device__ bool release_entry(const State<L>& S, uint32_t& nf, uint32_t fsel) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t k0, s0, pv0, nx0;
+  uint64_t p0;
+  f_load(S, fsel, k0, p0, s0);
+  load_links<L>(S.F_lk, fsel, pv0, nx0);
+  if (pv0 != L::kNone || nx0 != L::kNone) return false;
+  const uint32_t Lx = nf - 1;
+  uint32_t lk = 0, lsz = 0, lpv = L::kNone, lnx = L::kNone, lag = 0;
+  uint64_t lpos = 0;
+  if (fsel != Lx) {
+    f_load(S, Lx, lk, lpos, lsz);
+    load_links<L>(S.F_lk, Lx, lpv, lnx);
+    if (S.F_age) lag = S.F_age[Lx];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (fsel != Lx) {
+      f_store(S, fsel, lk, lpos, lsz);
+      store_links<L>(S.F_lk, fsel, lpv, lnx);
+      if (S.F_age) S.F_age[fsel] = lag;
+      set_next(S, lpv, L::kF | fsel);
+      set_prev(S, lnx, L::kF | fsel);
+    }
+    if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
+  }
+  __syncwarp();
+  nf = Lx;
+  return true;
+}
+
+// Variant (NEXT-4, reading Q26; torch release_available_cached_blocks), with
+// max_split_size set, before release-all: key = max(s, max_split_size); in the
+// request's class (stream, pool) the smallest (size, addr) free block of size
+// >= key is released, else blocks of size >= max_split_size from the largest
+// (size, addr) down until >= key units are released. Returns 1 when torch
+// would retry the device (one block released, or >= key units), 0 when it goes
+// on to release-all, -1 on a non-whole block (never, as such blocks are not
+// split: XM_T_OVERFLOW).
+template <class L>
+__device__ int release_available(const State<L>& S, uint32_t& nf, typename L::Acc& reserved,
+                                 uint32_t& n_release, uint32_t& live_segs, uint32_t cls, uint32_t s,
+                                 uint32_t msplit) {
+  const uint32_t key = s < msplit ? msplit : s;
+  uint32_t sz;
+  uint32_t f = f_arg(S, nf, cls, key, false, sz);
+  if (f != kNone32) {
+    if (!release_entry(S, nf, f)) return -1;
+    reserved -= typename L::Acc(sz);
+    n_release += 1;
+    live_segs -= 1;
+    return 1;
+  }
+  uint64_t got = 0;
+  while (got < key) {
+    f = f_arg(S, nf, cls, 0, true, sz);
+    if (f == kNone32 || sz < msplit) break;
+    if (!release_entry(S, nf, f)) return -1;
+    got += sz;
+    reserved -= typename L::Acc(sz);
+    n_release += 1;
+    live_segs -= 1;
+  }
+  return got >= key ? 1 : 0;
 }
 
 // Variant (SPEC.md:283 D3): release fully-free segments one at a
@@ -620,17 +796,19 @@ __device__ __forceinline__ void reclaim_largest_first(State<L>& S, uint32_t& nf,
     const uint32_t fsel = __reduce_min_sync(kFull, (c1 && hi == mh && uint32_t(bpos) == ml) ? bf : kNone32);
     // load phase: the last entry (moved into fsel)
     const uint32_t Lx = nf - 1;
-    uint32_t lk = 0, lsz = 0, lpv = L::kNone, lnx = L::kNone;
+    uint32_t lk = 0, lsz = 0, lpv = L::kNone, lnx = L::kNone, lag = 0;
     uint64_t lpos = 0;
     if (fsel != Lx) {
       f_load(S, Lx, lk, lpos, lsz);
       load_links<L>(S.F_lk, Lx, lpv, lnx);
+      if (S.F_age) lag = S.F_age[Lx];
     }
     __syncwarp();
     if (lane == 0) {                                       // one lane writes
       if (fsel != Lx) {
         f_store(S, fsel, lk, lpos, lsz);
         store_links<L>(S.F_lk, fsel, lpv, lnx);
+        if (S.F_age) S.F_age[fsel] = lag;
         set_next(S, lpv, L::kF | fsel);
         set_prev(S, lnx, L::kF | fsel);
       }
@@ -683,9 +861,17 @@ __device__ __forceinline__ uint32_t best_fit_exact(const State<L>& S, uint32_t n
 // __syncwarp(): no lane stores before every lane has loaded, so a lagging
 // group can never read state this event already changed, and the barrier at
 // the end of the event orders the stores before the next event's loads.
-template <class L, bool kCurve>
+// kOpt bits: kOptCurve (NEXT-1 memory curve), kOptKnobs (torch's
+// max_split_size / garbage_collection_threshold, readings Q26/Q27). The default
+// instantiation (0) carries none of their instructions.
+constexpr int kOptCurve = 1, kOptKnobs = 2;
+
+template <class L, int kOpt>
 __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow& G, int64_t e0,
-                                            uint32_t n, uint64_t cap_u, xm_result& R) {
+                                            uint32_t n, uint64_t cap_u, xm_result& R,
+                                            bool gc_on, uint64_t gc_bar) {
+  constexpr bool kCurve = (kOpt & kOptCurve) != 0;
+  constexpr bool kKnobs = (kOpt & kOptKnobs) != 0;
   using Acc = typename L::Acc;
   constexpr uint32_t kNone = L::kNone, kF = L::kF;
   const uint32_t lane = threadIdx.x & 31;
@@ -715,6 +901,8 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   uint32_t ix_tensor = 0, ix_blk = 0, ix_res = 0;
   int status = kStatusOk;
   uint32_t done_total = 0;
+  uint32_t srch_large = 0, srch_small = 0;   // GC: free-block searches per pool (torch
+                                             // get_free_blocks_call_count)
 
   // events are loaded ahead of the replay: the packed form two tiles ahead
   // (raw words; the events may be read straight from host memory over PCIe,
@@ -869,20 +1057,43 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
             }
           }
         }
+        if constexpr (kKnobs) {
+          if (gc_on) { if (small) ++srch_small; else ++srch_large; }
+          // torch get_free_block: "Do not return an oversized block" (Q26)
+          if (fsel != kNone32 && u.msplit_u != 0xFFFFFFFFu) {
+            uint32_t bs;
+            if constexpr (L::kPacked) bs = fkey_sel & kKeyMax;
+            else bs = S.F_size[fsel];
+            if ((s < u.msplit_u && bs >= u.msplit_u) ||
+                (s >= u.msplit_u && uint64_t(bs) >= uint64_t(s) + u.nsr_u))
+              fsel = kNone32;
+          }
+        }
         // ---- load phase (plus the rare reclaim / growth, each self-contained) ----
         uint32_t bsize, bprev = kNone, bnext = kNone;
         uint64_t bposu;
         if (fsel == kNone32) {
+          if constexpr (kKnobs) {
+            if (gc_on) gc_collect(S, nf, reserved, n_release, live_segs, srch_large, gc_bar, u.unit_shift);
+          }
           // a4/a6: new segment from the device level (PAPER.md:259 (iv), 169, 654)
           uint32_t a;
           if (small) a = u.sbuf_u;
           else if (s < u.minlarge_u) a = u.lbuf_u;
           else a = uint32_t((uint64_t(s) + u.rlarge_u - 1) / u.rlarge_u * u.rlarge_u);
           if (uint64_t(reserved) + a > cap_u) {                // device level refuses (Q10)
-            if (u.reclaim_d3)                                  // SPEC D3 variant (NEXT-4)
+            if (u.reclaim_d3) {                                // SPEC D3 variant (NEXT-4)
               reclaim_largest_first(S, nf, reserved, n_release, live_segs, a, cap_u);
-            else
-              reclaim(S, nf, reserved, n_release, live_segs);  // reclaim cached segments (Q3)
+            } else {
+              int ra = 0;                                      // torch: release_available,
+              if constexpr (kKnobs) {                          // then release-all (Q26)
+                if (u.msplit_u != 0xFFFFFFFFu)
+                  ra = release_available(S, nf, reserved, n_release, live_segs, cls, s, u.msplit_u);
+              }
+              if (ra < 0) { status = kStatusOverflow; break; }
+              if (ra == 0 || uint64_t(reserved) + a > cap_u)
+                reclaim(S, nf, reserved, n_release, live_segs);  // reclaim cached segments (Q3)
+            }
             if (uint64_t(reserved) + a > cap_u) { status = kStatusOom; break; }  // both levels failed
           }
           // layout limits (address width, narrow sizes): restart WIDE
@@ -907,18 +1118,20 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         }
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
-        const bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
+        bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
+        if constexpr (kKnobs) split = split && (small || s < u.msplit_u);   // torch should_split (Q26)
         if (split && fsel == kNone32 && nf >= S.cap_f && !grow_f(S, G, nf)) {
           status = kStatusOverflow;
           break;
         }
         const bool remove = !split && fsel != kNone32;  // the whole free block is taken
         const uint32_t Lx = nf - 1;
-        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
+        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone, lag = 0;
         uint64_t lpos = 0;
         if (remove && fsel != Lx) {
           f_load(S, Lx, lk, lpos, lsz);
           load_links<L>(S.F_lk, Lx, lpv, lnx);
+          if (kKnobs && S.F_age) lag = S.F_age[Lx];
         }
         __syncwarp();
         // ---- store phase (every lane stores the same values; no location is
@@ -930,6 +1143,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           if (fsel == kNone32) r = nf++;               // new segment: no right neighbour
           f_store(S, r, make_key(cls, rem), bposu + s, rem);
           store_links<L>(S.F_lk, r, id, bnext);
+          if (kKnobs && S.F_age) S.F_age[r] = small ? srch_small : srch_large;   // enters now
           asize = s;
           bnext = kF | r;
         } else {
@@ -938,6 +1152,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
             if (fsel != Lx) {
               f_store(S, fsel, lk, lpos, lsz);
               store_links<L>(S.F_lk, fsel, lpv, lnx);
+              if (kKnobs && S.F_age) S.F_age[fsel] = lag;
               set_next(S, lpv, kF | fsel);
               set_prev(S, lnx, kF | fsel);
             }
@@ -976,12 +1191,15 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
           break;
         }
         const uint32_t Lx = nf - 1;                      // for removing N_ (both free)
-        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone;
+        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone, lag = 0;
         uint64_t lpos = 0;
         if (pf && qf && N_ != Lx) {
           f_load(S, Lx, lk, lpos, lsz);
           load_links<L>(S.F_lk, Lx, lpv, lnx);
+          if (kKnobs && S.F_age) lag = S.F_age[Lx];
         }
+        // GC age: the merged / new free block enters the free list now
+        const uint32_t now_age = (acls & 1u) ? srch_small : srch_large;
         __syncwarp();
         // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
         // (PAPER.md:259 (iv)) ----
@@ -995,18 +1213,21 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
             // two values to one location in one event)
             f_store(S, N_, nk, ppos, nsz);
             store_links<L>(S.F_lk, N_, lpv, nn);
+            if (kKnobs && S.F_age) S.F_age[N_] = now_age;
             set_next(S, lpv, kF | N_);
             set_prev(S, nn, kF | N_);
             if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
             nf = Lx;
           } else {
             f_store(S, P_, nk, ppos, nsz);
+            if (kKnobs && S.F_age) S.F_age[P_] = now_age;
             set_next(S, p, nn);
             set_prev(S, nn, p);
             if (qf) {                                 // drop N_: move the last entry there
               if (N_ != Lx) {
                 f_store(S, N_, lk, lpos, lsz);
                 store_links<L>(S.F_lk, N_, lpv, lnx);
+                if (kKnobs && S.F_age) S.F_age[N_] = lag;
                 set_next(S, lpv, kF | N_);
                 set_prev(S, lnx, kF | N_);
               }
@@ -1017,12 +1238,14 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         } else if (qf) {
           const uint32_t nsz = nsz0 + sz;
           f_store(S, N_, make_key(acls, nsz), apos, nsz);
+          if (kKnobs && S.F_age) S.F_age[N_] = now_age;
           set_prev(S, q, p);
           set_next(S, p, q);
         } else {
           const uint32_t r = nf++;
           f_store(S, r, make_key(acls, sz), apos, sz);
           store_links<L>(S.F_lk, r, p, q);
+          if (kKnobs && S.F_age) S.F_age[r] = now_age;
           set_next(S, p, kF | r);
           set_prev(S, q, kF | r);
         }
@@ -1084,6 +1307,10 @@ __device__ void wait_ready(const uint32_t* ready, uint32_t k) {
   __syncwarp();
 }
 
+// kKnobs: the torch-knob variants (max_split_size / garbage_collection_threshold,
+// readings Q26/Q27) are a separate kernel, so the default one carries none of
+// their code or registers.
+template <bool kKnobs>
 __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   HeapHdr* hdr = reinterpret_cast<HeapHdr*>(smem);
@@ -1127,18 +1354,23 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     // shared memory, NARROW layout: A region + an initial free list
     const uint32_t npa = uint32_t((a_bytes<Narrow>(na) + kPage - 1) / kPage);
     const uint32_t nfc = min(round_scan(min(nf_exact, na / XM_F_INIT_DIV + 64)), Narrow::kCapMax);
-    const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc) + kPage - 1) / kPage);
+    const bool ages = kKnobs && P.u.gc_threshold > 0.0;   // F_age only when GC is configured
+    // GC acts only with a finite capacity (torch: set_per_process_memory_fraction)
+    const bool gc_on = ages && cap != ~0ull;
+    const uint64_t gc_bar = gc_on ? uint64_t(P.u.gc_threshold * double(cap)) : 0ull;
+    const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc, ages) + kPage - 1) / kPage);
     if (na <= Narrow::kMaxIdx && npa + npf <= P.heap_pages) {
       const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);
       ticket_release(hdr);
       State<Narrow> S;
       carve_a(S, pages + size_t(start) * kPage, na);
-      carve_f(S, pages + size_t(start + npa) * kPage, nfc);
+      carve_f(S, pages + size_t(start + npa) * kPage, nfc, ages);
       fill_sentinels(S, 0, nfc);
       __syncwarp();
       Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
-      st = P.curve ? replay_trace<Narrow, true>(P, S, G, e0, n, cap_u, R)
-                   : replay_trace<Narrow, false>(P, S, G, e0, n, cap_u, R);
+      constexpr int kO = kKnobs ? kOptKnobs : 0;
+      st = P.curve ? replay_trace<Narrow, kO | kOptCurve>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar)
+                   : replay_trace<Narrow, kO>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar);
       heap_free(hdr, start, npa);                  // A pages
       heap_free(hdr, G.fstart, G.fnp);             // current F pages (maybe moved)
       if (st == kStatusOverflow && lane == 0) atomicAdd(stats, 1u);
@@ -1154,10 +1386,11 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       unsigned char* base = P.arena + size_t(slot) * P.arena_bytes;
       State<Wide> S;
       carve_a(S, base, na);
-      carve_f(S, base + align16(a_bytes<Wide>(P.arena_ids)), nf_exact);
+      carve_f(S, base + align16(a_bytes<Wide>(P.arena_ids)), nf_exact, ages);
       Grow G{hdr, pages, P.heap_pages, kNone32, 0, stats};
-      st = P.curve ? replay_trace<Wide, true>(P, S, G, e0, n, cap_u, R)
-                   : replay_trace<Wide, false>(P, S, G, e0, n, cap_u, R);
+      constexpr int kO = kKnobs ? kOptKnobs : 0;
+      st = P.curve ? replay_trace<Wide, kO | kOptCurve>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar)
+                   : replay_trace<Wide, kO>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar);
       __syncwarp();
       __threadfence();
       if (lane == 0) atomicAnd(P.counter + 1 + (slot >> 5), ~(1u << (slot & 31)));
@@ -1199,7 +1432,7 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   // state cannot live in shared memory
   p.arena_ids = b->max_ids;
   p.arena_free = b->max_events + 1;
-  p.arena_per_warp = (align16(a_bytes<Wide>(p.arena_ids)) + f_bytes<Wide>(p.arena_free) + 255) & ~size_t(255);
+  p.arena_per_warp = (align16(a_bytes<Wide>(p.arena_ids)) + f_bytes<Wide>(p.arena_free, true) + 255) & ~size_t(255);
   // Slots: at most one per warp and 64, and within a byte budget
   // (XM_ARENA_BUDGET, default 4 GiB): every slot is sized for the batch's
   // longest trace, so one very long trace must not make the scratch
@@ -1249,9 +1482,11 @@ int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
   cudaError_t e = cudaMemsetAsync(d_scratch, 0, 256, st);
   if (e != cudaSuccess) return int(e);
   const size_t smem = kHdrBytes + size_t(plan.heap_pages) * kPage;
-  e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const bool knobs = u.msplit_u != 0xFFFFFFFFu || u.gc_threshold > 0.0;
+  auto kern = knobs ? k_replay<true> : k_replay<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return int(e);
-  k_replay<<<plan.ctas, plan.warps_per_cta * 32, smem, st>>>(P);
+  kern<<<plan.ctas, plan.warps_per_cta * 32, smem, st>>>(P);
   *n_launches += 1;
   return int(cudaGetLastError());
 }

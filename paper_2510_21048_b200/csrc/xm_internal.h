@@ -40,6 +40,9 @@ struct UnitConfig {
   uint32_t strict;       // large split iff rem > small (1) or >= (0)
   uint32_t div_shift;    // log2(roundup_power2_divisions), 0 = off (NEXT-4 variant)
   uint32_t reclaim_d3;   // 1: SPEC D3 largest-first reclamation (NEXT-4 variant)
+  uint32_t msplit_u;     // torch max_split_size / min_block; 0xFFFFFFFF = off (Q26)
+  uint32_t nsr_u;        // torch max_non_split_rounding / min_block (Q26)
+  double gc_threshold;   // torch garbage_collection_threshold; 0 = off (Q27)
 };
 
 // Launch geometry + scratch layout of the replay kernel for one batch.

@@ -21,11 +21,13 @@ def gpu_run(batch, cfg=None, capacity=True):
     return h, summ
 
 
-def oracle_run(batch, strict=1, parallel=False, div=0, reclaim=0):
+def oracle_run(batch, strict=1, parallel=False, div=0, reclaim=0, msplit=None, gc=0.0):
     ocfg = oracle.Config(large_split_strict=strict, roundup_power2_divisions=div,
-                         reclaim_policy=reclaim)
+                         reclaim_policy=reclaim, gc_threshold=gc,
+                         **({"max_split_size": msplit} if msplit is not None else {}))
     if parallel:
-        return oracle.simulate_batch_parallel(batch, ocfg)
+        import oracle_pool
+        return oracle_pool.run(batch, ocfg)
     return oracle.simulate_batch(batch, ocfg)
 
 

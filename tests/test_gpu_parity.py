@@ -333,12 +333,62 @@ def test_variant_d3_largest_first_reclaim(golden):
     assert_parity(b, h3, o)
 
 
+# ---- NEXT-4: torch max_split_size_mb / garbage_collection_threshold (Q26, Q27) ----
+def _knob_corpus():
+    import test_oracle_variants as V
+    M = 1 << 20
+    hands = [V._one(lambda t: t.alloc(0, 100 * M).free(0).alloc(1, 90 * M).free(1).alloc(2, 30 * M)
+                    .alloc(3, 70 * M), oracle.UNLIMITED),
+             V._one(lambda t: t.alloc(0, 100 * M).alloc(1, 30 * M).alloc(2, M).free(0).free(1)
+                    .free(2).alloc(3, 70 * M), 180 * M),
+             V._one(lambda t: t.alloc(0, 66 * M).alloc(1, 70 * M).alloc(2, 30 * M).free(0).free(1)
+                    .free(2).alloc(3, 120 * M), 200 * M),
+             V._one(lambda t: t.alloc(0, 200 * M).alloc(1, 150 * M).alloc(2, 120 * M).alloc(3, 60 * M)
+                    .free(0).free(2).alloc(4, 110 * M).free(4).alloc(5, 100 * M).free(5)
+                    .alloc(6, 300 * M), 1000 * M)]
+    from workloads.trace import from_arrays
+    caps = [oracle.UNLIMITED, 180 * M, 200 * M, 1000 * M]
+    return concat([from_arrays(by, tg, c) for (by, tg), c in zip(hands, caps)]
+                  + [fuzz.spec1_corpus(300, 800, salt=110), fuzz.capacity_corpus(400, 800, salt=111),
+                     fuzz.small_size_corpus(100, 500, salt=112), suites.config3().subset([0, 30])])
+
+
+@pytest.mark.parametrize("msplit,gc", [(21 << 20, 0.0), (32 << 20, 0.0), (64 << 20, 0.0),
+                                       (None, 0.3), (None, 0.6), (None, 0.9), (24 << 20, 0.5)])
+def test_variant_torch_knobs(msplit, gc):
+    b = _knob_corpus()
+    cfg = xm.Config(garbage_collection_threshold=gc,
+                    **({"max_split_size": msplit} if msplit is not None else {}))
+    h, _ = gpu_run(b, cfg)
+    o = oracle_run(b, msplit=msplit, gc=gc)
+    assert_parity(b, h, o)
+    # the knobs change the replay on this corpus (not a vacuous comparison)
+    assert (o["peak_reserved"] != oracle_run(b)["peak_reserved"]).any()
+    # the global-arena (wide) layout and free-list growth take the same paths
+    h2, _ = gpu_run(b, xm.Config(smem_per_warp=4096, warps_per_cta=1, garbage_collection_threshold=gc,
+                                 **({"max_split_size": msplit} if msplit is not None else {})))
+    assert_parity(b, h2, o)
+
+
+def test_variant_torch_knobs_config4():
+    """Both knobs on the full config-4 suite (its Monte-Carlo half has finite
+    capacities, so GC and release_available fire on realistic traces)."""
+    b = suites.config4()
+    cfg = xm.Config(max_split_size=64 << 20, garbage_collection_threshold=0.6)
+    h, _ = gpu_run(b, cfg)
+    assert_parity(b, h, oracle_run(b, parallel=True, msplit=64 << 20, gc=0.6))
+
+
 def test_variant_config_validation():
     b = hand.h7()
     with pytest.raises(xm.XMemError):
         gpu_run(b, xm.Config(roundup_power2_divisions=3))
     with pytest.raises(xm.XMemError):
         gpu_run(b, xm.Config(reclaim_policy=7))
+    with pytest.raises(xm.XMemError):
+        gpu_run(b, xm.Config(garbage_collection_threshold=1.0))
+    with pytest.raises(xm.XMemError):
+        gpu_run(b, xm.Config(max_split_size=1000))
 
 
 def test_packed_event_format():

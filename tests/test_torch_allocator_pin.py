@@ -32,15 +32,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 MiB = 1 << 20
 
 
-def torch_replay_batch(batch, full=False, conf=""):
+def torch_replay_batch(batch, full=False, conf="", segments=False):
     """All traces of a workloads.Batch in one fresh process (cache emptied between).
     Returns per-trace stats (and, if full, the per-event curve and pointers)."""
     with tempfile.TemporaryDirectory() as d:
         p, q = os.path.join(d, "t.npz"), os.path.join(d, "o.npz")
         np.savez(p, bytes=batch.bytes, tag=batch.tag, off=batch.off, capacity=batch.capacity)
+        env = dict(os.environ, XM_PIN_SEGMENTS="1") if segments else None
         r = subprocess.run([sys.executable, os.path.join(HERE, "torch_replay.py"), p, q]
                            + ([conf] if conf else []),
-                           capture_output=True, text=True, timeout=900)
+                           capture_output=True, text=True, timeout=900, env=env)
         assert r.returncode == 0, r.stderr[-2000:]
         o = np.load(q)
         stats = json.loads(str(o["stats"]))
@@ -202,3 +203,79 @@ def test_roundup_power2_divisions_training_traces_given_torch_addresses():
         bc = np.asarray(bc, np.int64)
         assert (bc[:, 2] == res).all(), (b.names[t], "reserved curve")
         assert (bc[:, 1] == curve[a:z, 0]).all(), (b.names[t], "allocated curve")
+
+
+# ---- NEXT-4: max_split_size_mb / garbage_collection_threshold (readings Q26, Q27) ----
+def _knob_hands():
+    import test_oracle_variants as V
+    from workloads.trace import from_arrays
+    M = MiB
+    cases = [  # H9, H10, H11 (walk succeeds / falls through), H12 -- tests/test_oracle_variants.py
+        (lambda t: t.alloc(0, 100 * M).free(0).alloc(1, 90 * M).free(1).alloc(2, 30 * M)
+         .alloc(3, 70 * M), 4096 * M),
+        (lambda t: t.alloc(0, 100 * M).alloc(1, 30 * M).alloc(2, M).free(0).free(1).free(2)
+         .alloc(3, 70 * M), 180 * M),
+        (lambda t: t.alloc(0, 66 * M).alloc(1, 70 * M).alloc(2, 30 * M).free(0).free(1).free(2)
+         .alloc(3, 120 * M), 200 * M),
+        (lambda t: t.alloc(0, 66 * M).alloc(1, 70 * M).alloc(2, 30 * M).free(0).free(1).free(2)
+         .alloc(3, 150 * M), 200 * M),
+        (lambda t: t.alloc(0, 200 * M).alloc(1, 150 * M).alloc(2, 120 * M).alloc(3, 60 * M).free(0)
+         .free(2).alloc(4, 110 * M).free(4).alloc(5, 100 * M).free(5).alloc(6, 300 * M), 1000 * M),
+    ]
+    return concat([from_arrays(*V._one(ev, cap), cap) for ev, cap in cases])
+
+
+KNOB_FIELDS = FIELDS + ["n_seg_release", "final_reserved"]
+
+
+@pytest.mark.parametrize("conf,msplit,gc", [("max_split_size_mb:64", 64 * MiB, 0.0),
+                                            ("garbage_collection_threshold:0.5", None, 0.5),
+                                            ("max_split_size_mb:64,garbage_collection_threshold:0.5",
+                                             64 * MiB, 0.5)])
+def test_torch_knobs_hand_traces_match_real_torch(conf, msplit, gc):
+    """H9-H12 under the real allocator with PYTORCH_CUDA_ALLOC_CONF set; the
+    model's capacity is torch's own allowed_memory_maximum for the fraction."""
+    b = _knob_hands()
+    reals = torch_replay_batch(b, conf=conf)
+    b.capacity = np.array([r["allowed"] for r in reals], np.uint64)
+    kw = {"max_split_size": msplit} if msplit else {}
+    o = oracle.simulate_batch(b, oracle.Config(gc_threshold=gc, **kw))
+    tr = xm.load_traces(b.bytes, b.tag, b.off)
+    g, _ = xm.peaks(xm.simulate_batch(tr.to_device(capacity=b.capacity),
+                                      xm.Config(garbage_collection_threshold=gc, **kw)))
+    for t in range(b.n_traces):
+        for f in KNOB_FIELDS:
+            assert int(o[f][t]) == reals[t][f], (conf, t, f, int(o[f][t]), reals[t][f])
+            assert int(g[f][t]) == reals[t][f], (conf, t, f)
+
+
+@pytest.mark.parametrize("conf,msplit,gc", [("max_split_size_mb:24", 24 * MiB, 0.0),
+                                            ("garbage_collection_threshold:0.6", None, 0.6)])
+def test_torch_knobs_fuzz_traces_given_torch_addresses(conf, msplit, gc):
+    """Random capacity-limited traces under the real allocator: given torch's
+    own segment addresses, the independent gap model (tests/bruteforce.py, the
+    model that pins the oracle) reproduces torch's per-event reserved and
+    allocated curves exactly."""
+    import bruteforce
+    c = fuzz.capacity_corpus(40, 300, salt=113)
+    c.capacity = np.maximum(c.capacity, np.uint64(64 * MiB))     # above the CUDA context's floor
+    stats, curve, ptr = torch_replay_batch(c, full=True, conf=conf, segments=True)
+    n_diff = 0
+    for t in range(c.n_traces):
+        a, z = int(c.off[t]), int(c.off[t + 1])
+        by, tg = c.bytes[a:z], c.tag[a:z]
+        res = curve[a:z, 1]
+        n = stats[t]["fail_idx"] if stats[t]["fail_idx"] >= 0 else z - a
+        nseg = curve[a:z, 2]
+        grew = [i for i in range(n) if nseg[i] > (nseg[i - 1] if i else 0)]
+        bases = [int(ptr[a + i]) for i in grew]
+        bo, bc = bruteforce.simulate(by, tg, stats[t]["allowed"], bases=bases, msplit=msplit, gc=gc)
+        bc = np.asarray(bc, np.int64)
+        assert bo["events_done"] == n, (t, bo["events_done"], n)
+        assert (bc[:n, 2] == res[:n]).all(), (t, "reserved curve")
+        assert (bc[:n, 1] == curve[a:a + n, 0]).all(), (t, "allocated curve")
+        # the model's own (bump-address) replay differs from torch only through ties
+        o, _ = oracle.simulate_trace(by, tg, stats[t]["allowed"], cfg=oracle.Config(
+            gc_threshold=gc, **({"max_split_size": msplit} if msplit else {})))
+        n_diff += o["peak_reserved"] != stats[t]["peak_reserved"]
+    assert n_diff <= c.n_traces // 10, f"{n_diff}/{c.n_traces} traces differ from torch by ties"

@@ -10,7 +10,8 @@ tests/test_torch_allocator_pin.py.
 usage: torch_replay.py IN.npz OUT.npz [ALLOC_CONF]   (IN: bytes, tag, off, capacity)
 ALLOC_CONF: optional PYTORCH_CUDA_ALLOC_CONF for the replay (allocator variants).
 OUT: stats (JSON string, one dict per trace), and per event: allocated bytes,
-reserved bytes and the returned device pointer (0 for frees).
+reserved bytes (+ with XM_PIN_SEGMENTS=1 the segments obtained so far) and the
+returned device pointer (0 for frees).
 """
 import json
 import os
@@ -21,11 +22,14 @@ import numpy as np
 
 def replay_one(torch, by, tg, cap, curve, ptr):
     dev = torch.device("cuda", 0)
-    total = torch.cuda.get_device_properties(0).total_memory
-    torch.cuda.set_per_process_memory_fraction(min(1.0, cap / total), 0)
+    total = torch.cuda.mem_get_info(0)[1]            # cudaMemGetInfo, as torch's setMemoryFraction
+    frac = min(1.0, cap / total)
+    torch.cuda.set_per_process_memory_fraction(frac, 0)
+    allowed = int(frac * float(total))               # static_cast<size_t>(fraction * double(total))
     torch.cuda.empty_cache()
     torch.cuda.reset_peak_memory_stats(0)
     base = torch.cuda.memory_stats(0)
+    seg0 = base.get("segment.all.allocated", 0)
     streams = {0: torch.cuda.current_stream(0)}
     live = {}
     fail = -1
@@ -49,6 +53,8 @@ def replay_one(torch, by, tg, cap, curve, ptr):
             del live[bid]
         curve[i, 0] = torch.cuda.memory_allocated(0)
         curve[i, 1] = torch.cuda.memory_reserved(0)
+        if curve.shape[1] > 2:        # segments obtained so far (new segment at i: it grew)
+            curve[i, 2] = torch.cuda.memory_stats(0)["segment.all.allocated"] - seg0
     s = torch.cuda.memory_stats(0)
     out = {
         "peak_allocated_blk": s["allocated_bytes.all.peak"],
@@ -59,6 +65,7 @@ def replay_one(torch, by, tg, cap, curve, ptr):
         "max_live_segments": s["segment.all.peak"],
         "fail_idx": fail,
         "num_ooms": s.get("num_ooms", 0) - base.get("num_ooms", 0),
+        "allowed": allowed,
     }
     live.clear()
     return out
@@ -73,7 +80,7 @@ def main(inp, outp, conf=""):
     d = np.load(inp)
     off, cap = d["off"], d["capacity"]
     E = int(off[-1])
-    curve = np.zeros((E, 2), np.int64)
+    curve = np.zeros((E, 3 if os.environ.get("XM_PIN_SEGMENTS") else 2), np.int64)
     ptr = np.zeros(E, np.int64)
     res = []
     for t in range(len(off) - 1):
