@@ -308,6 +308,30 @@ int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_con
                      void* d_ws, size_t ws_bytes, xm_result* h_out, void* stream);
 
 /*
+ * End-to-end from the caller's RAW host arrays, validated on the device: the
+ * xm_load_traces contract (same inputs: bytes[n_events], tag[n_events] = any
+ * 28-bit block id | stream << 28, off[n_traces+1]; same checks: zero or
+ * >= 2^40 request S:231, alloc of a live id S:249, free of a non-live id or
+ * with another size S:258; a free replays on its block's alloc stream) and
+ * xm_simulate_host's results, without the host loader: the events go to the
+ * device as they are (read in place over PCIe when page-locked, else copied
+ * into d_ws), K5's matching kernel keyed by the raw block id (one open block
+ * per id in a valid trace) validates every trace and renumbers its ids
+ * densely while writing the wire arrays longest first, and k_replay replays
+ * them. Synchronous; h_out[n_traces] HOST, caller order.
+ *   capacity: HOST [n_traces] or NULL (cfg->capacity).  d_ws: DEVICE,
+ *   >= xm_raw_ws_bytes(off, n_traces, cfg) (~52 B per event).
+ * Errors: XM_EINVAL / XM_ERANGE with *bad_trace = the first invalid caller
+ * trace (its results, and those of every other trace, are still written but
+ * meaningless for it); XM_ENOMEM; XM_ECUDA. XM_FULL mode only. Traces longer
+ * than 2^31-1 events: XM_ERANGE.
+ */
+size_t xm_raw_ws_bytes(const int64_t* off, int64_t n_traces, const xm_config* cfg);
+int xm_simulate_raw(const int64_t* bytes, const uint32_t* tag, const int64_t* off, int64_t n_traces,
+                    const uint64_t* capacity, const xm_config* cfg, void* d_ws, size_t ws_bytes,
+                    xm_result* h_out, int64_t* bad_trace, void* stream);
+
+/*
  * Config-5 support (kernel K4; input generation, not part of
  * the allocator model): expand Monte Carlo traces from templates ON THE DEVICE
  * so that a paper-scale batch (1M traces) never crosses PCIe.
@@ -408,7 +432,7 @@ typedef struct {
   uint32_t max_events;      /* longest trace (host value; sizes the scratch)               */
 } xm_instants;
 
-typedef struct {            /* per trace, 56 bytes                                         */
+typedef struct {            /* per trace, 64 bytes                                         */
   uint64_t n_blocks;        /* allocations                                                 */
   uint64_t n_orphan;        /* frees with no open block at their address                   */
   uint64_t n_mismatch;      /* matched frees whose |bytes| differs from the block's size   */
@@ -418,6 +442,9 @@ typedef struct {            /* per trace, 56 bytes                              
   uint32_t max_open;        /* most blocks open at once                                    */
   uint32_t n_ids;           /* dense id space of the wire trace (<= max_open + 31); the    */
                             /* replay needs <= 2^27 (xm_batch tag bits 0-26)               */
+  uint64_t n_reopened;      /* allocations at an address whose block is still open (a     */
+                            /* lost free in a profile; an invalid trace for the device     */
+                            /* loader of xm_simulate_raw)                     */
 } xm_lifecycle;
 
 size_t xm_reconstruct_scratch_bytes(const xm_instants* in);

@@ -29,7 +29,7 @@ import numpy as np
 from . import _build
 
 __all__ = ["Config", "Traces", "DeviceBatch", "load_traces", "simulate_batch", "peaks",
-           "simulate_host", "Templates", "expand_templates", "lib", "XMemError", "RESULT_DTYPE", "FIELDS", "UNLIMITED"]
+           "simulate_host", "simulate_raw", "Templates", "expand_templates", "lib", "XMemError", "RESULT_DTYPE", "FIELDS", "UNLIMITED"]
 
 UNLIMITED = 0xFFFFFFFFFFFFFFFF
 XM_FULL, XM_ALLOCATED_ONLY = 0, 1
@@ -99,11 +99,11 @@ class _Instants(ctypes.Structure):
                 ("max_events", ctypes.c_uint32)]
 
 
-# xm_lifecycle (include/xmem.h): per-trace reconstruction tallies, 56 B
+# xm_lifecycle (include/xmem.h): per-trace reconstruction tallies, 64 B
 LIFECYCLE_DTYPE = np.dtype([("n_blocks", "<u8"), ("n_orphan", "<u8"), ("n_mismatch", "<u8"),
                             ("n_persistent", "<u8"), ("n_kept", "<u8"), ("n_invalid", "<u8"),
-                            ("max_open", "<u4"), ("n_ids", "<u4")])
-assert LIFECYCLE_DTYPE.itemsize == 56
+                            ("max_open", "<u4"), ("n_ids", "<u4"), ("n_reopened", "<u8")])
+assert LIFECYCLE_DTYPE.itemsize == 64
 
 
 class _Profiles(ctypes.Structure):
@@ -183,6 +183,10 @@ def lib():
         L.xm_host_ws_bytes.argtypes = [P, ctypes.POINTER(_Cfg)]
         L.xm_host_ws_bytes.restype = ctypes.c_size_t
         L.xm_simulate_host.argtypes = [P, P, ctypes.POINTER(_Cfg), P, ctypes.c_size_t, P, P]
+        L.xm_raw_ws_bytes.argtypes = [P, ctypes.c_int64, ctypes.POINTER(_Cfg)]
+        L.xm_raw_ws_bytes.restype = ctypes.c_size_t
+        L.xm_simulate_raw.argtypes = [P, P, P, ctypes.c_int64, P, ctypes.POINTER(_Cfg), P,
+                                      ctypes.c_size_t, P, ctypes.POINTER(ctypes.c_int64), P]
         L.xm_metrics_scratch_bytes.argtypes = [I64]
         L.xm_metrics_scratch_bytes.restype = ctypes.c_size_t
         L.xm_metrics_batch.argtypes = [P, I64, P, ctypes.c_size_t, ctypes.POINTER(_Metrics), P]
@@ -394,6 +398,39 @@ def simulate_host(tr: Traces, cfg: Config = Config(), capacity: Optional[np.ndar
     return h, workspace
 
 
+def simulate_raw(bytes_: np.ndarray, tag: np.ndarray, off: np.ndarray, cfg: Config = Config(),
+                 capacity: Optional[np.ndarray] = None, stream=None, workspace=None):
+    """xm_simulate_raw: the caller's raw host arrays (xm_load_traces' contract)
+    validated, renumbered and replayed on the device; results (numpy
+    RESULT_DTYPE, caller order) and the workspace for reuse. Page-locked
+    arrays (e.g. numpy views of pinned torch tensors) are read in place.
+    Raises XMemError (with .bad_trace) on an invalid trace."""
+    import torch
+    by = np.ascontiguousarray(bytes_, np.int64)
+    tg = np.ascontiguousarray(tag, np.uint32)
+    of = np.ascontiguousarray(off, np.int64)
+    T = len(of) - 1
+    c = cfg.c()
+    need = int(lib().xm_raw_ws_bytes(_np_ptr(of), T, ctypes.byref(c)))
+    if need == 0:
+        _check(-1, "xm_raw_ws_bytes")
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device="cuda")
+    h = np.zeros(T, RESULT_DTYPE)
+    cap = None if capacity is None else np.ascontiguousarray(capacity, np.uint64)
+    bad = ctypes.c_int64(-1)
+    rc = lib().xm_simulate_raw(_np_ptr(by), _np_ptr(tg), _np_ptr(of), T,
+                               _np_ptr(cap) if cap is not None else None, ctypes.byref(c),
+                               ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _np_ptr(h),
+                               ctypes.byref(bad), _stream_ptr(stream))
+    if rc != 0:
+        msg = lib().xm_last_error().decode(errors="replace")
+        err = XMemError(f"xm_simulate_raw failed ({rc}): {msg}")
+        err.bad_trace = bad.value
+        raise err
+    return h, workspace
+
+
 def as_dict(h: np.ndarray) -> Dict[str, np.ndarray]:
     return {k: h[k].astype(np.uint64) for k in FIELDS}
 
@@ -550,7 +587,7 @@ def reconstruct(ins: DeviceInstants, wire: bool = True, stream=None, scratch=Non
     E, T = ins.n_events, ins.n_traces
     partner = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     mism = torch.empty(max(E, 1), dtype=torch.uint8, device=dev)
-    rec = torch.empty((max(T, 1), 56), dtype=torch.uint8, device=dev)
+    rec = torch.empty((max(T, 1), LIFECYCLE_DTYPE.itemsize), dtype=torch.uint8, device=dev)
     wb = wt = wo = wn = None
     if wire:
         wb = torch.empty(max(E, 1), dtype=torch.int64, device=dev)

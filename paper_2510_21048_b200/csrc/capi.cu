@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "xm_internal.h"
 
@@ -412,4 +413,162 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
   }
   if (rc) return rc;
   return xm_peaks(d_out, I.n_traces, h_out, nullptr, XM_UNLIMITED, stream);
+}
+
+// ---- raw host traces -> device loader -> replay (xm_simulate_raw) -----------------
+namespace {
+struct RawLayout {
+  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, scratch, total;
+};
+
+struct RawShape {
+  int64_t T, E;
+  uint32_t max_events, max_ids;
+};
+
+RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
+  RawLayout L{};
+  size_t p = 0;
+  const size_t E = size_t(R.E > 0 ? R.E : 1), T = size_t(R.T > 0 ? R.T : 1);
+  L.bytes = p; p += al(8 * E);
+  L.tag = p; p += al(4 * E);
+  L.off = p; p += al(8 * (T + 1));
+  L.order = p; p += al(4 * T);
+  L.cap = p; p += al(8 * T);
+  L.rec = p; p += al(sizeof(xm_lifecycle) * T);
+  L.k5 = p; p += al(loader_scratch_bytes(R.T, R.E, R.max_events));
+  L.wbytes = p; p += al(8 * E);
+  L.wtag = p; p += al(4 * E);
+  L.woff = p; p += al(8 * (T + 1));
+  L.wnids = p; p += al(4 * T);
+  L.out = p; p += al(sizeof(xm_result) * T);
+  L.scratch = p;
+  xm_batch b{};
+  b.n_traces = R.T;
+  b.n_events = R.E;
+  b.max_ids = R.max_ids;
+  b.max_events = R.max_events;
+  p += al(xm_scratch_bytes(&b, cfg));
+  L.total = p;
+  return L;
+}
+
+// host checks of the offsets (the per-event checks run on the device)
+int raw_shape(const int64_t* off, int64_t T, RawShape* R, int64_t* bad) {
+  if (!off || T < 0) return set_error(XM_EINVAL, "xm_simulate_raw: null offsets or negative n_traces");
+  if (off[0] != 0) return set_error(XM_EINVAL, "xm_simulate_raw: off[0] != 0");
+  int64_t mx = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t n = off[t + 1] - off[t];
+    if (n < 0) { if (bad) *bad = t; return set_error(XM_EINVAL, "xm_simulate_raw: offsets not monotone"); }
+    if (n > 0x7FFFFFFFll) {
+      if (bad) *bad = t;
+      return set_error(XM_ERANGE, "xm_simulate_raw: trace longer than 2^31-1 events");
+    }
+    mx = std::max(mx, n);
+  }
+  R->T = T;
+  R->E = off[T];
+  R->max_events = uint32_t(mx);
+  // dense ids of the loader: <= max live + 31 (K5), bounded by the trace length
+  R->max_ids = uint32_t(std::min<int64_t>(mx + 32, int64_t(1) << 27));
+  return XM_OK;
+}
+
+// device-usable pointer of page-locked host memory, or null (pageable)
+const void* mapped(const void* h) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+}  // namespace
+
+extern "C" size_t xm_raw_ws_bytes(const int64_t* h_off, int64_t n_traces, const xm_config* cfg) {
+  RawShape R{};
+  if (!cfg || raw_shape(h_off, n_traces, &R, nullptr)) return 0;
+  return raw_layout(R, cfg).total;
+}
+
+extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, const int64_t* h_off,
+                               int64_t n_traces, const uint64_t* h_capacity, const xm_config* cfg,
+                               void* d_ws, size_t ws_bytes, xm_result* h_out, int64_t* bad_trace,
+                               void* stream) {
+  if (bad_trace) *bad_trace = -1;
+  if (!cfg || !h_out) return set_error(XM_EINVAL, "xm_simulate_raw: null argument");
+  RawShape R{};
+  int rc = raw_shape(h_off, n_traces, &R, bad_trace);
+  if (rc) return rc;
+  if (R.T == 0) return XM_OK;
+  if (R.E > 0 && (!h_bytes || !h_tag)) return set_error(XM_EINVAL, "xm_simulate_raw: null event arrays");
+  if (cfg->mode != XM_FULL) return set_error(XM_EINVAL, "xm_simulate_raw: XM_FULL mode only");
+  UnitConfig u;
+  if ((rc = make_unit_config(cfg, &u))) return rc;
+  const RawLayout L = raw_layout(R, cfg);
+  if (!d_ws || ws_bytes < L.total) return set_error(XM_ENOMEM, "xm_simulate_raw: workspace too small");
+  if (!cuda_usable()) return set_error(XM_ECUDA, "no CUDA device");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(d_ws);
+  cudaError_t e = cudaSuccess;
+  auto cp = [&](size_t o, const void* src, size_t n) {
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, st);
+  };
+  // processing order: longest first, ties in caller order (as xm_load_traces)
+  std::vector<uint32_t> order(size_t(R.T));
+  for (int64_t i = 0; i < R.T; ++i) order[size_t(i)] = uint32_t(i);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
+  });
+  // events: read in place by the loader kernel when page-locked, else copied
+  const int64_t* d_bytes = static_cast<const int64_t*>(mapped(h_bytes));
+  const uint32_t* d_tag = static_cast<const uint32_t*>(mapped(h_tag));
+  if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
+  if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
+  cp(L.off, h_off, 8 * size_t(R.T + 1));
+  cp(L.order, order.data(), 4 * size_t(R.T));
+  if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
+  if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
+  int launches = 0;
+  xm_lifecycle* d_rec = reinterpret_cast<xm_lifecycle*>(w + L.rec);
+  int ek = launch_loader(d_bytes, d_tag, reinterpret_cast<const int64_t*>(w + L.off), R.T, R.E,
+                         R.max_events, w + L.k5, d_rec, reinterpret_cast<const uint32_t*>(w + L.order),
+                         reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
+                         reinterpret_cast<int64_t*>(w + L.woff), reinterpret_cast<uint32_t*>(w + L.wnids),
+                         stream, &launches);
+  if (ek) return set_error(XM_ECUDA, std::string("xm_simulate_raw loader: ") + cudaGetErrorString(cudaError_t(ek)));
+  xm_batch b{};
+  b.bytes = reinterpret_cast<const int64_t*>(w + L.wbytes);
+  b.tag = reinterpret_cast<const uint32_t*>(w + L.wtag);
+  b.off = reinterpret_cast<const int64_t*>(w + L.woff);
+  b.n_ids = reinterpret_cast<const uint32_t*>(w + L.wnids);
+  b.order = reinterpret_cast<const uint32_t*>(w + L.order);
+  b.capacity = h_capacity ? reinterpret_cast<const uint64_t*>(w + L.cap) : nullptr;
+  b.n_traces = R.T;
+  b.n_events = R.E;
+  b.max_ids = R.max_ids;
+  b.max_events = R.max_events;
+  xm_result* d_out = reinterpret_cast<xm_result*>(w + L.out);
+  rc = simulate(&b, cfg, w + L.scratch, L.total - L.scratch, d_out, stream, nullptr);
+  launch_counter() += launches;
+  if (rc) return rc;
+  // results and the loader's verdicts back (one synchronisation)
+  std::vector<xm_lifecycle> rec(size_t(R.T));
+  e = cudaMemcpyAsync(h_out, d_out, sizeof(xm_result) * size_t(R.T), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(rec.data(), d_rec, sizeof(xm_lifecycle) * size_t(R.T), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw D2H: ") + cudaGetErrorString(e));
+  for (int64_t t = 0; t < R.T; ++t) {
+    const xm_lifecycle& r = rec[size_t(t)];
+    const char* m = r.n_invalid ? "zero-byte or >= 2^40 request (SPEC.md:231)"
+                  : r.n_reopened ? "alloc of a live id (SPEC.md:249)"
+                  : r.n_orphan ? "free of a non-live id (SPEC.md:258)"
+                  : r.n_mismatch ? "free size differs from the alloc's request (SPEC.md:258)"
+                  : r.n_ids > (1u << 27) ? "more than 2^27 live blocks" : nullptr;
+    if (m) {
+      if (bad_trace) *bad_trace = t;
+      return set_error(XM_EINVAL, std::string("xm_simulate_raw: trace ") + std::to_string(t) + ": " + m);
+    }
+  }
+  clear_error();
+  return XM_OK;
 }

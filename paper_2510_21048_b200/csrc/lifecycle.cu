@@ -58,6 +58,8 @@ struct __align__(16) ARec {                 // what a matching free needs, in on
 };
 
 struct LParams {
+  const uint32_t* __restrict__ tag;       // loader mode (xm_simulate_raw): raw block id |
+                                          // stream << 28 stands for (addr, stream); else null
   const uint64_t* __restrict__ addr;
   const int64_t* __restrict__ bytes;
   const uint8_t* __restrict__ stream;
@@ -108,15 +110,21 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       reinterpret_cast<uint4*>(T)[h] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
-    unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0;
+    unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0,
+                       n_reopen = 0;
     for (int base = 0; base < n; base += 32) {
       const int li = base + int(lane);
       const bool valid = li < n;
-      const uint64_t a = valid ? P.addr[e0 + li] : ~0ull - lane;
+      uint64_t a = valid ? (P.tag ? 0ull : P.addr[e0 + li]) : ~0ull - lane;
       int64_t b = valid ? P.bytes[e0 + li] : 0;
       // |bytes| >= XM_MAX_REQUEST is out of the replay's range: invalid like 0
       if (b >= int64_t(XM_MAX_REQUEST) || b <= -int64_t(XM_MAX_REQUEST)) b = 0;
-      const uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
+      uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
+      if (P.tag) {                          // loader mode: the raw block id is the key
+        const uint32_t g = valid ? P.tag[e0 + li] : 0u;
+        a = valid ? uint64_t(g & 0x0FFFFFFFu) : a;
+        s = g >> 28;
+      }
       const bool is_alloc = b > 0, is_free = b < 0;
       // ---- dense ids for this tile's allocations (ids freed before the tile) ----
       const unsigned am = __ballot_sync(kFull, is_alloc);
@@ -126,14 +134,16 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       if (is_alloc) {
         const uint32_t id = ka < take ? ids[top - 1 - ka] : fresh + (ka - take);
         my_tag = id | (s << 28);
-        P.partner[e0 + li] = -1;
-        P.mismatch[e0 + li] = 0;
+        if (P.partner) {
+          P.partner[e0 + li] = -1;
+          P.mismatch[e0 + li] = 0;
+        }
       }
       top -= take;
       fresh += na - take;
       __syncwarp();
       // ---- matching (LIFO per address) ----
-      bool matched = false;
+      bool matched = false, reopened = false;
       int blk = -1;
       uint32_t blk_tag = 0;                 // the matched allocation's record
       long long blk_bytes = 0;
@@ -177,6 +187,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
         __syncwarp();
         if (act) {
           if (is_alloc) {
+            reopened = found && T[h].top >= 0;           // its address still has an open block
             // one 16-byte store / load per record
             const unsigned long long ub = static_cast<unsigned long long>(b);
             reinterpret_cast<int4*>(P.arec)[e0 + li] =
@@ -197,16 +208,16 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       __syncwarp();
       // ---- per-instant outputs ----
       bool mism = false;
-      if (is_free) {
-        P.partner[e0 + li] = matched ? blk : -1;
-        if (matched) {
-          P.partner[e0 + blk] = li;
-          mism = blk_bytes != -b;
+      if (is_free && matched) mism = blk_bytes != -b;
+      if (P.partner) {                      // (the loader mode needs the tallies only)
+        if (is_free) {
+          P.partner[e0 + li] = matched ? blk : -1;
+          if (matched) P.partner[e0 + blk] = li;
+          P.mismatch[e0 + li] = mism ? 1 : 0;
+        } else if (valid && b == 0) {
+          P.partner[e0 + li] = -1;
+          P.mismatch[e0 + li] = 0;
         }
-        P.mismatch[e0 + li] = mism ? 1 : 0;
-      } else if (valid && b == 0) {
-        P.partner[e0 + li] = -1;
-        P.mismatch[e0 + li] = 0;
       }
       __syncwarp();
       // ---- matched blocks' ids go back on the stack ----
@@ -242,6 +253,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       n_orphan += __popc(__ballot_sync(kFull, is_free && !matched));
       n_mism += __popc(__ballot_sync(kFull, mism));
       n_inv += __popc(__ballot_sync(kFull, valid && b == 0));
+      n_reopen += __popc(__ballot_sync(kFull, reopened));
       __syncwarp();
     }
     if (lane == 0) {
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       r.n_invalid = n_inv;
       r.max_open = max_open;
       r.n_ids = fresh;
+      r.n_reopened = n_reopen;
       P.rec[k] = r;
     }
     __syncwarp();
@@ -482,3 +495,61 @@ extern "C" int xm_blocks_from_instants(const xm_instants* in, const int64_t* d_t
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("k_blocks: ") + cudaGetErrorString(e));
   return XM_OK;
 }
+
+// ---- device loader (xm_simulate_raw): K5 keyed by raw block ids ------------------
+namespace xm_internal {
+
+// Scratch of the loader mode for T traces / E events / the longest trace.
+size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events) {
+  xm_instants in{};
+  in.n_traces = T;
+  in.n_events = E;
+  in.max_events = max_events;
+  return layout(&in).total;
+}
+
+// Validation + dense renumbering of raw traces on the device: k_reconstruct with
+// the raw block id as the matching key (one open block per id in a valid trace,
+// SPEC.md:249/258), tallies only (no partner output), then the wire arrays
+// stored in `d_order`. A trace is valid iff its n_orphan, n_mismatch, n_invalid
+// and n_reopened are 0; then its wire form is the trace itself with dense ids.
+int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* d_off, int64_t T,
+                  int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
+                  const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
+                  uint32_t* w_nids, void* stream, int* n_launches) {
+  xm_instants in{};
+  in.n_traces = T;
+  in.n_events = E;
+  in.max_events = max_events;
+  in.off = d_off;
+  in.bytes = d_bytes;
+  const Layout L = layout(&in);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(d_scratch);
+  cudaError_t e = cudaMemsetAsync(base, 0, 256, st);
+  if (e != cudaSuccess) return int(e);
+  LParams P{};
+  P.tag = d_tag;
+  P.bytes = d_bytes;
+  P.off = d_off;
+  P.n_traces = T;
+  P.hbits = L.hbits;
+  P.tables = reinterpret_cast<Slot*>(base + L.tables);
+  P.idstacks = reinterpret_cast<uint32_t*>(base + L.stacks);
+  P.max_events = max_events ? max_events : 1;
+  P.arec = reinterpret_cast<ARec*>(base + L.arec);
+  P.st_bytes = reinterpret_cast<int64_t*>(base + L.st_bytes);
+  P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
+  P.rec = d_rec;
+  P.work = reinterpret_cast<unsigned int*>(base);
+  k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
+  k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, d_order, T, w_off);
+  const int64_t want = (T + 7) / 8;
+  const int g = int(want < int64_t(L.ctas) * 8 ? want : int64_t(L.ctas) * 8);
+  k_wire_compact<<<g > 0 ? g : 1, 256, 0, st>>>(d_off, w_off, d_rec, d_order, P.st_bytes, P.st_tag, T,
+                                               w_bytes, w_tag, w_nids);
+  *n_launches += 3;
+  return int(cudaGetLastError());
+}
+
+}  // namespace xm_internal

@@ -68,4 +68,11 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t 
                 xm_result* d_out, void* stream, int* n_launches);
 size_t scan_scratch_bytes(const xm_batch* b);
 
+// Device loader of xm_simulate_raw (lifecycle.cu): K5 keyed by raw block ids.
+size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events);
+int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* d_off, int64_t T,
+                  int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
+                  const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
+                  uint32_t* w_nids, void* stream, int* n_launches);
+
 }  // namespace xm_internal

@@ -79,6 +79,16 @@ def _check(ins):
         for k in TALLIES:
             assert int(rec[k][t]) == tal[k], (t, k, int(rec[k][t]), tal[k])
         assert tal["max_open"] <= int(rec["n_ids"][t]) <= tal["max_open"] + 31
+        # n_reopened: allocations at an address whose earlier block is still open
+        # (brute force over the oracle's pairing)
+        open_at, reop = {}, 0
+        for j in range(len(by)):
+            if by[j] > 0:
+                reop += open_at.get(int(a[j]), 0) > 0
+                open_at[int(a[j])] = open_at.get(int(a[j]), 0) + 1
+            elif by[j] < 0 and p[j] >= 0:
+                open_at[int(a[j])] -= 1
+        assert int(rec["n_reopened"][t]) == reop, (t, int(rec["n_reopened"][t]), reop)
         ob, ot, kept = oracle.wire_from_partner(by, st, p)
         q = pos[t]
         gb = wbytes[woff[q]:woff[q + 1]]
