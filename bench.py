@@ -295,9 +295,32 @@ def _init_dist(dev):
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group(backend)
+def relaunch(args) -> int:
+    """--gpus N > 1 without a launcher: run this same command under
+    torch.distributed.run, one rank per GPU, rendezvous on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank "
+                         f"per GPU (or omit the launcher and let bench.py start them)")
+    if world > 1 and os.environ.get("XM_BENCH_BACKEND", "nccl") == "nccl":
+        # keep NCCL's communicator-init log (rank count per communicator)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         return run_reference(args, world, rank)
     if args.workload == "cfg5":

@@ -22,9 +22,38 @@ class ShardPlan:
     shards: List[np.ndarray]    # global trace indices per rank (in replay order)
     events: np.ndarray          # events per rank
 
+    def __post_init__(self):
+        self._cache = {}        # per device: gather permutation and padded buffers
+
     @property
     def max_shard(self) -> int:
         return max((len(s) for s in self.shards), default=0)
+
+    def perm(self, device):
+        """Global trace t's row in the rank-major padded gather, as a device
+        tensor built once per device (not re-uploaded every step)."""
+        key = ("perm", str(device))
+        if key not in self._cache:
+            import torch
+            M = self.max_shard
+            T = sum(len(s) for s in self.shards)
+            src = np.concatenate([r * M + np.arange(len(s)) for r, s in enumerate(self.shards)]) \
+                if T else np.zeros(0, np.int64)
+            dst = np.concatenate(self.shards) if T else np.zeros(0, np.int64)
+            p = np.empty(T, np.int64)
+            p[dst] = src
+            self._cache[key] = torch.from_numpy(p).to(device)
+        return self._cache[key]
+
+    def buffers(self, device, width):
+        """(pad [M, width], full [W*M, width]) uint8 gather buffers, reused."""
+        key = ("buf", str(device), width)
+        if key not in self._cache:
+            import torch
+            M = self.max_shard
+            self._cache[key] = (torch.zeros((M, width), dtype=torch.uint8, device=device),
+                                torch.empty((self.world * M, width), dtype=torch.uint8, device=device))
+        return self._cache[key]
 
 
 def lpt_plan(lengths: np.ndarray, world: int) -> ShardPlan:
@@ -56,24 +85,15 @@ def gather_results(local, plan: ShardPlan, rank: int, group=None):
     width = local.shape[1] if local.dim() == 2 else 64
     # gloo (CPU tests, debugging) gathers host tensors; NCCL the device ones
     dev = "cpu" if dist.get_backend(group) == "gloo" else local.device
-    pad = torch.zeros((M, width), dtype=torch.uint8, device=dev)
+    pad, full = plan.buffers(dev, width)
     pad[: local.shape[0]] = local.to(dev)
-    full = torch.empty((W * M, width), dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(full, pad, group=group)
     return reorder(full, plan).to(local.device)
 
 
 def reorder(full, plan: ShardPlan):
     """[W*M, 64] rank-major padded results -> [T_total, 64] in global order."""
-    import torch
-    M = plan.max_shard
-    T = sum(len(s) for s in plan.shards)
-    src = np.concatenate([r * M + np.arange(len(s)) for r, s in enumerate(plan.shards)]) \
-        if T else np.zeros(0, np.int64)
-    dst = np.concatenate(plan.shards) if T else np.zeros(0, np.int64)
-    perm = np.empty(T, np.int64)
-    perm[dst] = src
-    return full.index_select(0, torch.from_numpy(perm).to(full.device))
+    return full.index_select(0, plan.perm(full.device))
 
 
 SUM_KEYS = ("n_traces", "events_done", "n_oom", "n_overflow", "sum_peak_reserved", "n_predicted_oom")
