@@ -162,7 +162,7 @@ def lib():
     """Load libxmem.so (building it in-tree if stale). Fails loudly."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("XM_LIB") or _build.LIB    # XM_LIB: A/B tooling only
         if not os.path.exists(path) or os.environ.get("XM_REBUILD"):
             _build.build()
         L = ctypes.CDLL(path)

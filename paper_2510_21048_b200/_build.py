@@ -10,7 +10,9 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 DEBUG = bool(os.environ.get("XM_DEBUG"))
 TIMING = bool(os.environ.get("XM_TIMING"))
-LIB = os.path.join(PKG, "libxmem_debug.so" if DEBUG else ("libxmem_timing.so" if TIMING else "libxmem.so"))
+TAG = os.environ.get("XM_BUILD_TAG", "")          # A/B tooling: a separately named variant
+LIB = os.path.join(PKG, "libxmem_debug.so" if DEBUG else ("libxmem_timing.so" if TIMING else
+                                                         (f"libxmem_{TAG}.so" if TAG else "libxmem.so")))
 SOURCES = ["loader.cpp", "capi.cu", "replay.cu", "scan.cu", "expand.cu", "metrics.cu", "lifecycle.cu", "orchestrate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -31,7 +33,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     bdir = os.path.join(PKG, "build")
     os.makedirs(bdir, exist_ok=True)
     for src in SOURCES:
-        obj = os.path.join(bdir, src + (".dbg.o" if DEBUG else (".tim.o" if TIMING else ".o")))
+        obj = os.path.join(bdir, src + (".dbg.o" if DEBUG else (".tim.o" if TIMING else (f".{TAG}.o" if TAG else ".o"))))
+        path = os.path.join(CSRC, src)
+        if src == "replay.cu" and os.environ.get("XM_REPLAY_SRC"):   # A/B tooling
+            path = os.path.abspath(os.environ["XM_REPLAY_SRC"])
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), *(["-DXM_TIMING"] if TIMING else []),
                *([f"-DXM_HEAP_RESERVE_DIV={os.environ['XM_HEAP_RESERVE_DIV']}"] if os.environ.get("XM_HEAP_RESERVE_DIV") else []),
                *([f"-DXM_F_INIT_DIV={os.environ['XM_F_INIT_DIV']}"] if os.environ.get("XM_F_INIT_DIV") else []),
@@ -40,8 +45,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
                *([f"-DXM_K1_WARPS={os.environ['XM_K1_WARPS']}"] if os.environ.get("XM_K1_WARPS") else []),
                *([f"-DXM_MAX_NAP={os.environ['XM_MAX_NAP']}"] if os.environ.get("XM_MAX_NAP") else []),
                *([f"-DXM_K1_PER_LANE={os.environ['XM_K1_PER_LANE']}"] if os.environ.get("XM_K1_PER_LANE") else []),
+               *[f"-D{k}={os.environ[k]}" for k in ("XM_K1C_PER", "XM_K1C_STAGES", "XM_K1C_CTAS_PER_SM", "XM_K1C_THREADS")
+                 if os.environ.get(k)],
                "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src),
+               "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", path,
                "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []

@@ -328,6 +328,24 @@ __device__ __forceinline__ void set_prev(const State<L>& S, uint32_t ref, uint32
   if (ref != L::kNone) p[0] = typename L::Link(v);
 }
 
+// link halves of a record whose kind (allocated id / free entry) is known
+template <class L>
+__device__ __forceinline__ void a_set_next(const State<L>& S, uint32_t id, uint32_t v) {
+  S.A_lk[2 * id + 1] = typename L::Link(v);
+}
+template <class L>
+__device__ __forceinline__ void a_set_prev(const State<L>& S, uint32_t id, uint32_t v) {
+  S.A_lk[2 * id] = typename L::Link(v);
+}
+template <class L>
+__device__ __forceinline__ void f_set_next(const State<L>& S, uint32_t f, uint32_t v) {
+  S.F_lk[2 * f + 1] = typename L::Link(v);
+}
+template <class L>
+__device__ __forceinline__ void f_set_prev(const State<L>& S, uint32_t f, uint32_t v) {
+  S.F_lk[2 * f] = typename L::Link(v);
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -876,6 +894,9 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
   constexpr uint32_t kNone = L::kNone, kF = L::kF;
   const uint32_t lane = threadIdx.x & 31;
   const xm_internal::UnitConfig& u = P.u;
+  // a7's large-pool rule (reading Q1): split iff rem > small_size (torch), or
+  // rem >= small_size (SPEC) -- one threshold either way
+  const uint32_t lsplit = u.strict ? u.small_u + 1u : u.small_u;
   const long long* __restrict__ by = reinterpret_cast<const long long*>(P.bytes) + e0;
   const uint32_t* __restrict__ tg = P.tag + e0;
   const unsigned long long* __restrict__ pk = P.packed ? P.packed + e0 : nullptr;
@@ -1118,7 +1139,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         }
         // a7: split (PAPER.md:258 (iii); reading Q1)
         const uint32_t rem = bsize - s;
-        bool split = small ? (rem >= 1u) : (u.strict ? (rem > u.small_u) : (rem >= u.small_u));
+        bool split = rem >= (small ? 1u : lsplit);
         if constexpr (kKnobs) split = split && (small || s < u.msplit_u);   // torch should_split (Q26)
         if (split && fsel == kNone32 && nf >= S.cap_f && !grow_f(S, G, nf)) {
           status = kStatusOverflow;
@@ -1136,33 +1157,43 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         __syncwarp();
         // ---- store phase (every lane stores the same values; no location is
         // written twice with different values within an event, so lanes that
-        // run unconverged cannot leave a stale value) ----
+        // run unconverged cannot leave a stale value). A free block's
+        // neighbours are allocated blocks or none (free neighbours are always
+        // merged), so their links are set directly in A. ----
         uint32_t asize;
-        if (split) {
-          uint32_t r = fsel;                           // remainder keeps the free entry
-          if (fsel == kNone32) r = nf++;               // new segment: no right neighbour
-          f_store(S, r, make_key(cls, rem), bposu + s, rem);
-          store_links<L>(S.F_lk, r, id, bnext);
-          if (kKnobs && S.F_age) S.F_age[r] = small ? srch_small : srch_large;   // enters now
-          asize = s;
-          bnext = kF | r;
-        } else {
-          set_prev(S, bnext, id);
-          if (remove) {                                // move the last entry into fsel
-            if (fsel != Lx) {
-              f_store(S, fsel, lk, lpos, lsz);
-              store_links<L>(S.F_lk, fsel, lpv, lnx);
-              if (kKnobs && S.F_age) S.F_age[fsel] = lag;
-              set_next(S, lpv, kF | fsel);
-              set_prev(S, lnx, kF | fsel);
-            }
-            if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
-            nf = Lx;
+        if (fsel == kNone32) {                         // new segment: no neighbours
+          if (split) {
+            const uint32_t r = nf++;                   // the remainder, right of the block
+            f_store(S, r, make_key(cls, rem), bposu + s, rem);
+            store_links<L>(S.F_lk, r, id, kNone);
+            if (kKnobs && S.F_age) S.F_age[r] = small ? srch_small : srch_large;   // enters now
+            asize = s;
+            bnext = kF | r;
+          } else {
+            asize = bsize;
           }
+        } else if (split) {                            // the remainder keeps entry fsel
+          f_store(S, fsel, make_key(cls, rem), bposu + s, rem);
+          f_set_prev(S, fsel, id);
+          if (kKnobs && S.F_age) S.F_age[fsel] = small ? srch_small : srch_large;
+          if (bprev != kNone) a_set_next(S, bprev, id);
+          asize = s;
+          bnext = kF | fsel;
+        } else {                                       // the whole block: drop entry fsel
+          if (fsel != Lx) {                            // (the last entry moves into it)
+            f_store(S, fsel, lk, lpos, lsz);
+            store_links<L>(S.F_lk, fsel, lpv, lnx);
+            if (kKnobs && S.F_age) S.F_age[fsel] = lag;
+            if (lpv != kNone) a_set_next(S, lpv, kF | fsel);
+            if (lnx != kNone) a_set_prev(S, lnx, kF | fsel);
+          }
+          if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
+          nf = Lx;
+          if (bprev != kNone) a_set_next(S, bprev, id);
+          if (bnext != kNone) a_set_prev(S, bnext, id);
           asize = bsize;
         }
         a_store(S, id, bposu, asize, bprev, bnext);
-        set_next(S, bprev, id);
         blk += asize;
         // a9: the block peak only moves up on allocs, first index (Q7)
         if (blk > pk_blk) { pk_blk = blk; ix_blk = base + j; }
@@ -1179,75 +1210,88 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
         const bool pf = p != kNone && (p & kF);
         const bool qf = q != kNone && (q & kF);
         const uint32_t P_ = p & ~kF, N_ = q & ~kF;
-        uint32_t psz = 0, nsz0 = 0, nnx = kNone, k_, npv_;
-        uint64_t ppos = 0, npos_;
-        if (pf) f_load(S, P_, k_, ppos, psz);
-        if (qf) {
-          f_load(S, N_, k_, npos_, nsz0);
-          load_links<L>(S.F_lk, N_, npv_, nnx);
-        }
-        if (!pf && !qf && nf >= S.cap_f && !grow_f(S, G, nf)) {
-          status = kStatusOverflow;
-          break;
-        }
-        const uint32_t Lx = nf - 1;                      // for removing N_ (both free)
-        uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone, lag = 0;
-        uint64_t lpos = 0;
-        if (pf && qf && N_ != Lx) {
-          f_load(S, Lx, lk, lpos, lsz);
-          load_links<L>(S.F_lk, Lx, lpv, lnx);
-          if (kKnobs && S.F_age) lag = S.F_age[Lx];
-        }
         // GC age: the merged / new free block enters the free list now
         const uint32_t now_age = (acls & 1u) ? srch_small : srch_large;
-        __syncwarp();
-        // ---- store phase: a8, coalesce with free neighbours; reserved unchanged
-        // (PAPER.md:259 (iv)) ----
-        if (pf) {
-          const uint32_t nsz = psz + sz + (qf ? nsz0 : 0u);
-          const uint32_t nn = qf ? nnx : q;
-          const uint32_t nk = make_key(acls, nsz);
-          if (qf && N_ != Lx && Lx == P_) {
-            // the merged entry is the last one and moves into N_'s slot: write
-            // it there once (writing P_ first and then its sentinel would store
-            // two values to one location in one event)
-            f_store(S, N_, nk, ppos, nsz);
-            store_links<L>(S.F_lk, N_, lpv, nn);
-            if (kKnobs && S.F_age) S.F_age[N_] = now_age;
-            set_next(S, lpv, kF | N_);
-            set_prev(S, nn, kF | N_);
-            if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
-            nf = Lx;
-          } else {
-            f_store(S, P_, nk, ppos, nsz);
-            if (kKnobs && S.F_age) S.F_age[P_] = now_age;
-            set_next(S, p, nn);
-            set_prev(S, nn, p);
-            if (qf) {                                 // drop N_: move the last entry there
-              if (N_ != Lx) {
-                f_store(S, N_, lk, lpos, lsz);
-                store_links<L>(S.F_lk, N_, lpv, lnx);
-                if (kKnobs && S.F_age) S.F_age[N_] = lag;
-                set_next(S, lpv, kF | N_);
-                set_prev(S, lnx, kF | N_);
-              }
-              if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
-              nf = Lx;
-            }
+        if (!pf && !qf) {
+          // neither neighbour is free: a new free entry, which the neighbours
+          // (allocated blocks or none) point to
+          if (nf >= S.cap_f && !grow_f(S, G, nf)) {
+            status = kStatusOverflow;
+            break;
           }
-        } else if (qf) {
-          const uint32_t nsz = nsz0 + sz;
-          f_store(S, N_, make_key(acls, nsz), apos, nsz);
-          if (kKnobs && S.F_age) S.F_age[N_] = now_age;
-          set_prev(S, q, p);
-          set_next(S, p, q);
-        } else {
+          __syncwarp();
           const uint32_t r = nf++;
           f_store(S, r, make_key(acls, sz), apos, sz);
           store_links<L>(S.F_lk, r, p, q);
           if (kKnobs && S.F_age) S.F_age[r] = now_age;
-          set_next(S, p, kF | r);
-          set_prev(S, q, kF | r);
+          if (p != kNone) a_set_next(S, p, kF | r);
+          if (q != kNone) a_set_prev(S, q, kF | r);
+        } else if (!qf) {
+          // a8: the free previous block absorbs this one (reserved unchanged,
+          // PAPER.md:259 (iv))
+          uint32_t k_, psz;
+          uint64_t ppos;
+          f_load(S, P_, k_, ppos, psz);
+          __syncwarp();
+          const uint32_t nsz = psz + sz;
+          f_store(S, P_, make_key(acls, nsz), ppos, nsz);
+          if (kKnobs && S.F_age) S.F_age[P_] = now_age;
+          f_set_next(S, P_, q);
+          if (q != kNone) a_set_prev(S, q, p);
+        } else if (!pf) {
+          // this block absorbs the free next one, whose entry it takes over
+          uint32_t k_, nsz0;
+          uint64_t npos_;
+          f_load(S, N_, k_, npos_, nsz0);
+          __syncwarp();
+          const uint32_t nsz = nsz0 + sz;
+          f_store(S, N_, make_key(acls, nsz), apos, nsz);
+          if (kKnobs && S.F_age) S.F_age[N_] = now_age;
+          f_set_prev(S, N_, p);
+          if (p != kNone) a_set_next(S, p, q);
+        } else {
+          // both neighbours free: prev absorbs this block and next; next's
+          // entry is dropped (the last entry moves into it)
+          uint32_t k_, psz, nsz0, nnx, npv_;
+          uint64_t ppos, npos_;
+          f_load(S, P_, k_, ppos, psz);
+          f_load(S, N_, k_, npos_, nsz0);
+          load_links<L>(S.F_lk, N_, npv_, nnx);
+          const uint32_t Lx = nf - 1;
+          uint32_t lk = 0, lsz = 0, lpv = kNone, lnx = kNone, lag = 0;
+          uint64_t lpos = 0;
+          if (N_ != Lx) {
+            f_load(S, Lx, lk, lpos, lsz);
+            load_links<L>(S.F_lk, Lx, lpv, lnx);
+            if (kKnobs && S.F_age) lag = S.F_age[Lx];
+          }
+          __syncwarp();
+          const uint32_t nsz = psz + sz + nsz0;
+          const uint32_t nk = make_key(acls, nsz);
+          if (N_ != Lx && Lx == P_) {
+            // the merged entry is the last one and moves into N_'s slot: write
+            // it there once (writing P_ first and then its sentinel would store
+            // two values to one location in one event)
+            f_store(S, N_, nk, ppos, nsz);
+            store_links<L>(S.F_lk, N_, lpv, nnx);
+            if (kKnobs && S.F_age) S.F_age[N_] = now_age;
+            if (lpv != kNone) a_set_next(S, lpv, kF | N_);
+            if (nnx != kNone) a_set_prev(S, nnx, kF | N_);
+          } else {
+            f_store(S, P_, nk, ppos, nsz);
+            if (kKnobs && S.F_age) S.F_age[P_] = now_age;
+            f_set_next(S, P_, nnx);
+            if (nnx != kNone) a_set_prev(S, nnx, p);
+            if (N_ != Lx) {                            // drop N_: the last entry moves there
+              f_store(S, N_, lk, lpos, lsz);
+              store_links<L>(S.F_lk, N_, lpv, lnx);
+              if (kKnobs && S.F_age) S.F_age[N_] = lag;
+              if (lpv != kNone) a_set_next(S, lpv, kF | N_);
+              if (lnx != kNone) a_set_prev(S, lnx, kF | N_);
+            }
+          }
+          if constexpr (L::kPacked) S.F_kp[Lx] = kSentinel;
+          nf = Lx;
         }
         blk -= sz;
       }

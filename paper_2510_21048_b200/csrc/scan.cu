@@ -20,10 +20,14 @@
 //        and the tile's first/last pieces are stored for crossing traces
 //   K1b  one thread per crossing trace folds its pieces (~len/4096 of them)
 // HBM traffic: 8 B/event read once + 0.5 B/event row map + 48 B/tile + 64 B/trace.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "rounding.cuh"
 #include "xm_internal.h"
@@ -496,6 +500,493 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
   }
 }
 
+
+// ---- K1c: contiguous event chunks streamed by TMA (the default K1 path) ------
+//
+// The same quantity as K1t (max prefix sum of +-s per trace and its first
+// index), but trace-oblivious: the batch's events are cut into G contiguous
+// chunks of whole 2048-event tiles, one per persistent CTA, so every CTA
+// streams an equal share at full rate no matter how long its traces are, and
+// no trace start waits on a work counter. Tiles arrive by TMA
+// (cp.async.bulk.tensor.2d, the events viewed as rows of 16 words with the
+// 128-byte swizzle, so each thread's 8 consecutive events read back without
+// bank conflicts) into a kCStages-deep mbarrier ring, issued kCStages-1 tiles
+// ahead by one elected thread. A tile without a trace start (the common case)
+// is one piece: a warp scan + arg-max per warp and a fold onto the CTA's
+// running piece. Otherwise a segmented scan of (starts-here flag, piece,
+// trace): traces that start and end inside the chunk are finished in place;
+// each chunk leaves its head piece (events before its first trace start) and
+// its tail piece (from its last trace start), and the last CTA to finish
+// folds those across chunks (the same segmented scan over G elements).
+// HBM: 8 B/event read once + 64 B/trace written.
+#ifndef XM_K1C_PER
+#define XM_K1C_PER 8
+#endif
+#ifndef XM_K1C_STAGES
+#define XM_K1C_STAGES 3
+#endif
+#ifndef XM_K1C_CTAS_PER_SM
+#define XM_K1C_CTAS_PER_SM 3
+#endif
+#ifndef XM_K1C_THREADS
+#define XM_K1C_THREADS 256
+#endif
+constexpr int kCThreads = XM_K1C_THREADS;
+constexpr int kCWarps = kCThreads / 32;
+constexpr int kCPer = XM_K1C_PER;                  // consecutive events per thread (8 or 16)
+constexpr int kCTile = kCThreads * kCPer;          // events per tile (16 per 128-byte row)
+constexpr int kCRows = kCTile / 16;                // TMA box rows (<= 256)
+constexpr int kCStages = XM_K1C_STAGES;
+constexpr int kCSmem = kCStages * kCTile * 8 + 1024;      // + 1024 for the swizzle alignment
+constexpr int kCList = kCTile + 64;               // trace starts listed per (re)fill: a refill
+                                                   // from a tile's first start covers the tile
+static_assert(kCPer == 8 || kCPer == 16, "K1c: 8 or 16 events per thread");
+static_assert(kCRows <= 256, "K1c: TMA box");
+
+// segmented-scan element: a piece (sum, max prefix or kNeg if empty, global
+// index of its first maximum), whether a trace starts inside it (f), and the
+// trace of its last start (tr, when f)
+struct SegE {
+  int64_t sum, mx, arg;
+  int32_t tr;
+  bool f;
+};
+
+__device__ __forceinline__ SegE seg_id() { return SegE{0, kNeg, -1, -1, false}; }
+
+// a then b
+__device__ __forceinline__ SegE seg_op(const SegE& a, const SegE& b) {
+  if (b.f) return b;
+  SegE r;
+  r.sum = a.sum + b.sum;
+  const int64_t cand = a.sum + b.mx;
+  const bool take = b.mx != kNeg && cand > a.mx;       // strict: the first index wins
+  r.mx = take ? cand : a.mx;
+  r.arg = take ? b.arg : a.arg;
+  r.tr = a.tr;
+  r.f = a.f;
+  return r;
+}
+
+__device__ __forceinline__ SegE shfl_up_seg(const SegE& e, int o) {
+  SegE r;
+  r.sum = __shfl_up_sync(kFull, e.sum, o);
+  r.mx = __shfl_up_sync(kFull, e.mx, o);
+  r.arg = __shfl_up_sync(kFull, e.arg, o);
+  r.tr = __shfl_up_sync(kFull, e.tr, o);
+  r.f = __shfl_up_sync(kFull, int(e.f), o) != 0;
+  return r;
+}
+
+__device__ __forceinline__ SegE shfl_seg(const SegE& e, int src) {
+  SegE r;
+  r.sum = __shfl_sync(kFull, e.sum, src);
+  r.mx = __shfl_sync(kFull, e.mx, src);
+  r.arg = __shfl_sync(kFull, e.arg, src);
+  r.tr = __shfl_sync(kFull, e.tr, src);
+  r.f = __shfl_sync(kFull, int(e.f), src) != 0;
+  return r;
+}
+
+// inclusive warp segmented scan
+__device__ __forceinline__ SegE warp_seg_scan(SegE x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const SegE y = shfl_up_seg(x, o);
+    if (lane >= o) x = seg_op(y, x);
+  }
+  return x;
+}
+
+struct __align__(16) ChunkSum {   // one per chunk (K1c), in scratch; 64 B
+  int64_t h_sum, h_mx, h_arg;      // head piece: events before the chunk's first trace start
+  int64_t t_sum, t_mx, t_arg;      // tail piece: from its last trace start to its end
+  int32_t t_tr;                    // trace of the last start
+  int32_t has;                     // a trace starts inside the chunk
+  int64_t pad;
+};
+static_assert(sizeof(ChunkSum) == 64, "ChunkSum");
+
+// another CTA's record (L2, not a possibly stale L1 line)
+__device__ __forceinline__ ChunkSum load_chunk(const ChunkSum* p) {
+  ChunkSum r;
+  const longlong2* s = reinterpret_cast<const longlong2*>(p);
+  longlong2* d = reinterpret_cast<longlong2*>(&r);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] = __ldcg(s + i);
+  return r;
+}
+
+struct CParams {
+  const int64_t* __restrict__ bytes;    // events (signed bytes or packed words)
+  const int64_t* __restrict__ off;
+  const uint32_t* __restrict__ order;
+  int64_t n_traces, n_events;
+  int64_t rows;                         // full 16-event rows covered by the tensor map
+  int64_t n_tiles;
+  uint32_t unit_shift;
+  xm_internal::UnitConfig u;
+  ChunkSum* chunks;
+  unsigned int* done;
+  xm_result* out;
+};
+
+__device__ __forceinline__ void c_write(const CParams& P, int32_t tr, int64_t mx, int64_t arg) {
+  const int64_t o = P.off[tr];
+  xm_result R{};
+  R.peak_allocated = mx > 0 ? uint64_t(mx) << P.unit_shift : 0ull;
+  R.peak_allocated_idx = mx > 0 ? uint32_t(arg - o) : 0u;
+  R.events_done = uint32_t(P.off[tr + 1] - o);
+  R.status = XM_T_OK;
+  P.out[P.order[tr]] = R;
+}
+
+template <bool kPacked, bool kDiv>
+__device__ __forceinline__ int64_t c_delta(int64_t raw, const CParams& P) {
+  if constexpr (kPacked && !kDiv) {
+    // |request| in bits 0-40, allocation bit 41: ceil(|b| / 2^sh) with the sign
+    // of the event (the same value as rounded_delta(unpack_bytes(raw), sh))
+    const uint64_t m = uint64_t(raw) & ((1ull << 41) - 1);
+    const int64_t u = int64_t((m + ((1ull << P.unit_shift) - 1)) >> P.unit_shift);
+    return (raw >> 41) & 1 ? u : -u;
+  }
+  const int64_t b = kPacked ? unpack_bytes(raw) : raw;
+  if constexpr (kDiv) return rounded_delta(b, P.u);
+  else return rounded_delta(b, P.unit_shift);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+// Last CTA: fold the chunk pieces (segmented scan over the G chunk elements).
+__device__ void c_fixup(const CParams& P, int G, SegE* s_w) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  SegE carry = seg_id();
+  for (int base = 0; base < G; base += kCThreads) {
+    const int c = base + tid;
+    SegE e = seg_id();
+    ChunkSum cs{};
+    if (c < G) {
+      cs = load_chunk(P.chunks + c);
+      e = cs.has ? SegE{cs.t_sum, cs.t_mx, cs.t_arg, cs.t_tr, true}
+                 : SegE{cs.h_sum, cs.h_mx, cs.h_arg, -1, false};
+    }
+    const SegE inc = warp_seg_scan(e, lane);
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    SegE pre = carry;
+    for (int k = 0; k < w; ++k) pre = seg_op(pre, s_w[k]);
+    SegE ex = shfl_up_seg(inc, 1);
+    if (lane == 0) ex = seg_id();
+    const SegE cin = seg_op(pre, ex);               // everything before chunk c
+    if (c < G && cs.has && cin.f) {                 // chunk c ends the trace open at its start
+      const SegE h{cs.h_sum, cs.h_mx, cs.h_arg, -1, false};
+      const SegE d = seg_op(cin, h);
+      c_write(P, cin.tr, d.mx, d.arg);
+    }
+    SegE tot = carry;
+    for (int k = 0; k < kCWarps; ++k) tot = seg_op(tot, s_w[k]);
+    carry = tot;
+    __syncthreads();
+  }
+  if (tid == 0 && carry.f) c_write(P, carry.tr, carry.mx, carry.arg);   // ends at the last event
+}
+
+// warp 0: list the distinct trace starts at or after trace jn (the last trace
+// of a run of equal offsets; the earlier ones are empty) below `end`, up to
+// kCList of them, as chunk-relative positions; returns (count, next jn) and
+// whether every start below `end` is listed
+__device__ __forceinline__ void list_starts(const CParams& P, int64_t& jn, int64_t c0, int64_t end,
+                                            uint32_t* pos, int32_t* tr, int& cnt, bool& all) {
+  const int lane = threadIdx.x & 31;
+  cnt = 0;
+  all = false;
+  for (;;) {
+    if (cnt > kCList - 32) return;                 // full: refilled later
+    const int64_t x = jn + lane;
+    const int64_t v = x < P.n_traces ? P.off[x] : INT64_MAX;
+    const int64_t vn = x < P.n_traces ? P.off[x + 1] : INT64_MAX;
+    const bool in = v < end;
+    const bool keep = in && vn != v;
+    const unsigned km = __ballot_sync(kFull, keep);
+    if (keep) {
+      const int d = cnt + __popc(km & ((1u << lane) - 1u));
+      pos[d] = uint32_t(v - c0);
+      tr[d] = int32_t(x);
+    }
+    cnt += __popc(km);
+    const int nin = __popc(__ballot_sync(kFull, in));
+    jn += nin;
+    if (nin < 32) { all = true; return; }
+  }
+}
+
+template <bool kPacked, bool kDiv>
+__global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(const __grid_constant__ CUtensorMap tm,
+                                                           CParams P) {
+  extern __shared__ unsigned char c_dsm[];
+  __shared__ __align__(8) unsigned long long s_bar[kCStages];
+  __shared__ uint32_t s_pos[kCList];             // the chunk's trace starts (chunk-relative)
+  __shared__ int32_t s_tr[kCList];               // ... and the trace starting there
+  __shared__ int s_cnt, s_all;
+  __shared__ long long s_jn;
+  __shared__ SegE s_w[2][kCWarps];
+  __shared__ SegE s_run[2];                      // the chunk through tile k (k & 1), by warp 0
+  __shared__ SegE s_head;
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(c_dsm) + 1023) & ~uintptr_t(1023));
+  const int G = gridDim.x;
+  const int64_t c = blockIdx.x;
+  const int64_t k0 = c * P.n_tiles / G, k1 = (c + 1) * P.n_tiles / G;   // this chunk's tiles
+  const int nk = int(k1 - k0);
+  const int64_t c0 = k0 * kCTile;                                       // first event
+  const int64_t c1 = min(k1 * kCTile, P.n_events);                      // past the last
+
+  // prologue: barriers, the first tiles in flight, empty traces, the chunk's starts
+  if (tid == 0) {
+    for (int s = 0; s < kCStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {                        // tile k0+k into stage k % kCStages
+    const int s = k % kCStages;
+    const uint32_t bar = smem_u32(&s_bar[s]);
+    const int64_t row = (k0 + k) * kCRows;
+    if (row < P.rows) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(kCTile * 8) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + size_t(s) * kCTile * 8)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(int(row)), "r"(bar)
+          : "memory");
+    } else {                                       // past the tensor: read from global
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < kCStages - 1 && k < nk; ++k) issue(k);
+  for (int64_t t = int64_t(blockIdx.x) * kCThreads + tid; t < P.n_traces;
+       t += int64_t(G) * kCThreads)
+    if (P.off[t + 1] == P.off[t]) P.out[P.order[t]] = xm_result{};   // empty trace
+  if (w == 0) {                                    // jn = first trace with off[jn] >= c0
+    int64_t lo = 0, hi = P.n_traces;               // answer in [lo, hi]
+    while (hi - lo > 32) {
+      const int64_t step = (hi - lo + 31) / 32;
+      const int64_t x = lo + int64_t(lane) * step;
+      const bool below = x < hi && P.off[x] < c0;
+      const int nbl = __popc(__ballot_sync(kFull, below));   // lanes 0..nbl-1 are below
+      const int64_t nlo = nbl == 0 ? lo : lo + int64_t(nbl - 1) * step + 1;
+      const int64_t nhi = min(hi, lo + int64_t(nbl) * step);
+      lo = nlo;
+      hi = nhi;
+    }
+    const int64_t x = lo + lane;
+    const bool below = x < hi && P.off[x] < c0;
+    int64_t jn = lo + __popc(__ballot_sync(kFull, below));
+    int cnt;
+    bool all;
+    list_starts(P, jn, c0, c1, s_pos, s_tr, cnt, all);
+    if (lane == 0) { s_cnt = cnt; s_all = all; s_jn = jn; }
+  }
+  __syncthreads();
+  int cnt = s_cnt;                                 // listed starts (CTA-uniform)
+  bool all = s_all;
+  int bi = 0;                                      // first listed start not yet passed
+
+  SegE run = seg_id();                             // the chunk so far (warp 0's copy is live)
+  if (tid == 0) { s_run[1] = seg_id(); s_head = seg_id(); }
+  __syncthreads();
+  for (int k = 0; k < nk; ++k) {
+    const int64_t ts = (k0 + k) * kCTile;
+    const int64_t te = min(ts + kCTile, P.n_events);
+    const uint32_t rte = uint32_t(te - c0);
+    if (tid == 0 && k + kCStages - 1 < nk) issue(k + kCStages - 1);
+    if (!all && (bi == cnt || s_pos[cnt - 1] < rte)) {
+      // (rare) unlisted starts may lie in this tile: relist from its first start
+      __syncthreads();
+      if (w == 0) {
+        int64_t jn = bi < cnt ? int64_t(s_tr[bi]) : int64_t(s_jn);
+        int nc;
+        bool na;
+        list_starts(P, jn, c0, c1, s_pos, s_tr, nc, na);
+        if (lane == 0) { s_cnt = nc; s_all = na; s_jn = jn; }
+      }
+      __syncthreads();
+      cnt = s_cnt;
+      all = s_all;
+      bi = 0;
+    }
+    // starts in this tile: listed entries [bi, bi + nb) (each warp counts them)
+    int nb = 0;
+    for (;;) {
+      const int i = bi + nb + lane;
+      const bool in = i < cnt && s_pos[i] < rte;
+      const int m = __popc(__ballot_sync(kFull, in));
+      nb += m;
+      if (m < 32) break;
+    }
+    const int s = k % kCStages;
+    mbar_wait(smem_u32(&s_bar[s]), uint32_t((k / kCStages) & 1));
+    const int64_t p0 = ts + int64_t(tid) * kCPer;  // first event of this thread
+    int64_t d[kCPer];
+    if (p0 + kCPer <= P.rows * 16) {
+      // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r & 7)
+      const unsigned char* st = ring + size_t(s) * kCTile * 8;
+      const int r = (tid * kCPer) >> 4;
+      const int j0 = (tid * kCPer & 15) >> 1;
+#pragma unroll
+      for (int q = 0; q < kCPer / 2; ++q) {
+        const int ch = (j0 + q) ^ (r & 7);
+        const longlong2 v = *reinterpret_cast<const longlong2*>(st + r * 128 + ch * 16);
+        d[2 * q] = v.x;
+        d[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kCPer; ++q)
+        d[q] = p0 + q < te ? reinterpret_cast<const long long*>(P.bytes)[p0 + q] : 0;
+    }
+    const int nv = int(max(int64_t(0), min(int64_t(kCPer), te - p0)));
+#pragma unroll
+    for (int q = 0; q < kCPer; ++q) d[q] = q < nv ? c_delta<kPacked, kDiv>(d[q], P) : 0;
+    SegE* sw = s_w[k & 1];
+    // this thread's starts: listed entries [b, bend) below r0 + kCPer
+    const uint32_t r0 = uint32_t(p0 - c0);
+    int b = bi + nb;
+    if (nb) {
+      int lo = bi, hi = bi + nb;                   // first start at or after r0
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (s_pos[m] < r0) lo = m + 1; else hi = m;
+      }
+      b = lo;
+    }
+    const bool mine = b < bi + nb && s_pos[b] < r0 + kCPer;
+    SegE cur, hd;
+    if (!mine) {
+      // ===== no trace starts here: one piece (sum, max prefix, first arg-max) =====
+      int64_t sum = 0, mx = kNeg;
+      int ai = -1;
+#pragma unroll
+      for (int q = 0; q < kCPer; ++q) {
+        sum += d[q];
+        if (q < nv && sum > mx) { mx = sum; ai = q; }
+      }
+      cur = SegE{sum, mx, ai < 0 ? -1 : p0 + ai, -1, false};
+    } else {
+      // ===== pieces split at the starts; traces wholly inside are finished =====
+      const int bend = bi + nb;
+      uint32_t nxt = s_pos[b];
+      cur = seg_id();
+      hd = seg_id();
+      bool seen = false;
+#pragma unroll
+      for (int q = 0; q < kCPer; ++q) {
+        if (q < nv) {
+          if (r0 + q == nxt) {
+            if (!seen) hd = cur;
+            else c_write(P, cur.tr, cur.mx, cur.arg);
+            seen = true;
+            cur = SegE{0, kNeg, -1, s_tr[b], true};
+            ++b;
+            nxt = b < bend ? s_pos[b] : 0xFFFFFFFFu;
+          }
+          cur.sum += d[q];
+          if (cur.sum > cur.mx) { cur.mx = cur.sum; cur.arg = p0 + q; }
+        }
+      }
+    }
+    SegE inc;
+    const bool wany = __any_sync(kFull, mine);    // warp-uniform
+    if (!wany) {
+      // warp without starts: exclusive prefix of the sums, first arg-max
+      int64_t incl = cur.sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned long long uk =
+          static_cast<unsigned long long>(cur.mx == kNeg ? kNeg : incl - cur.sum + cur.mx) ^
+          0x8000000000000000ull;
+      const unsigned khi = unsigned(uk >> 32), klo = unsigned(uk);
+      const unsigned mh = __reduce_max_sync(kFull, khi);
+      const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
+      const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
+      const int64_t wmx = static_cast<int64_t>((static_cast<unsigned long long>(mh) << 32 | ml) ^
+                                               0x8000000000000000ull);
+      const int64_t warg = __shfl_sync(kFull, cur.arg, src);
+      inc = SegE{incl, wmx, wmx == kNeg ? -1 : warg, -1, false};
+    } else {
+      inc = warp_seg_scan(cur, lane);
+    }
+    if (lane == 31) sw[w] = inc;
+    __syncthreads();                               // sw complete; the stage may be refilled
+    if (wany) {
+      const SegE ex = shfl_up_seg(inc, 1);         // lanes before this one
+      if (mine) {
+        // finish the trace open at this thread's first start: the chunk before
+        // this tile (warp 0's fold, s_run), the warps and lanes before this one
+        SegE pre = s_run[(k + 1) & 1];
+        for (int j = 0; j < w; ++j) pre = seg_op(pre, sw[j]);
+        const SegE cin = lane ? seg_op(pre, ex) : pre;
+        const SegE dn = seg_op(cin, SegE{hd.sum, hd.mx, hd.arg, -1, false});
+        if (cin.f) {
+          c_write(P, cin.tr, dn.mx, dn.arg);       // started in this chunk: finished here
+        } else {                                   // the chunk's head piece (one thread)
+          s_head = dn;
+        }
+      }
+    }
+    if (w == 0) {                                  // warp 0 folds the tile onto the chunk
+      SegE e = lane < kCWarps ? sw[lane] : seg_id();
+#pragma unroll
+      for (int o = 1; o < kCWarps; o <<= 1) {
+        const SegE y = shfl_up_seg(e, o);
+        if (lane >= o) e = seg_op(y, e);
+      }
+      run = seg_op(run, shfl_seg(e, kCWarps - 1));
+      if (lane == 0) s_run[k & 1] = run;
+    }
+    bi += nb;
+  }
+  // chunk record: head (or the whole chunk when no trace starts in it) and tail
+  __syncthreads();                                 // s_head
+  if (tid == 0) {                                  // (warp 0 holds the chunk's piece)
+    ChunkSum cs;
+    if (run.f) {
+      const SegE h = s_head;
+      cs = ChunkSum{h.sum, h.mx, h.arg, run.sum, run.mx, run.arg, run.tr, 1, 0};
+    } else {
+      cs = ChunkSum{run.sum, run.mx, run.arg, 0, kNeg, -1, -1, 0, 0};
+    }
+    P.chunks[c] = cs;
+    __threadfence();
+    s_last = atomicAdd(P.done, 1u) == unsigned(G - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    c_fixup(P, G, s_w[0]);
+  }
+}
+
 }  // namespace
 
 namespace xm_internal {
@@ -504,7 +995,81 @@ static int64_t n_tiles_of(const xm_batch* b) { return (b->n_events + kTile - 1) 
 
 size_t scan_scratch_bytes(const xm_batch* b) {
   const int64_t nt = n_tiles_of(b);
-  return 256 + size_t(nt) * (2 * sizeof(Mono) + 4 * kThreads) + 256;
+  const size_t flat = 256 + size_t(nt) * (2 * sizeof(Mono) + 4 * kThreads) + 256;
+  const size_t chunks = 256 + size_t(1024) * XM_K1C_CTAS_PER_SM * sizeof(ChunkSum);   // <= 512 SMs
+  return std::max(flat, chunks);
+}
+
+// K1c's tensor map: the events as rows of 16 x 8-byte words, 128-row boxes,
+// 128-byte swizzle. cuTensorMapEncodeTiled comes from the driver through the
+// runtime's entry-point query (no link against libcuda).
+static bool encode_event_map(const void* base, int64_t rows, CUtensorMap* tm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {16, cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, cuuint32_t(kCRows)};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// K1 path: K1t when every trace fits one CTA's trace loop (<= kTraceMax
+// events; measured faster there), else K1c; env XM_K1 = c | t | f(lat)
+// forces one for tooling and tests
+static char k1_path(const xm_batch* b) {
+  const char* e = getenv("XM_K1");
+  if (e && (e[0] == 't' || e[0] == 'f' || e[0] == 'c')) return e[0];
+  return b->max_events <= uint32_t(kTraceMax) ? 't' : 'c';
+}
+
+static int launch_chunks(const xm_batch* b, const UnitConfig& u, void* d_scratch, xm_result* d_out,
+                         cudaStream_t st, int* n_launches, bool* used) {
+  *used = false;
+  const void* ev = b->packed ? static_cast<const void*>(b->packed) : static_cast<const void*>(b->bytes);
+  if (b->n_events <= 0 || (reinterpret_cast<uintptr_t>(ev) & 15)) return 0;
+  const int64_t rows = b->n_events / 16;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (rows > 0 && !encode_event_map(ev, rows, &tm)) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CParams P{};
+  P.bytes = static_cast<const int64_t*>(ev);
+  P.off = b->off;
+  P.order = b->order;
+  P.n_traces = b->n_traces;
+  P.n_events = b->n_events;
+  P.rows = rows;
+  P.n_tiles = (b->n_events + kCTile - 1) / kCTile;
+  P.unit_shift = u.unit_shift;
+  P.u = u;
+  P.done = static_cast<unsigned int*>(d_scratch) + 1;
+  P.chunks = reinterpret_cast<ChunkSum*>(static_cast<char*>(d_scratch) + 256);
+  P.out = d_out;
+  const int G = int(std::min<int64_t>(P.n_tiles, int64_t(std::min(sms, 1024)) * XM_K1C_CTAS_PER_SM));
+  cudaError_t e = cudaMemsetAsync(d_scratch, 0, 8, st);
+  if (e != cudaSuccess) return int(e);
+  const bool dv = u.div_shift != 0;
+  auto kern = b->packed ? (dv ? k_scan_chunks<true, true> : k_scan_chunks<true, false>)
+                        : (dv ? k_scan_chunks<false, true> : k_scan_chunks<false, false>);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem);
+  if (e != cudaSuccess) return int(e);
+  kern<<<G, kCThreads, kCSmem, st>>>(tm, P);
+  *n_launches += 1;
+  *used = true;
+  return int(cudaGetLastError());
 }
 
 int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
@@ -528,7 +1093,13 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
   P.row_trace = reinterpret_cast<uint32_t*>(s);
   P.out = d_out;
   P.work = static_cast<unsigned int*>(d_scratch);
-  if (b->max_events <= uint32_t(kTraceMax)) {
+  const char path = k1_path(b);
+  if (path == 'c') {
+    bool used = false;
+    const int e = launch_chunks(b, u, d_scratch, d_out, st, n_launches, &used);
+    if (e || used) return e;
+  }
+  if (path != 'f' && b->max_events <= uint32_t(kTraceMax)) {
     // every trace is short enough for one CTA: the trace-per-CTA path
     cudaError_t e = cudaMemsetAsync(d_scratch, 0, 4, st);
     if (e != cudaSuccess) return int(e);

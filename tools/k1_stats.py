@@ -16,12 +16,16 @@ cfg = xm.Config(mode=1)
 out = xm.simulate_batch(dev, cfg)
 torch.cuda.synchronize()
 ts = []
+reps = int(os.environ.get("REPS", "20"))
 for _ in range(10):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record(); xm.simulate_batch(dev, cfg, out=out); e1.record(); torch.cuda.synchronize()
-    ts.append(e0.elapsed_time(e1))
+    e0.record()
+    for _r in range(reps):
+        xm.simulate_batch(dev, cfg, out=out)
+    e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) / reps)
 ms = float(np.median(ts))
 alg = 8 * b.n_events + 8 * (b.n_traces + 1) + 64 * b.n_traces
-print(json.dumps({"workload": wl, "rep": rep, "n_events": b.n_events, "ms": ms, "min_ms": min(ts),
+print(json.dumps({"path": os.environ.get("XM_K1", "c"), "workload": wl, "rep": rep, "n_events": b.n_events, "ms": ms, "min_ms": min(ts),
                   "GBps": alg / (ms / 1e3) / 1e9, "ev_per_s": b.n_events / (ms / 1e3),
                   "launches": xm.last_launch_count()}))
