@@ -501,23 +501,24 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
 }
 
 
-// ---- K1c: contiguous event chunks streamed by TMA (the default K1 path) ------
+// ---- K1c: contiguous event chunks streamed by TMA -----------------------------
 //
 // The same quantity as K1t (max prefix sum of +-s per trace and its first
-// index), but trace-oblivious: the batch's events are cut into G contiguous
-// chunks of whole 2048-event tiles, one per persistent CTA, so every CTA
-// streams an equal share at full rate no matter how long its traces are, and
-// no trace start waits on a work counter. Tiles arrive by TMA
-// (cp.async.bulk.tensor.2d, the events viewed as rows of 16 words with the
-// 128-byte swizzle, so each thread's 8 consecutive events read back without
-// bank conflicts) into a kCStages-deep mbarrier ring, issued kCStages-1 tiles
-// ahead by one elected thread. A tile without a trace start (the common case)
-// is one piece: a warp scan + arg-max per warp and a fold onto the CTA's
-// running piece. Otherwise a segmented scan of (starts-here flag, piece,
-// trace): traces that start and end inside the chunk are finished in place;
-// each chunk leaves its head piece (events before its first trace start) and
-// its tail piece (from its last trace start), and the last CTA to finish
-// folds those across chunks (the same segmented scan over G elements).
+// index), but trace-oblivious: the batch's events are cut into contiguous
+// chunks of whole tiles, one per WARP of a persistent grid, so every warp
+// streams an equal share no matter how long the traces are, no trace start
+// waits on a work counter, and no barrier couples the warps of a CTA while
+// they stream. Each warp's tiles arrive by TMA (cp.async.bulk.tensor.2d; the
+// events viewed as rows of 16 words with the 128-byte swizzle, so each lane's
+// consecutive events read back without bank conflicts) into the warp's own
+// kCStages-deep mbarrier ring, kCStages tiles ahead, issued by lane 0. A tile
+// without a trace start (the common case) is one piece: a warp scan + arg-max
+// folded onto the warp's running piece. Otherwise a segmented scan of
+// (starts-here flag, piece, trace): traces that start and end inside the
+// warp's chunk are finished in place. Each chunk leaves its head piece (events
+// before its first trace start) and tail piece (from its last start); warp 0
+// folds its CTA's chunk records into one, and the last CTA to finish folds
+// the CTA records (the same segmented scan).
 // HBM: 8 B/event read once + 64 B/trace written.
 #ifndef XM_K1C_PER
 #define XM_K1C_PER 8
@@ -533,15 +534,16 @@ __global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
 #endif
 constexpr int kCThreads = XM_K1C_THREADS;
 constexpr int kCWarps = kCThreads / 32;
-constexpr int kCPer = XM_K1C_PER;                  // consecutive events per thread (8 or 16)
-constexpr int kCTile = kCThreads * kCPer;          // events per tile (16 per 128-byte row)
-constexpr int kCRows = kCTile / 16;                // TMA box rows (<= 256)
+constexpr int kCPer = XM_K1C_PER;                  // consecutive events per lane (8 or 16)
+constexpr int kCTile = 32 * kCPer;                 // events per warp tile (16 per 128-byte row)
+constexpr int kCRows = kCTile / 16;                // TMA box rows
+constexpr int kCTileBytes = kCTile * 8;            // a multiple of 1024 (the swizzle atom)
 constexpr int kCStages = XM_K1C_STAGES;
-constexpr int kCSmem = kCStages * kCTile * 8 + 1024;      // + 1024 for the swizzle alignment
-constexpr int kCList = kCTile + 64;               // trace starts listed per (re)fill: a refill
+constexpr int kCSmem = kCWarps * kCStages * kCTileBytes + 1024;   // + the swizzle alignment
+constexpr int kCList = kCTile + 64;                // trace starts listed per (re)fill: a refill
                                                    // from a tile's first start covers the tile
-static_assert(kCPer == 8 || kCPer == 16, "K1c: 8 or 16 events per thread");
-static_assert(kCRows <= 256, "K1c: TMA box");
+static_assert(kCPer == 8 || kCPer == 16, "K1c: 8 or 16 events per lane");
+static_assert(kCTileBytes % 1024 == 0, "K1c: swizzle atom");
 
 // segmented-scan element: a piece (sum, max prefix or kNeg if empty, global
 // index of its first maximum), whether a trace starts inside it (f), and the
@@ -703,7 +705,7 @@ __device__ void c_fixup(const CParams& P, int G, SegE* s_w) {
   if (tid == 0 && carry.f) c_write(P, carry.tr, carry.mx, carry.arg);   // ends at the last event
 }
 
-// warp 0: list the distinct trace starts at or after trace jn (the last trace
+// one warp: list the distinct trace starts at or after trace jn (the last trace
 // of a run of equal offsets; the earlier ones are empty) below `end`, up to
 // kCList of them, as chunk-relative positions; returns (count, next jn) and
 // whether every start below `end` is listed
@@ -732,59 +734,89 @@ __device__ __forceinline__ void list_starts(const CParams& P, int64_t& jn, int64
   }
 }
 
+// the pieces of a run of records (chunk heads and tails) in order: the traces
+// that end inside the run are finished; returns the run's own record. One warp,
+// n <= 32 records, the carry-in of the run is the identity.
+__device__ ChunkSum fold_records(const CParams& P, const ChunkSum* rec, int n) {
+  const int lane = threadIdx.x & 31;
+  ChunkSum cs{};
+  SegE e = seg_id(), h = seg_id();
+  if (lane < n) {
+    cs = rec[lane];
+    h = SegE{cs.h_sum, cs.h_mx, cs.h_arg, -1, false};
+    e = cs.has ? SegE{cs.t_sum, cs.t_mx, cs.t_arg, cs.t_tr, true} : h;
+  }
+  const SegE inc = warp_seg_scan(e, lane);
+  SegE cin = shfl_up_seg(inc, 1);
+  if (lane == 0) cin = seg_id();
+  const SegE dn = seg_op(cin, h);
+  const bool has = lane < n && cs.has;
+  if (has && cin.f) c_write(P, cin.tr, dn.mx, dn.arg);   // ends at this record's first start
+  const unsigned hm = __ballot_sync(kFull, has && !cin.f);   // the run's first start
+  const SegE tot = shfl_seg(inc, 31);
+  ChunkSum r{};
+  if (hm) {
+    const SegE hh = shfl_seg(dn, __ffs(hm) - 1);
+    r = ChunkSum{hh.sum, hh.mx, hh.arg, tot.sum, tot.mx, tot.arg, tot.tr, 1, 0};
+  } else {
+    r = ChunkSum{tot.sum, tot.mx, tot.arg, 0, kNeg, -1, -1, 0, 0};
+  }
+  return r;
+}
+
 template <bool kPacked, bool kDiv>
 __global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(const __grid_constant__ CUtensorMap tm,
                                                            CParams P) {
   extern __shared__ unsigned char c_dsm[];
-  __shared__ __align__(8) unsigned long long s_bar[kCStages];
-  __shared__ uint32_t s_pos[kCList];             // the chunk's trace starts (chunk-relative)
-  __shared__ int32_t s_tr[kCList];               // ... and the trace starting there
-  __shared__ int s_cnt, s_all;
-  __shared__ long long s_jn;
-  __shared__ SegE s_w[2][kCWarps];
-  __shared__ SegE s_run[2];                      // the chunk through tile k (k & 1), by warp 0
-  __shared__ SegE s_head;
+  __shared__ __align__(8) unsigned long long s_bar[kCWarps][kCStages];
+  __shared__ uint32_t s_pos[kCWarps][kCList];    // each warp's listed trace starts (chunk-relative)
+  __shared__ int32_t s_tr[kCWarps][kCList];      // ... and the trace starting there
+  __shared__ ChunkSum s_rec[kCWarps];
+  __shared__ SegE s_w[kCWarps];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  unsigned char* ring = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(c_dsm) + 1023) & ~uintptr_t(1023));
+  // this warp's stages, as a shared-window address (1024-aligned: the swizzle atom)
+  const uint32_t ring = ((smem_u32(c_dsm) + 1023u) & ~1023u) + uint32_t(w * kCStages * kCTileBytes);
+  uint32_t* pos = s_pos[w];
+  int32_t* trs = s_tr[w];
   const int G = gridDim.x;
-  const int64_t c = blockIdx.x;
-  const int64_t k0 = c * P.n_tiles / G, k1 = (c + 1) * P.n_tiles / G;   // this chunk's tiles
+  const int64_t NW = int64_t(G) * kCWarps;
+  const int64_t u = int64_t(blockIdx.x) * kCWarps + w;              // this warp's chunk
+  const int64_t k0 = u * P.n_tiles / NW, k1 = (u + 1) * P.n_tiles / NW;
   const int nk = int(k1 - k0);
-  const int64_t c0 = k0 * kCTile;                                       // first event
-  const int64_t c1 = min(k1 * kCTile, P.n_events);                      // past the last
+  const int64_t c0 = k0 * kCTile;                                   // first event
+  const int64_t c1 = min(k1 * kCTile, P.n_events);                  // past the last
 
-  // prologue: barriers, the first tiles in flight, empty traces, the chunk's starts
-  if (tid == 0) {
-    for (int s = 0; s < kCStages; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[s])));
+  if (lane == 0) {
+    for (int st = 0; st < kCStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[w][st])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  __syncthreads();
-  auto issue = [&](int k) {                        // tile k0+k into stage k % kCStages
-    const int s = k % kCStages;
-    const uint32_t bar = smem_u32(&s_bar[s]);
+  __syncwarp();
+  auto issue = [&](int k, int st) {                // tile k0+k into stage st (= k % kCStages)
+    const uint32_t bar = smem_u32(&s_bar[w][st]);
     const int64_t row = (k0 + k) * kCRows;
     if (row < P.rows) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"(kCTile * 8) : "memory");
+                   "r"(kCTileBytes) : "memory");
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + size_t(s) * kCTile * 8)),
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(ring + uint32_t(st * kCTileBytes)),
           "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(int(row)), "r"(bar)
           : "memory");
     } else {                                       // past the tensor: read from global
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
     }
   };
-  if (tid == 0)
-    for (int k = 0; k < kCStages - 1 && k < nk; ++k) issue(k);
+  if (lane == 0)
+    for (int k = 0; k < kCStages && k < nk; ++k) issue(k, k);
   for (int64_t t = int64_t(blockIdx.x) * kCThreads + tid; t < P.n_traces;
        t += int64_t(G) * kCThreads)
     if (P.off[t + 1] == P.off[t]) P.out[P.order[t]] = xm_result{};   // empty trace
-  if (w == 0) {                                    // jn = first trace with off[jn] >= c0
+  // jn = first trace with off[jn] >= c0 (a 32-ary search), then the chunk's starts
+  int64_t jn;
+  {
     int64_t lo = 0, hi = P.n_traces;               // answer in [lo, hi]
     while (hi - lo > 32) {
       const int64_t step = (hi - lo + 31) / 32;
@@ -798,65 +830,127 @@ __global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(c
     }
     const int64_t x = lo + lane;
     const bool below = x < hi && P.off[x] < c0;
-    int64_t jn = lo + __popc(__ballot_sync(kFull, below));
-    int cnt;
-    bool all;
-    list_starts(P, jn, c0, c1, s_pos, s_tr, cnt, all);
-    if (lane == 0) { s_cnt = cnt; s_all = all; s_jn = jn; }
+    jn = lo + __popc(__ballot_sync(kFull, below));
   }
-  __syncthreads();
-  int cnt = s_cnt;                                 // listed starts (CTA-uniform)
-  bool all = s_all;
+  int cnt = 0;
+  bool all = true;
+  if (nk > 0) list_starts(P, jn, c0, c1, pos, trs, cnt, all);
+  __syncwarp();
   int bi = 0;                                      // first listed start not yet passed
 
-  SegE run = seg_id();                             // the chunk so far (warp 0's copy is live)
-  if (tid == 0) { s_run[1] = seg_id(); s_head = seg_id(); }
-  __syncthreads();
+  SegE run = seg_id();                             // this warp's chunk so far (warp-uniform)
+  SegE head = seg_id();                            // (the lane that closed the head piece)
+  bool head_here = false;
+  int st = 0;                                      // stage of tile k, and its phase
+  uint32_t phase = 0;
   for (int k = 0; k < nk; ++k) {
     const int64_t ts = (k0 + k) * kCTile;
     const int64_t te = min(ts + kCTile, P.n_events);
     const uint32_t rte = uint32_t(te - c0);
-    if (tid == 0 && k + kCStages - 1 < nk) issue(k + kCStages - 1);
-    if (!all && (bi == cnt || s_pos[cnt - 1] < rte)) {
+    if (!all && (bi == cnt || pos[cnt - 1] < rte)) {
       // (rare) unlisted starts may lie in this tile: relist from its first start
-      __syncthreads();
-      if (w == 0) {
-        int64_t jn = bi < cnt ? int64_t(s_tr[bi]) : int64_t(s_jn);
-        int nc;
-        bool na;
-        list_starts(P, jn, c0, c1, s_pos, s_tr, nc, na);
-        if (lane == 0) { s_cnt = nc; s_all = na; s_jn = jn; }
-      }
-      __syncthreads();
-      cnt = s_cnt;
-      all = s_all;
+      int64_t j = bi < cnt ? int64_t(trs[bi]) : jn;
+      __syncwarp();
+      list_starts(P, j, c0, c1, pos, trs, cnt, all);
+      __syncwarp();
+      jn = j;
       bi = 0;
     }
-    // starts in this tile: listed entries [bi, bi + nb) (each warp counts them)
+    // starts in this tile: listed entries [bi, bi + nb)
     int nb = 0;
     for (;;) {
       const int i = bi + nb + lane;
-      const bool in = i < cnt && s_pos[i] < rte;
+      const bool in = i < cnt && pos[i] < rte;
       const int m = __popc(__ballot_sync(kFull, in));
       nb += m;
       if (m < 32) break;
     }
-    const int s = k % kCStages;
-    mbar_wait(smem_u32(&s_bar[s]), uint32_t((k / kCStages) & 1));
-    const int64_t p0 = ts + int64_t(tid) * kCPer;  // first event of this thread
-    int64_t d[kCPer];
-    if (p0 + kCPer <= P.rows * 16) {
-      // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r & 7)
-      const unsigned char* st = ring + size_t(s) * kCTile * 8;
-      const int r = (tid * kCPer) >> 4;
-      const int j0 = (tid * kCPer & 15) >> 1;
+    mbar_wait(smem_u32(&s_bar[w][st]), phase);
+    const int64_t p0 = ts + int64_t(lane) * kCPer; // this lane's first event
+    const uint32_t sb = ring + uint32_t(st * kCTileBytes);
+    // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r & 7)
+    auto load_stage = [&](int64_t* d) {
+      const int r = (lane * kCPer) >> 4;
+      const int j0 = (lane * kCPer & 15) >> 1;
 #pragma unroll
       for (int q = 0; q < kCPer / 2; ++q) {
-        const int ch = (j0 + q) ^ (r & 7);
-        const longlong2 v = *reinterpret_cast<const longlong2*>(st + r * 128 + ch * 16);
-        d[2 * q] = v.x;
-        d[2 * q + 1] = v.y;
+        const uint32_t a = sb + uint32_t(r * 128 + (((j0 + q) ^ (r & 7)) << 4));
+        long long x, y;
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
+        d[2 * q] = x;
+        d[2 * q + 1] = y;
       }
+    };
+    // the warp's tile is whole and staged (every tile but the batch's last)
+    const bool full = te - ts == kCTile && ts + kCTile <= P.rows * 16;
+    int64_t d[kCPer];
+    bool done = false;
+    if constexpr (!kDiv) {
+      if (full && nb == 0) {
+        // ===== the common tile: no trace starts, no ragged end =====
+        // a2 in 32 bits: |request| < 2^40 (XM_MAX_REQUEST) makes |delta| =
+        // ceil(|b| / 2^sh) < 2^31, and while every |delta| of the tile is below
+        // 2^26 a lane's sums of up to 16 stay within int32; the warp scan is
+        // 64-bit. Otherwise (never on paper-shaped traces) the 64-bit path.
+        load_stage(d);
+        const int64_t msk = (1ll << P.unit_shift) - 1;
+        int32_t v[kCPer];
+        uint32_t orr = 0;
+#pragma unroll
+        for (int q = 0; q < kCPer; ++q) {
+          if constexpr (kPacked) {
+            const uint64_t m = uint64_t(d[q]) & ((1ull << 41) - 1);
+            const int32_t u = int32_t((m + uint64_t(msk)) >> P.unit_shift);
+            v[q] = (uint64_t(d[q]) >> 41) & 1 ? u : -u;
+          } else {
+            const int64_t b = d[q];
+            v[q] = int32_t((b + (b > 0 ? msk : 0)) >> P.unit_shift);   // floor for frees
+            if (uint32_t(int32_t(b >> 32) + 256) >= 512u) v[q] = INT32_MIN;
+          }
+          orr |= uint32_t(abs(v[q]));
+        }
+        int64_t sum, mx;
+        int ai = 0;
+        if (!__any_sync(kFull, orr >= (1u << 26))) {
+          int32_t s32 = v[0], m32 = v[0];
+#pragma unroll
+          for (int q = 1; q < kCPer; ++q) {
+            s32 += v[q];
+            if (s32 > m32) { m32 = s32; ai = q; }
+          }
+          sum = s32;
+          mx = m32;
+        } else {
+          sum = c_delta<kPacked, kDiv>(d[0], P);
+          mx = sum;
+#pragma unroll
+          for (int q = 1; q < kCPer; ++q) {
+            sum += c_delta<kPacked, kDiv>(d[q], P);
+            if (sum > mx) { mx = sum; ai = q; }
+          }
+        }
+        int64_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned long long uk = static_cast<unsigned long long>(incl - sum + mx) ^ 0x8000000000000000ull;
+        const unsigned khi = unsigned(uk >> 32), klo = unsigned(uk);
+        const unsigned mh = __reduce_max_sync(kFull, khi);
+        const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
+        const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
+        const int64_t wmx = static_cast<int64_t>((static_cast<unsigned long long>(mh) << 32 | ml) ^
+                                                 0x8000000000000000ull);
+        const int64_t warg = ts + int64_t(src) * kCPer + __shfl_sync(kFull, ai, src);
+        const int64_t wsum = __shfl_sync(kFull, incl, 31);
+        run = seg_op(run, SegE{wsum, wmx, warg, -1, false});
+        done = true;
+      }
+    }
+    if (!done) {
+    if (full || p0 + kCPer <= P.rows * 16) {
+      load_stage(d);
     } else {
 #pragma unroll
       for (int q = 0; q < kCPer; ++q)
@@ -865,22 +959,21 @@ __global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(c
     const int nv = int(max(int64_t(0), min(int64_t(kCPer), te - p0)));
 #pragma unroll
     for (int q = 0; q < kCPer; ++q) d[q] = q < nv ? c_delta<kPacked, kDiv>(d[q], P) : 0;
-    SegE* sw = s_w[k & 1];
-    // this thread's starts: listed entries [b, bend) below r0 + kCPer
+    // this lane's starts: listed entries [b, bi + nb) below r0 + kCPer
     const uint32_t r0 = uint32_t(p0 - c0);
     int b = bi + nb;
     if (nb) {
       int lo = bi, hi = bi + nb;                   // first start at or after r0
       while (lo < hi) {
         const int m = (lo + hi) >> 1;
-        if (s_pos[m] < r0) lo = m + 1; else hi = m;
+        if (pos[m] < r0) lo = m + 1; else hi = m;
       }
       b = lo;
     }
-    const bool mine = b < bi + nb && s_pos[b] < r0 + kCPer;
-    SegE cur, hd;
-    if (!mine) {
-      // ===== no trace starts here: one piece (sum, max prefix, first arg-max) =====
+    const bool mine = b < bi + nb && pos[b] < r0 + kCPer;
+    const bool wany = __any_sync(kFull, mine);    // warp-uniform
+    if (!wany) {
+      // ===== no trace starts in this tile: one piece =====
       int64_t sum = 0, mx = kNeg;
       int ai = -1;
 #pragma unroll
@@ -888,102 +981,104 @@ __global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(c
         sum += d[q];
         if (q < nv && sum > mx) { mx = sum; ai = q; }
       }
-      cur = SegE{sum, mx, ai < 0 ? -1 : p0 + ai, -1, false};
-    } else {
-      // ===== pieces split at the starts; traces wholly inside are finished =====
-      const int bend = bi + nb;
-      uint32_t nxt = s_pos[b];
-      cur = seg_id();
-      hd = seg_id();
-      bool seen = false;
-#pragma unroll
-      for (int q = 0; q < kCPer; ++q) {
-        if (q < nv) {
-          if (r0 + q == nxt) {
-            if (!seen) hd = cur;
-            else c_write(P, cur.tr, cur.mx, cur.arg);
-            seen = true;
-            cur = SegE{0, kNeg, -1, s_tr[b], true};
-            ++b;
-            nxt = b < bend ? s_pos[b] : 0xFFFFFFFFu;
-          }
-          cur.sum += d[q];
-          if (cur.sum > cur.mx) { cur.mx = cur.sum; cur.arg = p0 + q; }
-        }
-      }
-    }
-    SegE inc;
-    const bool wany = __any_sync(kFull, mine);    // warp-uniform
-    if (!wany) {
-      // warp without starts: exclusive prefix of the sums, first arg-max
-      int64_t incl = cur.sum;
+      int64_t incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int64_t y = __shfl_up_sync(kFull, incl, o);
         if (lane >= o) incl += y;
       }
       const unsigned long long uk =
-          static_cast<unsigned long long>(cur.mx == kNeg ? kNeg : incl - cur.sum + cur.mx) ^
-          0x8000000000000000ull;
+          static_cast<unsigned long long>(mx == kNeg ? kNeg : incl - sum + mx) ^ 0x8000000000000000ull;
       const unsigned khi = unsigned(uk >> 32), klo = unsigned(uk);
       const unsigned mh = __reduce_max_sync(kFull, khi);
       const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
       const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
       const int64_t wmx = static_cast<int64_t>((static_cast<unsigned long long>(mh) << 32 | ml) ^
                                                0x8000000000000000ull);
-      const int64_t warg = __shfl_sync(kFull, cur.arg, src);
-      inc = SegE{incl, wmx, wmx == kNeg ? -1 : warg, -1, false};
+      const int64_t warg = p0 + __shfl_sync(kFull, ai, src) - (int64_t(lane) - src) * kCPer;
+      const int64_t wsum = __shfl_sync(kFull, incl, 31);
+      run = seg_op(run, SegE{wsum, wmx, wmx == kNeg ? -1 : warg, -1, false});
     } else {
-      inc = warp_seg_scan(cur, lane);
-    }
-    if (lane == 31) sw[w] = inc;
-    __syncthreads();                               // sw complete; the stage may be refilled
-    if (wany) {
-      const SegE ex = shfl_up_seg(inc, 1);         // lanes before this one
+      // ===== pieces split at the starts; traces wholly inside a lane are finished =====
+      SegE cur = seg_id(), hd = seg_id();
+      if (!mine) {
+        int64_t sum = 0, mx = kNeg;
+        int ai = -1;
+#pragma unroll
+        for (int q = 0; q < kCPer; ++q) {
+          sum += d[q];
+          if (q < nv && sum > mx) { mx = sum; ai = q; }
+        }
+        cur = SegE{sum, mx, ai < 0 ? -1 : p0 + ai, -1, false};
+      } else {
+        const int bend = bi + nb;
+        uint32_t nxt = pos[b];
+        bool seen = false;
+#pragma unroll
+        for (int q = 0; q < kCPer; ++q) {
+          if (q < nv) {
+            if (r0 + q == nxt) {
+              if (!seen) hd = cur;
+              else c_write(P, cur.tr, cur.mx, cur.arg);
+              seen = true;
+              cur = SegE{0, kNeg, -1, trs[b], true};
+              ++b;
+              nxt = b < bend ? pos[b] : 0xFFFFFFFFu;
+            }
+            cur.sum += d[q];
+            if (cur.sum > cur.mx) { cur.mx = cur.sum; cur.arg = p0 + q; }
+          }
+        }
+      }
+      const SegE inc = warp_seg_scan(cur, lane);
+      const SegE ex = shfl_up_seg(inc, 1);
       if (mine) {
-        // finish the trace open at this thread's first start: the chunk before
-        // this tile (warp 0's fold, s_run), the warps and lanes before this one
-        SegE pre = s_run[(k + 1) & 1];
-        for (int j = 0; j < w; ++j) pre = seg_op(pre, sw[j]);
-        const SegE cin = lane ? seg_op(pre, ex) : pre;
+        // finish the trace open at this lane's first start
+        const SegE cin = lane ? seg_op(run, ex) : run;
         const SegE dn = seg_op(cin, SegE{hd.sum, hd.mx, hd.arg, -1, false});
         if (cin.f) {
           c_write(P, cin.tr, dn.mx, dn.arg);       // started in this chunk: finished here
-        } else {                                   // the chunk's head piece (one thread)
-          s_head = dn;
+        } else {                                   // the chunk's head piece (one lane)
+          head = dn;
+          head_here = true;
         }
       }
+      run = seg_op(run, shfl_seg(inc, 31));
     }
-    if (w == 0) {                                  // warp 0 folds the tile onto the chunk
-      SegE e = lane < kCWarps ? sw[lane] : seg_id();
-#pragma unroll
-      for (int o = 1; o < kCWarps; o <<= 1) {
-        const SegE y = shfl_up_seg(e, o);
-        if (lane >= o) e = seg_op(y, e);
-      }
-      run = seg_op(run, shfl_seg(e, kCWarps - 1));
-      if (lane == 0) s_run[k & 1] = run;
     }
+    __syncwarp();                                  // every lane has read the stage
+    if (lane == 0 && k + kCStages < nk) issue(k + kCStages, st);
+    if (++st == kCStages) { st = 0; phase ^= 1u; }
     bi += nb;
   }
-  // chunk record: head (or the whole chunk when no trace starts in it) and tail
-  __syncthreads();                                 // s_head
-  if (tid == 0) {                                  // (warp 0 holds the chunk's piece)
+  // this warp's chunk record, then the CTA's, then (last CTA) the grid's
+  const unsigned hm = __ballot_sync(kFull, head_here);
+  if (lane == 0) {
     ChunkSum cs;
     if (run.f) {
-      const SegE h = s_head;
-      cs = ChunkSum{h.sum, h.mx, h.arg, run.sum, run.mx, run.arg, run.tr, 1, 0};
+      cs = ChunkSum{0, kNeg, -1, run.sum, run.mx, run.arg, run.tr, 1, 0};
     } else {
       cs = ChunkSum{run.sum, run.mx, run.arg, 0, kNeg, -1, -1, 0, 0};
     }
-    P.chunks[c] = cs;
-    __threadfence();
-    s_last = atomicAdd(P.done, 1u) == unsigned(G - 1);
+    s_rec[w] = cs;
+  }
+  if (hm) {
+    const SegE h = shfl_seg(head, __ffs(hm) - 1);
+    if (lane == 0) { s_rec[w].h_sum = h.sum; s_rec[w].h_mx = h.mx; s_rec[w].h_arg = h.arg; }
+  }
+  __syncthreads();
+  if (w == 0) {
+    const ChunkSum cs = fold_records(P, s_rec, kCWarps);
+    if (lane == 0) {
+      P.chunks[blockIdx.x] = cs;
+      __threadfence();
+      s_last = atomicAdd(P.done, 1u) == unsigned(G - 1);
+    }
   }
   __syncthreads();
   if (s_last) {
     __threadfence();
-    c_fixup(P, G, s_w[0]);
+    c_fixup(P, G, s_w);
   }
 }
 
@@ -1017,7 +1112,7 @@ static bool encode_event_map(const void* base, int64_t rows, CUtensorMap* tm) {
   }
   const cuuint64_t dims[2] = {16, cuuint64_t(rows)};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {16, cuuint32_t(kCRows)};
+  const cuuint32_t box[2] = {16, cuuint32_t(kCRows)};   // one warp tile
   const cuuint32_t es[2] = {1, 1};
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1058,7 +1153,9 @@ static int launch_chunks(const xm_batch* b, const UnitConfig& u, void* d_scratch
   P.done = static_cast<unsigned int*>(d_scratch) + 1;
   P.chunks = reinterpret_cast<ChunkSum*>(static_cast<char*>(d_scratch) + 256);
   P.out = d_out;
-  const int G = int(std::min<int64_t>(P.n_tiles, int64_t(std::min(sms, 1024)) * XM_K1C_CTAS_PER_SM));
+  const int64_t by_tiles = (P.n_tiles + kCWarps - 1) / kCWarps;          // >= 1 tile per warp
+  const int G = int(std::max<int64_t>(1, std::min<int64_t>(by_tiles,
+                                                           int64_t(std::min(sms, 1024)) * XM_K1C_CTAS_PER_SM)));
   cudaError_t e = cudaMemsetAsync(d_scratch, 0, 8, st);
   if (e != cudaSuccess) return int(e);
   const bool dv = u.div_shift != 0;
