@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "xm_internal.h"
@@ -338,6 +339,10 @@ Layout layout(const xm_instants* in) {
   const int64_t budget_ctas = std::max<int64_t>(1, (int64_t(2) << 30) / per_cta);
   const int64_t cap_ctas = std::min<int64_t>(int64_t(sms) * kCtasPerSm, budget_ctas);
   L.ctas = uint32_t(want_ctas < cap_ctas ? (want_ctas > 0 ? want_ctas : 1) : cap_ctas);
+  if (const char* v = getenv("XM_K5_CTAS")) {        // tooling: cap the concurrency
+    const long c = strtol(v, nullptr, 10);
+    if (c > 0 && uint32_t(c) < L.ctas) L.ctas = uint32_t(c);
+  }
   L.n_slots = L.ctas * kWarps;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t o = 256;                                   // header: work counter
