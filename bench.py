@@ -152,17 +152,38 @@ def ncu_traffic(kernel="k_replay"):
         return None, None
 
 
-def ncu_issue(kernel="k_replay"):
+def peaks_clock():
+    """The SM clock MEASURED_PEAKS.json records (when no live clock sample)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("sm_max_mhz") or 0) or None
+    except Exception:
+        return None
+
+
+def ncu_issue(kernel="k_replay", kernel_ms=None, sm_mhz=None, events=None):
     """Warp-issue efficiency (smsp__issue_active %) and warp-instructions per
-    launch from the committed ncu summary (the north_star's second measure)."""
+    launch from the committed ncu summary (the north_star's second measure),
+    plus the issue roofline of this run: frac = warp-instructions / (SMs x 4
+    schedulers x SM clock x the live kernel time), one warp-instruction per
+    scheduler per cycle being the ceiling."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             k = json.load(f)["kernels"][kernel]
-        return {"issue_active_pct": k["issue_active_pct"],
-                "warp_instructions_per_launch": k["warp_instructions"],
-                "achieved_occupancy_pct": k["achieved_occupancy_pct"],
-                "source": "profiles/ncu_summary.json (" + k.get("source", "") + ")"}
+        r = {"issue_active_pct": k["issue_active_pct"],
+             "warp_instructions_per_launch": k["warp_instructions"],
+             "achieved_occupancy_pct": k["achieved_occupancy_pct"],
+             "source": "profiles/ncu_summary.json (" + k.get("source", "") + ")"}
+        if kernel_ms and sm_mhz:
+            import torch
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            cap = sms * 4 * sm_mhz * 1e6 * kernel_ms / 1e3
+            r.update({"frac": k["warp_instructions"] / cap, "sms": sms, "sm_mhz": sm_mhz,
+                      "ceiling_warp_instructions": cap})
+            if events:
+                r["warp_instructions_per_event"] = k["warp_instructions"] / events
+        return r
     except Exception:
         return None
 
@@ -480,10 +501,11 @@ def main():
             + (8 * batch.n_traces if has_cap else 0)
         e2e = {"value": done / dt_dev_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw),
                "d2h_bytes_per_step": int(128 * batch.n_traces), "ms_per_step": dt_dev_raw * 1e3,
-               "api": "xm_simulate_raw: the caller's raw arrays (page-locked host memory) read "
-                      "over PCIe by the device loader (K5 keyed by raw block id: validation "
-                      "S:231/S:249/S:258, dense ids, LPT-stored wire arrays) -> k_replay -> "
-                      "results + loader verdicts to the host, every step",
+               "api": "xm_simulate_raw: the caller's raw arrays (page-locked host memory) "
+                      "copied to the device in 24 chunks of whole traces on a copy stream, "
+                      "overlapping the device loader that waits per trace (K5 keyed by raw block "
+                      "id: validation S:231/S:249/S:258, dense ids, LPT-stored wire arrays) -> "
+                      "k_replay -> results + loader verdicts to the host, every step",
                "host_loader": {"value": done / dt_raw, "ms_per_step": dt_raw * 1e3,
                                "api": "xm_load_traces (host validation, dense ids, page-locked "
                                       "packing) + xm_simulate_host, every step",
@@ -508,7 +530,9 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "kernel": "k_replay",
             "alg_bytes_per_launch": alg, "kernel_ms": kern_ms, "peak_source": peak_src,
-            "traffic_source": tsrc, "issue": ncu_issue(),
+            "traffic_source": tsrc,
+            "issue": ncu_issue("k_replay", kern_ms,
+                               (clocks or {}).get("sm_mhz") or peaks_clock(), local_done),
             "note": "K2 is a serial integer state machine per trace (issue/latency-bound); "
                     "HBM fraction reported as the north_star asks, warp-issue efficiency "
                     "from ncu in 'issue'"}

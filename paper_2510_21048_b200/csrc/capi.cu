@@ -418,7 +418,7 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
 // ---- raw host traces -> device loader -> replay (xm_simulate_raw) -----------------
 namespace {
 struct RawLayout {
-  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, scratch, total;
+  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, scratch, total;
 };
 
 struct RawShape {
@@ -442,6 +442,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.woff = p; p += al(8 * (T + 1));
   L.wnids = p; p += al(4 * T);
   L.out = p; p += al(sizeof(xm_result) * T);
+  L.ready = p; p += al(sizeof(uint32_t));
   L.scratch = p;
   xm_batch b{};
   b.n_traces = R.T;
@@ -518,14 +519,67 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
   });
-  // events: read in place by the loader kernel when page-locked, else copied
+  // events. Page-locked (the usual case): copied by the DMA engine in chunks
+  // of whole traces in caller order on the library's copy stream, each chunk
+  // followed by a stream-ordered write of "traces resident so far" that the
+  // loader's warps wait on (trace k's warp starts once k is resident), so the
+  // transfer overlaps the loader (the copy engine moves ~55 GB/s where the
+  // warps reading host memory in place managed ~36). XM_RAW_INPUT=direct
+  // reads in place instead (tooling). Pageable: copied first.
   const int64_t* d_bytes = static_cast<const int64_t*>(mapped(h_bytes));
   const uint32_t* d_tag = static_cast<const uint32_t*>(mapped(h_tag));
-  if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
-  if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
+  const char* rin = std::getenv("XM_RAW_INPUT");
+  const bool direct = rin && !std::strcmp(rin, "direct");
+  const bool streamed = d_bytes && d_tag && !direct && R.E > 0;
   cp(L.off, h_off, 8 * size_t(R.T + 1));
   cp(L.order, order.data(), 4 * size_t(R.T));
   if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
+  uint32_t* ready = reinterpret_cast<uint32_t*>(w + L.ready);
+  Pipe* pp = nullptr;
+  if (streamed) {
+    if (e == cudaSuccess) e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = get_pipe(&pp);
+    // the copy stream starts after everything already queued on `stream`
+    if (e == cudaSuccess) e = cudaEventRecord(pp->start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, pp->start, 0);
+    const WriteValue32Fn wv = write_value32();
+    static thread_local std::vector<uint32_t> chunk_end;   // outlives the async copies
+    chunk_end.clear();
+    const int kChunks = 24;
+    int64_t t = 0, ev0 = 0;
+    for (int c = 0; c < kChunks && t < R.T && e == cudaSuccess; ++c) {
+      // whole traces up to about (c+1)/kChunks of the events; the copied range
+      // ends on a 32-event boundary (no cache line holds events of two chunks)
+      const int64_t goal = (R.E * (c + 1)) / kChunks;
+      while (t < R.T && (h_off[t + 1] <= goal || c == kChunks - 1)) ++t;
+      if (t == 0) continue;
+      int64_t ev1 = h_off[t];
+      if (t < R.T) ev1 = std::min<int64_t>(R.E, (ev1 + 31) & ~int64_t(31));
+      else ev1 = R.E;
+      if (ev1 > ev0) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(w + L.bytes + 8 * size_t(ev0), h_bytes + ev0,
+                                                  8 * size_t(ev1 - ev0), cudaMemcpyHostToDevice, pp->cs);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(w + L.tag + 4 * size_t(ev0), h_tag + ev0,
+                                                  4 * size_t(ev1 - ev0), cudaMemcpyHostToDevice, pp->cs);
+        ev0 = ev1;
+      }
+      chunk_end.push_back(uint32_t(t));
+      if (e != cudaSuccess) break;
+      if (wv) {
+        if (wv(pp->cs, reinterpret_cast<unsigned long long>(ready), uint32_t(t), 0) != 0) e = cudaErrorUnknown;
+      } else {
+        e = cudaMemcpyAsync(ready, &chunk_end.back(), sizeof(uint32_t), cudaMemcpyHostToDevice, pp->cs);
+      }
+    }
+    if (e == cudaSuccess && t < R.T) e = cudaErrorUnknown;      // (never: the last chunk takes all)
+    // every copy and counter write is queued before the kernel that waits on them
+    if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
+    d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
+    d_tag = reinterpret_cast<const uint32_t*>(w + L.tag);
+  } else if (!direct || !d_bytes || !d_tag) {
+    if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
+    if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
+  }
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
   int launches = 0;
   xm_lifecycle* d_rec = reinterpret_cast<xm_lifecycle*>(w + L.rec);
@@ -533,7 +587,14 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
                          R.max_events, w + L.k5, d_rec, reinterpret_cast<const uint32_t*>(w + L.order),
                          reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
                          reinterpret_cast<int64_t*>(w + L.woff), reinterpret_cast<uint32_t*>(w + L.wnids),
-                         stream, &launches);
+                         stream, &launches, streamed ? ready : nullptr);
+  // `stream` resumes (the replay, result download, later users of the
+  // workspace) only after the copies too, also when the launch failed
+  if (streamed) {
+    const cudaError_t e2 = cudaStreamWaitEvent(st, pp->copied, 0);
+    if (!ek && e2 != cudaSuccess)
+      return set_error(XM_ECUDA, std::string("stream wait: ") + cudaGetErrorString(e2));
+  }
   if (ek) return set_error(XM_ECUDA, std::string("xm_simulate_raw loader: ") + cudaGetErrorString(cudaError_t(ek)));
   xm_batch b{};
   b.bytes = reinterpret_cast<const int64_t*>(w + L.wbytes);

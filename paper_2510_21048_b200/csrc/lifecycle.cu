@@ -78,6 +78,8 @@ struct LParams {
   uint8_t* mismatch;
   xm_lifecycle* rec;
   unsigned int* work;
+  const uint32_t* ready;                  // loader mode, streamed input: traces (caller
+                                          // order) whose events are resident, or null
 };
 
 __device__ __forceinline__ uint32_t hash_addr(uint64_t a, uint32_t bits) {
@@ -95,6 +97,18 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     if (lane == 0) k = atomicAdd(P.work, 1u);
     k = __shfl_sync(kFull, k, 0);
     if (int64_t(k) >= P.n_traces) break;
+    if (P.ready) {                          // wait until trace k's events have landed
+      uint32_t nap = 256;
+      for (;;) {
+        uint32_t r = 0;
+        if (lane == 0)
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.ready) : "memory");
+        if (__shfl_sync(kFull, r, 0) > k) break;
+        __nanosleep(nap);
+        nap = min(nap * 2, 4096u);
+      }
+      __syncwarp();
+    }
     const unsigned gen = k + 1;
     const int64_t e0 = P.off[k];
     const int n = int(P.off[k + 1] - e0);
@@ -117,12 +131,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       const int li = base + int(lane);
       const bool valid = li < n;
       uint64_t a = valid ? (P.tag ? 0ull : P.addr[e0 + li]) : ~0ull - lane;
-      int64_t b = valid ? P.bytes[e0 + li] : 0;
+      int64_t b = valid ? __ldcg(reinterpret_cast<const long long*>(P.bytes) + e0 + li) : 0;
       // |bytes| >= XM_MAX_REQUEST is out of the replay's range: invalid like 0
       if (b >= int64_t(XM_MAX_REQUEST) || b <= -int64_t(XM_MAX_REQUEST)) b = 0;
       uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
       if (P.tag) {                          // loader mode: the raw block id is the key
-        const uint32_t g = valid ? P.tag[e0 + li] : 0u;
+        const uint32_t g = valid ? __ldcg(P.tag + e0 + li) : 0u;
         a = valid ? uint64_t(g & 0x0FFFFFFFu) : a;
         s = g >> 28;
       }
@@ -521,7 +535,7 @@ size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events) {
 int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* d_off, int64_t T,
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
-                  uint32_t* w_nids, void* stream, int* n_launches) {
+                  uint32_t* w_nids, void* stream, int* n_launches, const uint32_t* ready) {
   xm_instants in{};
   in.n_traces = T;
   in.n_events = E;
@@ -547,6 +561,7 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
   P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
+  P.ready = ready;
   k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
   k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, d_order, T, w_off);
   const int64_t want = (T + 7) / 8;

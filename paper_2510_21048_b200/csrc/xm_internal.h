@@ -73,6 +73,7 @@ size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events);
 int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* d_off, int64_t T,
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
-                  uint32_t* w_nids, void* stream, int* n_launches);
+                  uint32_t* w_nids, void* stream, int* n_launches,
+                  const uint32_t* ready = nullptr);
 
 }  // namespace xm_internal
