@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-k1", action="store_true",
+                    help="skip the K1 measurement (launch lists of the step alone)")
     ap.add_argument("--smem-per-warp", type=int, default=0)
     ap.add_argument("--warps-per-cta", type=int, default=0)
     ap.add_argument("--json-out", default="")
@@ -541,6 +543,8 @@ def main():
     # timed on the same resident events (capacities dropped: the mode needs none)
     k1 = None
     try:
+        if args.no_k1:
+            raise RuntimeError("skipped (--no-k1)")
         db1 = xm.DeviceBatch(db.bytes, db.tag, db.off, db.n_ids, db.order, None, db.n_traces,
                              db.n_events, db.max_ids, db.max_events)
         cfg1 = xm.Config(mode=1)

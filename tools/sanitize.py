@@ -28,7 +28,16 @@ tb = fuzz.spec1_corpus(1, 1000, salt=5)
 big = concat([tb] * 70)
 long = concat([fuzz.fragmentation_stress(40000, 1024, "long")])                # > 65536 events
 trl = xm.load_traces(long.bytes, long.tag, long.off)
+xm.peaks(xm.simulate_batch(trl.to_device(), xm.Config(mode=1)))               # K1c (auto: > 65536)
+os.environ["XM_K1"] = "c"
+xm.peaks(xm.simulate_batch(dev1, xm.Config(mode=1)))                           # K1c, short traces
+xm.peaks(xm.simulate_batch(tr.to_device(packed=True), xm.Config(mode=1)))      # K1c, packed
+os.environ["XM_K1"] = "f"
 xm.peaks(xm.simulate_batch(trl.to_device(), xm.Config(mode=1)))               # K1 flat
+del os.environ["XM_K1"]
+pin_b = torch.from_numpy(b.bytes).pin_memory().numpy()
+pin_t = torch.from_numpy(b.tag.view(np.int32)).pin_memory().numpy().view(np.uint32)
+xm.simulate_raw(pin_b, pin_t, b.off, xm.Config(), capacity=b.capacity)        # raw: DMA chunks + loader
 d = mc5.describe(np.arange(50))
 pool = xm.Templates(*mc5.template_pool())
 xm.peaks(xm.simulate_batch(xm.expand_templates(pool, d["tpl"], d["b"], d["seed"],
