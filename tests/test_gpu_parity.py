@@ -260,28 +260,29 @@ def test_allocated_only_mode_stepped_traces(packed):
     assert_parity(b, h, o, fields=["peak_allocated", "peak_allocated_idx", "events_done"])
 
 
-@pytest.mark.parametrize("spw,wpc", [(6144, 16), (12288, 16), (3072, 16)])
-def test_heap_page_handoffs_under_contention(spw, wpc):
+def test_heap_page_handoffs_under_contention():
     """The shared-memory heap's page hand-offs between warps (FIFO admission,
     free-list growth into pages another warp just released, release on trace
     end: fenced atomics on the page bitmap, replay.cu heap_*) under heavy
-    contention -- 16 warps on a heap of a few dozen pages, traces of very
+    contention -- 16 warps on heaps of 6-24 KB per warp, traces of very
     different footprints -- repeated; every run bit-exact vs the oracle, and
-    the contended paths provably taken (the kernel's own counters)."""
+    the contended paths provably taken (the kernel's own counters: admission
+    waits on the small heaps, free-list growths on the larger ones)."""
     b = concat([fuzz.spec1_corpus(600, 1000, salt=31), fuzz.small_size_corpus(300, 600, salt=32),
                 fuzz.capacity_corpus(200, 800, salt=33), fuzz.fragmentation_stress(3000, 512, "fr")])
     o = oracle_run(b)
     tr = xm.load_traces(b.bytes, b.tag, b.off)
     dev = tr.to_device(capacity=b.capacity)
-    cfg = xm.Config(smem_per_warp=spw, warps_per_cta=wpc)
     waits = grows = 0
-    for _ in range(4):
-        h, _ = xm.peaks(xm.simulate_batch(dev, cfg))
-        assert_parity(b, h, o)
-        scr = dev._scratch[(cfg.mode, cfg.smem_per_warp, cfg.warps_per_cta)]
-        st = scr[128:160].view(torch.int32).cpu().numpy()     # K2's stats (replay.cu)
-        waits += int(st[2])
-        grows += int(st[4])
+    for spw in (3072, 6144, 12288, 24576):
+        cfg = xm.Config(smem_per_warp=spw, warps_per_cta=16)
+        for _ in range(3):
+            h, _ = xm.peaks(xm.simulate_batch(dev, cfg))
+            assert_parity(b, h, o)
+            scr = dev._scratch[(cfg.mode, cfg.smem_per_warp, cfg.warps_per_cta)]
+            st = scr[128:160].view(torch.int32).cpu().numpy()     # K2's stats (replay.cu)
+            waits += int(st[2])
+            grows += int(st[4])
     assert waits > 0 and grows > 0, (waits, grows)
 
 

@@ -52,7 +52,8 @@ def test_raw_config4_full_and_variants():
                   oracle_run(c, msplit=24 << 20, gc=0.5))
 
 
-def test_raw_edge_cases():
+@pytest.mark.parametrize("pinned", [False, True])
+def test_raw_edge_cases(pinned):
     tb = TraceBuilder()
     tb.end_trace()                                    # empty
     tb.alloc(7, 1).end_trace()                        # open trace
@@ -66,7 +67,7 @@ def test_raw_edge_cases():
         tb.free(s, stream=(s + 1) % 16)
     tb.end_trace()
     b = tb.build()
-    assert_parity(b, _raw(b), oracle_run(b))
+    assert_parity(b, _raw(b, pinned=pinned), oracle_run(b))
 
 
 def _bad(kind):
@@ -83,12 +84,30 @@ def _bad(kind):
     return Batch(by, tg, off, np.full(len(traces), xm.UNLIMITED, np.uint64))
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("kind", ["dup", "nonlive", "size", "zero"])
-def test_raw_rejects_what_the_loader_rejects(kind):
+def test_raw_rejects_what_the_loader_rejects(kind, pinned):
+    """Also with page-locked input (the chunked DMA + per-trace wait path)."""
     b = _bad(kind)
     with pytest.raises(xm.XMemError) as e1:
         xm.load_traces(b.bytes, b.tag, b.off)
+    by, tg = b.bytes, b.tag
+    if pinned:
+        by = torch.from_numpy(np.ascontiguousarray(by)).pin_memory().numpy()
+        tg = torch.from_numpy(np.ascontiguousarray(tg).view(np.int32)).pin_memory().numpy().view(np.uint32)
     with pytest.raises(xm.XMemError) as e2:
-        xm.simulate_raw(b.bytes, b.tag, b.off)
+        xm.simulate_raw(by, tg, b.off)
     assert e2.value.bad_trace == 3
     assert "trace 3" in str(e1.value) and "trace 3" in str(e2.value)
+
+
+def test_raw_streamed_equals_in_place(monkeypatch):
+    """Page-locked input: the chunked DMA copies (default) and the loader
+    reading host memory in place (XM_RAW_INPUT=direct) give the same results,
+    on a batch of many short traces (chunks of many traces) and long ones."""
+    b = concat([fuzz.spec1_corpus(400, 900, salt=51), suites.config2(), fuzz.capacity_corpus(50, 400, salt=52)])
+    h1 = _raw(b, pinned=True)
+    monkeypatch.setenv("XM_RAW_INPUT", "direct")
+    h2 = _raw(b, pinned=True)
+    assert (h1 == h2).all()
+    assert_parity(b, h1, oracle_run(b))
