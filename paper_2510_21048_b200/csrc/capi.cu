@@ -544,8 +544,9 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, pp->start, 0);
     const WriteValue32Fn wv = write_value32();
     static thread_local std::vector<uint32_t> chunk_end;   // outlives the async copies
-    chunk_end.clear();
     const int kChunks = 24;
+    chunk_end.clear();
+    chunk_end.reserve(kChunks);          // no reallocation under pending copies
     int64_t t = 0, ev0 = 0;
     for (int c = 0; c < kChunks && t < R.T && e == cudaSuccess; ++c) {
       // whole traces up to about (c+1)/kChunks of the events; the copied range
