@@ -53,6 +53,12 @@
 #ifndef XM_ARENA_BUDGET
 #define XM_ARENA_BUDGET (4ull << 30)   // bytes of global arena slots (overflow path), see plan_replay
 #endif
+#ifndef XM_F_GROW_NUM
+#define XM_F_GROW_NUM 2         // free-list growth factor NUM/DEN (plus one scan block)
+#endif
+#ifndef XM_F_GROW_DEN
+#define XM_F_GROW_DEN 1
+#endif
 #ifndef XM_HEAP_RESERVE_DIV
 #define XM_HEAP_RESERVE_DIV 24  // admission keeps 1/24 of the heap for free-list growth (tuned)
 #endif
@@ -456,7 +462,12 @@ __device__ void ticket_release(HeapHdr* h) {
 // Wait (holding the ticket) until np pages can be claimed. Admission keeps a
 // reserve of free pages for the free-list growth of the traces already running
 // (unless the heap would otherwise sit idle).
-__device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats) {
+__device__ void heap_free(HeapHdr* h, uint32_t start, uint32_t np);
+
+// The A and F regions are claimed separately (each fits any hole of its own
+// size); the admission test counts both: np = A pages, np2 = F pages.
+__device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t* stats,
+                               uint32_t np2, uint32_t* start2) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t reserve = total / XM_HEAP_RESERVE_DIV;
   uint32_t start, hw = 0, nap = 256;
@@ -464,9 +475,13 @@ __device__ uint32_t heap_admit(HeapHdr* h, uint32_t total, uint32_t np, uint32_t
     uint32_t used = 0;
     for (uint32_t w = lane; w < kBitmapWords; w += 32) used += __popc(bitmap_word(h, w));
     used = __reduce_add_sync(kFull, used);
-    const bool admit = used == 0 || used + np + reserve <= total;
+    const bool admit = used == 0 || used + np + np2 + reserve <= total;
     start = admit ? first_fit(h, total, np) : kNone32;
-    if (start != kNone32 && try_claim(h, start, np)) break;
+    if (start != kNone32 && try_claim(h, start, np)) {
+      const uint32_t s2 = first_fit(h, total, np2);
+      if (s2 != kNone32 && try_claim(h, s2, np2)) { *start2 = s2; break; }
+      heap_free(h, start, np);                 // no hole for F: give A back, retry
+    }
     __nanosleep(nap);
     nap = min(nap * 2, uint32_t(XM_MAX_NAP));
     ++hw;
@@ -526,7 +541,7 @@ template <class L>
 __device__ __forceinline__ bool grow_f(State<L>& S, Grow& G, uint32_t nf) {
   if (G.fstart == kNone32 || S.cap_f >= L::kCapMax) return false;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t ncap = min(S.cap_f * 2 + kScanBlock, L::kCapMax);
+  const uint32_t ncap = min(round_scan(S.cap_f * XM_F_GROW_NUM / XM_F_GROW_DEN + kScanBlock), L::kCapMax);
   const bool age = S.F_age != nullptr;
   const uint32_t np = uint32_t((f_bytes<L>(ncap, age) + kPage - 1) / kPage);
   if (np > G.total) return false;
@@ -1404,14 +1419,15 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     const uint64_t gc_bar = gc_on ? uint64_t(P.u.gc_threshold * double(cap)) : 0ull;
     const uint32_t npf = uint32_t((f_bytes<Narrow>(nfc, ages) + kPage - 1) / kPage);
     if (na <= Narrow::kMaxIdx && npa + npf <= P.heap_pages) {
-      const uint32_t start = heap_admit(hdr, P.heap_pages, npa + npf, stats);
+      uint32_t fstart = 0;
+      const uint32_t start = heap_admit(hdr, P.heap_pages, npa, stats, npf, &fstart);
       ticket_release(hdr);
       State<Narrow> S;
       carve_a(S, pages + size_t(start) * kPage, na);
-      carve_f(S, pages + size_t(start + npa) * kPage, nfc, ages);
+      carve_f(S, pages + size_t(fstart) * kPage, nfc, ages);
       fill_sentinels(S, 0, nfc);
       __syncwarp();
-      Grow G{hdr, pages, P.heap_pages, start + npa, npf, stats};
+      Grow G{hdr, pages, P.heap_pages, fstart, npf, stats};
       constexpr int kO = kKnobs ? kOptKnobs : 0;
       st = P.curve ? replay_trace<Narrow, kO | kOptCurve>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar)
                    : replay_trace<Narrow, kO>(P, S, G, e0, n, cap_u, R, gc_on, gc_bar);
