@@ -127,3 +127,23 @@ def test_k1c_config4():
     b = type(b)(b.bytes, b.tag, b.off, np.full(b.n_traces, np.iinfo(np.uint64).max, np.uint64), b.names)
     h = _run(b, "c", True)
     assert_parity(b, h, oracle_run(b, parallel=True), fields=FIELDS)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("path", ["c", "t", "f"])
+def test_k1_paths_roundup_divisions(path, packed):
+    """The NEXT-4 rounding variant (torch roundup_power2_divisions:4, reading
+    Q20) through each K1 kernel's division path (kDiv), vs the oracle."""
+    b = concat([_seams_batch(long_len=150_000), fuzz.small_size_corpus(200, 600, salt=43)])
+    old = os.environ.get("XM_K1")
+    os.environ["XM_K1"] = path
+    try:
+        tr = xm.load_traces(b.bytes, b.tag, b.off)
+        dev = tr.to_device(packed=packed)
+        h, _ = xm.peaks(xm.simulate_batch(dev, xm.Config(mode=1, roundup_power2_divisions=4)))
+    finally:
+        if old is None:
+            del os.environ["XM_K1"]
+        else:
+            os.environ["XM_K1"] = old
+    assert_parity(b, h, oracle_run(b, div=4), fields=FIELDS)
