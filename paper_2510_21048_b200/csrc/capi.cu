@@ -421,6 +421,8 @@ struct RawLayout {
   size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, scratch, total;
 };
 
+constexpr int kRawChunks = 24;          // upload chunks of xm_simulate_raw
+
 struct RawShape {
   int64_t T, E;
   uint32_t max_events, max_ids;
@@ -442,7 +444,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.woff = p; p += al(8 * (T + 1));
   L.wnids = p; p += al(4 * T);
   L.out = p; p += al(sizeof(xm_result) * T);
-  L.ready = p; p += al(sizeof(uint32_t));
+  L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 1));   // chunk firsts + flags
   L.scratch = p;
   xm_batch b{};
   b.n_traces = R.T;
@@ -513,67 +515,80 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   auto cp = [&](size_t o, const void* src, size_t n) {
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, st);
   };
-  // processing order: longest first, ties in caller order (as xm_load_traces)
-  std::vector<uint32_t> order(size_t(R.T));
-  for (int64_t i = 0; i < R.T; ++i) order[size_t(i)] = uint32_t(i);
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
-  });
-  // events. Page-locked (the usual case): copied by the DMA engine in chunks
-  // of whole traces in caller order on the library's copy stream, each chunk
-  // followed by a stream-ordered write of "traces resident so far" that the
-  // loader's warps wait on (trace k's warp starts once k is resident), so the
-  // transfer overlaps the loader (the copy engine moves ~55 GB/s where the
-  // warps reading host memory in place managed ~36). XM_RAW_INPUT=direct
-  // reads in place instead (tooling). Pageable: copied first.
+  // events. Page-locked (the usual case): copied by the DMA engine in up to
+  // kRawChunks chunks of whole traces (contiguous in caller order) on the
+  // library's copy stream, the chunks holding the longest traces first (a
+  // trace's loader time grows with its length, so the last chunk to land
+  // should hold short ones); each chunk is followed by a stream-ordered write
+  // of its flag, which the loader's warps wait on (trace k's warp starts once
+  // its chunk has landed). The transfer thus overlaps the loader (the copy
+  // engine moves ~55 GB/s where warps reading host memory in place managed
+  // ~36). XM_RAW_INPUT=direct reads in place instead (tooling). Pageable:
+  // copied first.
   const int64_t* d_bytes = static_cast<const int64_t*>(mapped(h_bytes));
   const uint32_t* d_tag = static_cast<const uint32_t*>(mapped(h_tag));
   const char* rin = std::getenv("XM_RAW_INPUT");
   const bool direct = rin && !std::strcmp(rin, "direct");
   const bool streamed = d_bytes && d_tag && !direct && R.E > 0;
   cp(L.off, h_off, 8 * size_t(R.T + 1));
-  cp(L.order, order.data(), 4 * size_t(R.T));
-  if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
-  uint32_t* ready = reinterpret_cast<uint32_t*>(w + L.ready);
+  uint32_t* chunk_first = reinterpret_cast<uint32_t*>(w + L.ready);
+  uint32_t* chunk_flag = chunk_first + (kRawChunks + 1);
+  int n_chunks = 0;
   Pipe* pp = nullptr;
   if (streamed) {
-    if (e == cudaSuccess) e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
+    // chunks: whole traces up to about (c+1)/kRawChunks of the events
+    static thread_local std::vector<uint32_t> firsts;    // outlive the async copies
+    firsts.clear();
+    firsts.reserve(kRawChunks + 1);
+    std::vector<int64_t> maxlen;
+    int64_t t = 0;
+    for (int c = 0; c < kRawChunks && t < R.T; ++c) {
+      const int64_t goal = (R.E * (c + 1)) / kRawChunks;
+      const int64_t t0 = t;
+      int64_t ml = 0;
+      while (t < R.T && (h_off[t + 1] <= goal || c == kRawChunks - 1)) {
+        ml = std::max<int64_t>(ml, h_off[t + 1] - h_off[t]);
+        ++t;
+      }
+      if (t == t0) continue;
+      firsts.push_back(uint32_t(t0));
+      maxlen.push_back(ml);
+    }
+    n_chunks = int(firsts.size());
+    firsts.push_back(uint32_t(R.T));
+    cp(L.ready, firsts.data(), sizeof(uint32_t) * firsts.size());
+    if (e == cudaSuccess) e = cudaMemsetAsync(chunk_flag, 0, sizeof(uint32_t) * kRawChunks, st);
     if (e == cudaSuccess) e = get_pipe(&pp);
     // the copy stream starts after everything already queued on `stream`
     if (e == cudaSuccess) e = cudaEventRecord(pp->start, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, pp->start, 0);
     const WriteValue32Fn wv = write_value32();
-    static thread_local std::vector<uint32_t> chunk_end;   // outlives the async copies
-    const int kChunks = 24;
-    chunk_end.clear();
-    chunk_end.reserve(kChunks);          // no reallocation under pending copies
-    int64_t t = 0, ev0 = 0;
-    for (int c = 0; c < kChunks && t < R.T && e == cudaSuccess; ++c) {
-      // whole traces up to about (c+1)/kChunks of the events; the copied range
-      // ends on a 32-event boundary (no cache line holds events of two chunks)
-      const int64_t goal = (R.E * (c + 1)) / kChunks;
-      while (t < R.T && (h_off[t + 1] <= goal || c == kChunks - 1)) ++t;
-      if (t == 0) continue;
-      int64_t ev1 = h_off[t];
-      if (t < R.T) ev1 = std::min<int64_t>(R.E, (ev1 + 31) & ~int64_t(31));
-      else ev1 = R.E;
+    static thread_local std::vector<uint32_t> ones;
+    ones.assign(kRawChunks, 1u);
+    std::vector<int> corder(n_chunks);
+    for (int c = 0; c < n_chunks; ++c) corder[c] = c;
+    std::stable_sort(corder.begin(), corder.end(), [&](int a, int b) { return maxlen[a] > maxlen[b]; });
+    for (int c : corder) {
+      if (e != cudaSuccess) break;
+      // the copied range is widened to 32-event boundaries (whole cache lines:
+      // a boundary line is written by both neighbours, with the same bytes)
+      const int64_t ev0 = h_off[firsts[c]] & ~int64_t(31);
+      const int64_t ev1 = std::min<int64_t>(R.E, (h_off[firsts[c + 1]] + 31) & ~int64_t(31));
       if (ev1 > ev0) {
-        if (e == cudaSuccess) e = cudaMemcpyAsync(w + L.bytes + 8 * size_t(ev0), h_bytes + ev0,
-                                                  8 * size_t(ev1 - ev0), cudaMemcpyHostToDevice, pp->cs);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(w + L.tag + 4 * size_t(ev0), h_tag + ev0,
-                                                  4 * size_t(ev1 - ev0), cudaMemcpyHostToDevice, pp->cs);
-        ev0 = ev1;
+        e = cudaMemcpyAsync(w + L.bytes + 8 * size_t(ev0), h_bytes + ev0, 8 * size_t(ev1 - ev0),
+                            cudaMemcpyHostToDevice, pp->cs);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(w + L.tag + 4 * size_t(ev0), h_tag + ev0, 4 * size_t(ev1 - ev0),
+                              cudaMemcpyHostToDevice, pp->cs);
       }
-      chunk_end.push_back(uint32_t(t));
       if (e != cudaSuccess) break;
       if (wv) {
-        if (wv(pp->cs, reinterpret_cast<unsigned long long>(ready), uint32_t(t), 0) != 0) e = cudaErrorUnknown;
+        if (wv(pp->cs, reinterpret_cast<unsigned long long>(chunk_flag + c), 1u, 0) != 0) e = cudaErrorUnknown;
       } else {
-        e = cudaMemcpyAsync(ready, &chunk_end.back(), sizeof(uint32_t), cudaMemcpyHostToDevice, pp->cs);
+        e = cudaMemcpyAsync(chunk_flag + c, &ones[size_t(c)], sizeof(uint32_t), cudaMemcpyHostToDevice, pp->cs);
       }
     }
-    if (e == cudaSuccess && t < R.T) e = cudaErrorUnknown;      // (never: the last chunk takes all)
-    // every copy and counter write is queued before the kernel that waits on them
+    // every copy and flag write is queued before the kernel that waits on them
     if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
     d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
     d_tag = reinterpret_cast<const uint32_t*>(w + L.tag);
@@ -581,6 +596,15 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
     if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
   }
+  // processing order of the replay: longest first, ties in caller order (as
+  // xm_load_traces); computed while the first chunks are in flight
+  std::vector<uint32_t> order(size_t(R.T));
+  for (int64_t i = 0; i < R.T; ++i) order[size_t(i)] = uint32_t(i);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
+  });
+  cp(L.order, order.data(), 4 * size_t(R.T));
+  if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
   int launches = 0;
   xm_lifecycle* d_rec = reinterpret_cast<xm_lifecycle*>(w + L.rec);
@@ -588,7 +612,8 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
                          R.max_events, w + L.k5, d_rec, reinterpret_cast<const uint32_t*>(w + L.order),
                          reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
                          reinterpret_cast<int64_t*>(w + L.woff), reinterpret_cast<uint32_t*>(w + L.wnids),
-                         stream, &launches, streamed ? ready : nullptr);
+                         stream, &launches, streamed ? chunk_first : nullptr,
+                         streamed ? chunk_flag : nullptr, n_chunks);
   // `stream` resumes (the replay, result download, later users of the
   // workspace) only after the copies too, also when the launch failed
   if (streamed) {

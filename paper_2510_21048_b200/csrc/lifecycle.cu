@@ -78,8 +78,9 @@ struct LParams {
   uint8_t* mismatch;
   xm_lifecycle* rec;
   unsigned int* work;
-  const uint32_t* ready;                  // loader mode, streamed input: traces (caller
-                                          // order) whose events are resident, or null
+  const uint32_t* chunk_first;            // loader mode, streamed input: [n_chunks + 1]
+  const uint32_t* chunk_flag;             // first trace of each upload chunk, and its
+  int n_chunks;                           // "landed" flag (0 until copied); or null
 };
 
 __device__ __forceinline__ uint32_t hash_addr(uint64_t a, uint32_t bits) {
@@ -97,13 +98,18 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     if (lane == 0) k = atomicAdd(P.work, 1u);
     k = __shfl_sync(kFull, k, 0);
     if (int64_t(k) >= P.n_traces) break;
-    if (P.ready) {                          // wait until trace k's events have landed
+    if (P.chunk_flag) {                     // wait until trace k's chunk has landed
+      int lo = 0, hi = P.n_chunks - 1;      // the chunk c with first[c] <= k < first[c+1]
+      while (lo < hi) {
+        const int m = (lo + hi + 1) >> 1;
+        if (P.chunk_first[m] <= k) lo = m; else hi = m - 1;
+      }
       uint32_t nap = 256;
       for (;;) {
         uint32_t r = 0;
         if (lane == 0)
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.ready) : "memory");
-        if (__shfl_sync(kFull, r, 0) > k) break;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.chunk_flag + lo) : "memory");
+        if (__shfl_sync(kFull, r, 0) != 0) break;
         __nanosleep(nap);
         nap = min(nap * 2, 4096u);
       }
@@ -535,7 +541,8 @@ size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events) {
 int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* d_off, int64_t T,
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
-                  uint32_t* w_nids, void* stream, int* n_launches, const uint32_t* ready) {
+                  uint32_t* w_nids, void* stream, int* n_launches, const uint32_t* chunk_first,
+                  const uint32_t* chunk_flag, int n_chunks) {
   xm_instants in{};
   in.n_traces = T;
   in.n_events = E;
@@ -561,7 +568,9 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
   P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
-  P.ready = ready;
+  P.chunk_first = chunk_first;
+  P.chunk_flag = chunk_flag;
+  P.n_chunks = n_chunks;
   k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
   k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, d_order, T, w_off);
   const int64_t want = (T + 7) / 8;

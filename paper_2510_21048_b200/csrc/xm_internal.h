@@ -74,6 +74,7 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
                   uint32_t* w_nids, void* stream, int* n_launches,
-                  const uint32_t* ready = nullptr);
+                  const uint32_t* chunk_first = nullptr, const uint32_t* chunk_flag = nullptr,
+                  int n_chunks = 0);
 
 }  // namespace xm_internal
