@@ -54,6 +54,10 @@ extern "C" {
                          /* a result, not an error (SPEC.md:284 D4)            */
 #define XM_T_OVERFLOW 2  /* state exceeded its arena (defensive; never occurs  */
                          /* when scratch is sized by xm_scratch_bytes)          */
+#define XM_T_INVALID 3   /* not replayed: n_ids = 0 for a trace with events    */
+                         /* (a batch contract violation; xm_simulate_raw marks  */
+                         /* a trace its loader rejected this way and returns    */
+                         /* XM_EINVAL naming it)                                */
 
 /* -------------------------------------------------------------- modes */
 #define XM_FULL 0            /* full allocator replay (K2)                     */

@@ -418,7 +418,7 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
 // ---- raw host traces -> device loader -> replay (xm_simulate_raw) -----------------
 namespace {
 struct RawLayout {
-  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, scratch, total;
+  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, pos, scratch, total;
 };
 
 constexpr int kRawChunks = 24;          // upload chunks of xm_simulate_raw
@@ -445,6 +445,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.wnids = p; p += al(4 * T);
   L.out = p; p += al(sizeof(xm_result) * T);
   L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 1));   // chunk firsts + flags
+  L.pos = p; p += al(4 * T);                                        // caller -> stored index
   L.scratch = p;
   xm_batch b{};
   b.n_traces = R.T;
@@ -605,6 +606,20 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   });
   cp(L.order, order.data(), 4 * size_t(R.T));
   if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
+  // the wire arrays' offsets (stored order: a valid trace keeps all its
+  // events) and each caller trace's stored index, so the loader writes the
+  // wire in place (no staging / compaction pass)
+  static thread_local std::vector<int64_t> woff;      // outlive the async copies
+  static thread_local std::vector<uint32_t> pos;
+  woff.assign(size_t(R.T) + 1, 0);
+  pos.assign(size_t(R.T), 0);
+  for (int64_t k = 0; k < R.T; ++k) {
+    const uint32_t t = order[size_t(k)];
+    pos[t] = uint32_t(k);
+    woff[size_t(k) + 1] = woff[size_t(k)] + (h_off[t + 1] - h_off[t]);
+  }
+  cp(L.woff, woff.data(), 8 * size_t(R.T + 1));
+  cp(L.pos, pos.data(), 4 * size_t(R.T));
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
   int launches = 0;
   xm_lifecycle* d_rec = reinterpret_cast<xm_lifecycle*>(w + L.rec);
@@ -613,7 +628,8 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
                          reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
                          reinterpret_cast<int64_t*>(w + L.woff), reinterpret_cast<uint32_t*>(w + L.wnids),
                          stream, &launches, streamed ? chunk_first : nullptr,
-                         streamed ? chunk_flag : nullptr, n_chunks);
+                         streamed ? chunk_flag : nullptr, n_chunks,
+                         reinterpret_cast<const uint32_t*>(w + L.pos));
   // `stream` resumes (the replay, result download, later users of the
   // workspace) only after the copies too, also when the launch failed
   if (streamed) {

@@ -78,6 +78,9 @@ struct LParams {
   uint8_t* mismatch;
   xm_lifecycle* rec;
   unsigned int* work;
+  const int64_t* wire_off;                // loader mode, direct wire output: the wire
+  const uint32_t* pos;                    // offsets (stored order), caller -> stored
+  uint32_t* w_nids;                       // index, n_ids out (0 = invalid); or null
   const uint32_t* chunk_first;            // loader mode, streamed input: [n_chunks + 1]
   const uint32_t* chunk_flag;             // first trace of each upload chunk, and its
   int n_chunks;                           // "landed" flag (0 until copied); or null
@@ -117,6 +120,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     }
     const unsigned gen = k + 1;
     const int64_t e0 = P.off[k];
+    const uint32_t sk = P.wire_off ? P.pos[k] : 0u;
+    const int64_t wire0 = P.wire_off ? P.wire_off[sk] : 0;
     const int n = int(P.off[k + 1] - e0);
     // this trace's table: the first 2^hb slots of the warp's region, 2^hb > n
     // (at most n distinct addresses, so a free slot always exists; with about
@@ -249,7 +254,9 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       const bool kept = is_alloc || matched;
       const unsigned km = __ballot_sync(kFull, kept);
       if (kept) {
-        const int64_t dst = e0 + int64_t(n_kept) + __popc(km & lt);
+        // staging at the trace's input offset, or (direct wire output) at
+        // its final place in the stored-order wire arrays
+        const int64_t dst = (P.wire_off ? wire0 : e0) + int64_t(n_kept) + __popc(km & lt);
         if (is_alloc) {
           P.st_bytes[dst] = b;
           P.st_tag[dst] = my_tag;
@@ -289,6 +296,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       r.n_ids = fresh;
       r.n_reopened = n_reopen;
       P.rec[k] = r;
+      // direct wire output: a trace with any verdict (its wire events are not
+      // the trace) gets n_ids 0, which the replay refuses (XM_T_INVALID)
+      if (P.w_nids)
+        P.w_nids[sk] = (n_orphan | n_mism | n_inv | n_reopen) || fresh > (1u << 27) ? 0u : fresh;
     }
     __syncwarp();
   }
@@ -542,7 +553,7 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
                   uint32_t* w_nids, void* stream, int* n_launches, const uint32_t* chunk_first,
-                  const uint32_t* chunk_flag, int n_chunks) {
+                  const uint32_t* chunk_flag, int n_chunks, const uint32_t* d_pos) {
   xm_instants in{};
   in.n_traces = T;
   in.n_events = E;
@@ -568,10 +579,21 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
   P.st_tag = reinterpret_cast<uint32_t*>(base + L.st_tag);
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
+  if (d_pos) {                                      // direct wire output (w_off given)
+    P.wire_off = w_off;
+    P.pos = d_pos;
+    P.w_nids = w_nids;
+    P.st_bytes = w_bytes;
+    P.st_tag = w_tag;
+  }
   P.chunk_first = chunk_first;
   P.chunk_flag = chunk_flag;
   P.n_chunks = n_chunks;
   k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
+  if (d_pos) {                                      // written in place: no compaction
+    *n_launches += 1;
+    return int(cudaGetLastError());
+  }
   k_wire_offsets<<<1, 1024, 0, st>>>(d_rec, d_order, T, w_off);
   const int64_t want = (T + 7) / 8;
   const int g = int(want < int64_t(L.ctas) * 8 ? want : int64_t(L.ctas) * 8);

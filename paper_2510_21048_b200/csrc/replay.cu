@@ -1405,6 +1405,16 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
     if (P.ready) wait_ready(P.ready, k);
     const uint64_t cap_u = cap >> P.u.unit_shift;
     xm_result R;
+    if (na == 0 && n > 0) {                       // no ids for its events: refused
+      ticket_release(hdr);                        // (held since the pull)
+      if (lane == 0) {
+        R = xm_result{};
+        R.status = XM_T_INVALID;
+        P.out[t] = R;
+      }
+      __syncwarp();
+      continue;
+    }
 #ifdef XM_TIMING
     if (lane == 0) P.timing[2 * size_t(t)] = global_ns();
 #endif

@@ -75,6 +75,6 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
                   uint32_t* w_nids, void* stream, int* n_launches,
                   const uint32_t* chunk_first = nullptr, const uint32_t* chunk_flag = nullptr,
-                  int n_chunks = 0);
+                  int n_chunks = 0, const uint32_t* d_pos = nullptr);
 
 }  // namespace xm_internal
