@@ -888,63 +888,99 @@ __global__ void __launch_bounds__(kCThreads, XM_K1C_CTAS_PER_SM) k_scan_chunks(c
     if constexpr (!kDiv) {
       if (full && nb == 0) {
         // ===== the common tile: no trace starts, no ragged end =====
-        // a2 in 32 bits: |request| < 2^40 (XM_MAX_REQUEST) makes |delta| =
-        // ceil(|b| / 2^sh) < 2^31, and while every |delta| of the tile is below
-        // 2^26 a lane's sums of up to 16 stay within int32; the warp scan is
-        // 64-bit. Otherwise (never on paper-shaped traces) the 64-bit path.
+        // a2 in 32 bits (sh = log2 min_block < 32): |request| < 2^40
+        // (XM_MAX_REQUEST); the low word of b >> sh is one funnel shift of
+        // (hi, lo), plus one for an allocation with a remainder (ceil).
+        // Tier 32 (8 events per lane): every |b| < 2^31, so |delta| <= 2^22
+        // and the warp's 256 sums stay within int32, warp scan included.
+        // Tier 35: every |b| < 2^35 (|delta| <= 2^26): lane sums in int32,
+        // the warp scan in 64 bits. Else the 64-bit path.
         load_stage(d);
-        const int64_t msk = (1ll << P.unit_shift) - 1;
+        const uint32_t sh = P.unit_shift;
+        const uint32_t msk = (1u << sh) - 1u;
         int32_t v[kCPer];
-        uint32_t orr = 0;
+        uint32_t g32 = 0, g35 = 0;           // tier 32 iff g32 == 0, tier 35 iff g35 < 16
 #pragma unroll
         for (int q = 0; q < kCPer; ++q) {
-          if constexpr (kPacked) {
-            const uint64_t m = uint64_t(d[q]) & ((1ull << 41) - 1);
-            const int32_t u = int32_t((m + uint64_t(msk)) >> P.unit_shift);
-            v[q] = (uint64_t(d[q]) >> 41) & 1 ? u : -u;
+          const uint32_t lo = uint32_t(uint64_t(d[q]));
+          int32_t hi = int32_t(uint64_t(d[q]) >> 32);
+          bool pos;
+          if constexpr (kPacked) {           // |b| in bits 0-40, allocation bit 41
+            pos = (hi >> 9) & 1;
+            hi &= 0x1FF;
           } else {
-            const int64_t b = d[q];
-            v[q] = int32_t((b + (b > 0 ? msk : 0)) >> P.unit_shift);   // floor for frees
-            if (uint32_t(int32_t(b >> 32) + 256) >= 512u) v[q] = INT32_MIN;
+            pos = hi >= 0;
           }
-          orr |= uint32_t(abs(v[q]));
+          const uint32_t qv = __funnelshift_r(lo, uint32_t(hi), sh);
+          if constexpr (kPacked) {           // ceil of the magnitude, then the sign
+            const int32_t u = int32_t(qv) + ((lo & msk) ? 1 : 0);
+            v[q] = pos ? u : -u;
+            g32 |= uint32_t(hi) | (lo >> 31);                           // m < 2^31
+          } else {                           // ceil for allocations, floor for frees
+            v[q] = int32_t(qv) + ((pos && (lo & msk)) ? 1 : 0);
+            g32 |= uint32_t(hi ^ (int32_t(lo) >> 31));                 // b fits int32
+          }
+          g35 |= uint32_t(hi + 8);
         }
-        int64_t sum, mx;
         int ai = 0;
-        if (!__any_sync(kFull, orr >= (1u << 26))) {
+        if (kCPer == 8 && sh < 32 && !__any_sync(kFull, g32 != 0u)) {
+          // ---- tier 32 ----
           int32_t s32 = v[0], m32 = v[0];
 #pragma unroll
           for (int q = 1; q < kCPer; ++q) {
             s32 += v[q];
             if (s32 > m32) { m32 = s32; ai = q; }
           }
-          sum = s32;
-          mx = m32;
-        } else {
-          sum = c_delta<kPacked, kDiv>(d[0], P);
-          mx = sum;
+          int32_t incl = s32;
 #pragma unroll
-          for (int q = 1; q < kCPer; ++q) {
-            sum += c_delta<kPacked, kDiv>(d[q], P);
-            if (sum > mx) { mx = sum; ai = q; }
+          for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
           }
-        }
-        int64_t incl = sum;
+          const int32_t key = incl - s32 + m32;
+          const int32_t wm = __reduce_max_sync(kFull, key);
+          const int src = __ffs(__ballot_sync(kFull, key == wm)) - 1;
+          const int64_t warg = ts + int64_t(src) * kCPer + __shfl_sync(kFull, ai, src);
+          const int32_t wsum = __shfl_sync(kFull, incl, 31);
+          run = seg_op(run, SegE{int64_t(wsum), int64_t(wm), warg, -1, false});
+        } else {
+          int64_t sum, mx;
+          if (sh < 32 && !__any_sync(kFull, g35 >= 16u)) {
+            // ---- tier 35 ----
+            int32_t s32 = v[0], m32 = v[0];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int64_t y = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += y;
+            for (int q = 1; q < kCPer; ++q) {
+              s32 += v[q];
+              if (s32 > m32) { m32 = s32; ai = q; }
+            }
+            sum = s32;
+            mx = m32;
+          } else {
+            sum = c_delta<kPacked, kDiv>(d[0], P);
+            mx = sum;
+#pragma unroll
+            for (int q = 1; q < kCPer; ++q) {
+              sum += c_delta<kPacked, kDiv>(d[q], P);
+              if (sum > mx) { mx = sum; ai = q; }
+            }
+          }
+          int64_t incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const unsigned long long uk = static_cast<unsigned long long>(incl - sum + mx) ^ 0x8000000000000000ull;
+          const unsigned khi = unsigned(uk >> 32), klo = unsigned(uk);
+          const unsigned mh = __reduce_max_sync(kFull, khi);
+          const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
+          const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
+          const int64_t wmx = static_cast<int64_t>((static_cast<unsigned long long>(mh) << 32 | ml) ^
+                                                   0x8000000000000000ull);
+          const int64_t warg = ts + int64_t(src) * kCPer + __shfl_sync(kFull, ai, src);
+          const int64_t wsum = __shfl_sync(kFull, incl, 31);
+          run = seg_op(run, SegE{wsum, wmx, warg, -1, false});
         }
-        const unsigned long long uk = static_cast<unsigned long long>(incl - sum + mx) ^ 0x8000000000000000ull;
-        const unsigned khi = unsigned(uk >> 32), klo = unsigned(uk);
-        const unsigned mh = __reduce_max_sync(kFull, khi);
-        const unsigned ml = __reduce_max_sync(kFull, khi == mh ? klo : 0u);
-        const int src = __ffs(__ballot_sync(kFull, khi == mh && klo == ml)) - 1;
-        const int64_t wmx = static_cast<int64_t>((static_cast<unsigned long long>(mh) << 32 | ml) ^
-                                                 0x8000000000000000ull);
-        const int64_t warg = ts + int64_t(src) * kCPer + __shfl_sync(kFull, ai, src);
-        const int64_t wsum = __shfl_sync(kFull, incl, 31);
-        run = seg_op(run, SegE{wsum, wmx, warg, -1, false});
         done = true;
       }
     }

@@ -147,3 +147,21 @@ def test_k1_paths_roundup_divisions(path, packed):
         else:
             os.environ["XM_K1"] = old
     assert_parity(b, h, oracle_run(b, div=4), fields=FIELDS)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("path", ["c", "t"])
+def test_k1_paths_large_requests(path, packed):
+    """Requests around 2^31, 2^35 and up to 2^39 bytes, so K1c's common tiles
+    take each of its arithmetic tiers (32-bit warp scan, 32-bit lane sums with
+    a 64-bit warp scan, all 64-bit) and mix them across the warps of a chunk."""
+    rng = np.random.default_rng(91)
+    tb = TraceBuilder()
+    bid = 0
+    for top in [1 << 22, (1 << 31) + 5, 1 << 33, (1 << 35) + 7, 1 << 39]:
+        for _ in range(6):
+            bid = _random_trace(tb, rng, int(rng.integers(3000, 9000)), bid, max_bytes=top)
+            tb.end_trace()
+    b = concat([tb.build(), suites.config1()])
+    h = _run(b, path, packed)
+    assert_parity(b, h, oracle_run(b), fields=FIELDS)
