@@ -533,8 +533,11 @@ def main():
             "frac": achieved / peak, "traffic": traffic, "kernel": "k_replay",
             "alg_bytes_per_launch": alg, "kernel_ms": kern_ms, "peak_source": peak_src,
             "traffic_source": tsrc,
-            "issue": ncu_issue("k_replay", kern_ms,
-                               (clocks or {}).get("sm_mhz") or peaks_clock(), local_done),
+            # (the committed ncu capture is of the N=1 config-4 batch: the
+            # issue fraction is computed only for that launch)
+            "issue": (ncu_issue("k_replay", kern_ms,
+                                (clocks or {}).get("sm_mhz") or peaks_clock(), local_done)
+                      if world == 1 else ncu_issue()),
             "note": "K2 is a serial integer state machine per trace (issue/latency-bound); "
                     "HBM fraction reported as the north_star asks, warp-issue efficiency "
                     "from ncu in 'issue'"}
