@@ -37,6 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         path = os.path.join(CSRC, src)
         if src == "replay.cu" and os.environ.get("XM_REPLAY_SRC"):   # A/B tooling
             path = os.path.abspath(os.environ["XM_REPLAY_SRC"])
+        if src == "scan.cu" and os.environ.get("XM_SCAN_SRC"):       # A/B tooling
+            path = os.path.abspath(os.environ["XM_SCAN_SRC"])
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), *(["-DXM_TIMING"] if TIMING else []),
                *([f"-DXM_HEAP_RESERVE_DIV={os.environ['XM_HEAP_RESERVE_DIV']}"] if os.environ.get("XM_HEAP_RESERVE_DIV") else []),
                *([f"-DXM_F_INIT_DIV={os.environ['XM_F_INIT_DIV']}"] if os.environ.get("XM_F_INIT_DIV") else []),
@@ -46,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                *([f"-DXM_MAX_NAP={os.environ['XM_MAX_NAP']}"] if os.environ.get("XM_MAX_NAP") else []),
                *([f"-DXM_K1_PER_LANE={os.environ['XM_K1_PER_LANE']}"] if os.environ.get("XM_K1_PER_LANE") else []),
                *[f"-D{k}={os.environ[k]}" for k in ("XM_K1C_PER", "XM_K1C_STAGES", "XM_K1C_CTAS_PER_SM", "XM_K1C_THREADS",
-                           "XM_F_GROW_NUM", "XM_F_GROW_DEN")
+                           "XM_F_GROW_NUM", "XM_F_GROW_DEN", "XM_K1_MINB")
                  if os.environ.get(k)],
                "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", path,

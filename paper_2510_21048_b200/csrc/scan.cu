@@ -372,6 +372,9 @@ constexpr int kTraceMax = 1 << 16;
 #ifndef XM_K1_PER_LANE
 #define XM_K1_PER_LANE 8
 #endif
+#ifndef XM_K1_MINB
+#define XM_K1_MINB 8            // launch bound: 8 resident CTAs per SM (64 registers)
+#endif
 constexpr int kTWarps = XM_K1_WARPS;
 constexpr int kTThreads = 32 * kTWarps;
 constexpr int kPerLane = XM_K1_PER_LANE;
@@ -386,14 +389,17 @@ __device__ __forceinline__ int64_t k1_delta(int64_t b, const SParams& P) {
 }
 
 template <bool kPacked, bool kDiv>
-__global__ void __launch_bounds__(kTThreads) k_scan_trace(SParams P) {
+__global__ void __launch_bounds__(kTThreads, XM_K1_MINB) k_scan_trace(SParams P) {
   __shared__ long long s_sum[kTWarps], s_mx[kTWarps];
   __shared__ int s_arg[kTWarps];
   __shared__ unsigned int s_k;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const long long* by = reinterpret_cast<const long long*>(P.bytes);
-  for (;;) {
-    if (tid == 0) s_k = atomicAdd(P.work, 1u);
+  // the grid is exactly the resident CTAs: CTA i starts on stored trace i
+  // (the longest-first order's first wave) without touching the counter,
+  // then pulls gridDim.x + counter
+  for (bool first = true;; first = false) {
+    if (tid == 0) s_k = first ? blockIdx.x : gridDim.x + atomicAdd(P.work, 1u);
     __syncthreads();
     const unsigned k = s_k;
     __syncthreads();                        // s_k is rewritten by the next pull
@@ -1239,8 +1245,19 @@ int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * (64 / kTWarps));
+    // persistent grid = the CTAs resident at once (a CTA launched only when a
+    // first-wave one exits would find the work gone and only delay the end)
     const bool dv = u.div_shift != 0;
+    static int per_sm[4] = {0, 0, 0, 0};
+    const int vi = (P.packed ? 2 : 0) + (dv ? 1 : 0);
+    if (!per_sm[vi]) {
+      const void* fn = P.packed ? (dv ? (const void*)k_scan_trace<true, true> : (const void*)k_scan_trace<true, false>)
+                                : (dv ? (const void*)k_scan_trace<false, true> : (const void*)k_scan_trace<false, false>);
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kTThreads, 0) != cudaSuccess || nb < 1) nb = 1;
+      per_sm[vi] = nb;
+    }
+    const int64_t grid = std::min<int64_t>(std::max<int64_t>(b->n_traces, 1), int64_t(sms) * per_sm[vi]);
     if (P.packed) {
       if (dv) k_scan_trace<true, true><<<unsigned(grid), kTThreads, 0, st>>>(P);
       else k_scan_trace<true, false><<<unsigned(grid), kTThreads, 0, st>>>(P);
