@@ -244,8 +244,9 @@ HostLayout host_layout(const xm_traces_info& I, const xm_config* cfg, bool with_
 // on first use per device and kept for the thread's lifetime).
 struct Pipe {
   int dev = -1;
-  cudaStream_t cs = nullptr;
-  cudaEvent_t start = nullptr, copied = nullptr;
+  cudaStream_t cs = nullptr;        // copies
+  cudaStream_t ls = nullptr;        // xm_simulate_raw's loader (overlapped with the replay)
+  cudaEvent_t start = nullptr, copied = nullptr, meta = nullptr, ldone = nullptr;
 };
 thread_local Pipe g_pipe;
 
@@ -260,6 +261,9 @@ cudaError_t get_pipe(Pipe** out) {
     if ((e = cudaStreamCreateWithFlags(&q.cs, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&q.start, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&q.copied, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&q.ls, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&q.meta, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&q.ldone, cudaEventDisableTiming)) != cudaSuccess) return e;
     p = q;   // a previous device's objects are leaked, not destroyed under another context
   }
   *out = &p;
@@ -418,10 +422,13 @@ extern "C" int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity,
 // ---- raw host traces -> device loader -> replay (xm_simulate_raw) -----------------
 namespace {
 struct RawLayout {
-  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, pos, scratch, total;
+  size_t bytes, tag, off, order, cap, rec, k5, wbytes, wtag, woff, wnids, out, ready, pos, loaded, scratch,
+      total;
 };
 
-constexpr int kRawChunks = 24;          // upload chunks of xm_simulate_raw
+constexpr int kRawChunks = 256;         // most upload chunks of xm_simulate_raw (ready area)
+constexpr int kRawDefaultChunks = 24;   // upload chunks by default
+constexpr int kRawLoaderSms = 24;       // SMs of the overlapped loader by default
 
 struct RawShape {
   int64_t T, E;
@@ -446,6 +453,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.out = p; p += al(sizeof(xm_result) * T);
   L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 1));   // chunk firsts + flags
   L.pos = p; p += al(4 * T);                                        // caller -> stored index
+  L.loaded = p; p += al(4 * (T + 1));                               // completion queue + tail
   L.scratch = p;
   xm_batch b{};
   b.n_traces = R.T;
@@ -485,6 +493,25 @@ const void* mapped(const void* h) {
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) { cudaGetLastError(); return nullptr; }
   return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
+
+// the loader's verdicts: XM_EINVAL naming the first trace that breaks the
+// xm_load_traces contract, else XM_OK
+int raw_verdicts(const std::vector<xm_lifecycle>& rec, int64_t T, int64_t* bad_trace) {
+  for (int64_t t = 0; t < T; ++t) {
+    const xm_lifecycle& r = rec[size_t(t)];
+    const char* m = r.n_invalid ? "zero-byte or >= 2^40 request (SPEC.md:231)"
+                  : r.n_reopened ? "alloc of a live id (SPEC.md:249)"
+                  : r.n_orphan ? "free of a non-live id (SPEC.md:258)"
+                  : r.n_mismatch ? "free size differs from the alloc's request (SPEC.md:258)"
+                  : r.n_ids > (1u << 27) ? "more than 2^27 live blocks" : nullptr;
+    if (m) {
+      if (bad_trace) *bad_trace = t;
+      return set_error(XM_EINVAL, std::string("xm_simulate_raw: trace ") + std::to_string(t) + ": " + m);
+    }
+  }
+  clear_error();
+  return XM_OK;
+}
 }  // namespace
 
 extern "C" size_t xm_raw_ws_bytes(const int64_t* h_off, int64_t n_traces, const xm_config* cfg) {
@@ -516,16 +543,16 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   auto cp = [&](size_t o, const void* src, size_t n) {
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(w + o, src, n, cudaMemcpyHostToDevice, st);
   };
-  // events. Page-locked (the usual case): copied by the DMA engine in up to
-  // kRawChunks chunks of whole traces (contiguous in caller order) on the
-  // library's copy stream, the chunks holding the longest traces first (a
-  // trace's loader time grows with its length, so the last chunk to land
-  // should hold short ones); each chunk is followed by a stream-ordered write
-  // of its flag, which the loader's warps wait on (trace k's warp starts once
-  // its chunk has landed). The transfer thus overlaps the loader (the copy
-  // engine moves ~55 GB/s where warps reading host memory in place managed
-  // ~36). XM_RAW_INPUT=direct reads in place instead (tooling). Pageable:
-  // copied first.
+  // events. Page-locked (the usual case): copied by the DMA engine in chunks
+  // of whole traces (contiguous in caller order) on the library's copy
+  // stream, the chunks holding the longest traces first (a trace's loader and
+  // replay time grow with its length, so the last chunks to land should hold
+  // short ones); each chunk is followed by a stream-ordered write of its
+  // flag, which the loader's warps wait on (trace t's warp starts once its
+  // chunk has landed). The transfer thus overlaps the loader (the copy engine
+  // moves ~55 GB/s where warps reading host memory in place managed ~36).
+  // XM_RAW_INPUT=direct reads in place instead (tooling). Pageable: copied
+  // first.
   const int64_t* d_bytes = static_cast<const int64_t*>(mapped(h_bytes));
   const uint32_t* d_tag = static_cast<const uint32_t*>(mapped(h_tag));
   const char* rin = std::getenv("XM_RAW_INPUT");
@@ -536,18 +563,23 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   uint32_t* chunk_flag = chunk_first + (kRawChunks + 1);
   int n_chunks = 0;
   Pipe* pp = nullptr;
+  static thread_local std::vector<uint32_t> firsts;    // outlive the async copies
+  static thread_local std::vector<uint32_t> ones;
+  std::vector<int> corder;
   if (streamed) {
-    // chunks: whole traces up to about (c+1)/kRawChunks of the events
-    static thread_local std::vector<uint32_t> firsts;    // outlive the async copies
+    // chunks: whole traces up to about (c+1)/n of the events (n: XM_RAW_CHUNKS,
+    // tooling, at most kRawChunks)
+    const char* nc = std::getenv("XM_RAW_CHUNKS");
+    const int want = nc ? std::max(1, std::min(kRawChunks, std::atoi(nc))) : kRawDefaultChunks;
     firsts.clear();
-    firsts.reserve(kRawChunks + 1);
+    firsts.reserve(size_t(want) + 1);
     std::vector<int64_t> maxlen;
     int64_t t = 0;
-    for (int c = 0; c < kRawChunks && t < R.T; ++c) {
-      const int64_t goal = (R.E * (c + 1)) / kRawChunks;
+    for (int c = 0; c < want && t < R.T; ++c) {
+      const int64_t goal = (R.E * (c + 1)) / want;
       const int64_t t0 = t;
       int64_t ml = 0;
-      while (t < R.T && (h_off[t + 1] <= goal || c == kRawChunks - 1)) {
+      while (t < R.T && (h_off[t + 1] <= goal || c == want - 1)) {
         ml = std::max<int64_t>(ml, h_off[t + 1] - h_off[t]);
         ++t;
       }
@@ -560,21 +592,35 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     cp(L.ready, firsts.data(), sizeof(uint32_t) * firsts.size());
     if (e == cudaSuccess) e = cudaMemsetAsync(chunk_flag, 0, sizeof(uint32_t) * kRawChunks, st);
     if (e == cudaSuccess) e = get_pipe(&pp);
-    // the copy stream starts after everything already queued on `stream`
-    if (e == cudaSuccess) e = cudaEventRecord(pp->start, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, pp->start, 0);
-    const WriteValue32Fn wv = write_value32();
-    static thread_local std::vector<uint32_t> ones;
     ones.assign(kRawChunks, 1u);
-    std::vector<int> corder(n_chunks);
-    for (int c = 0; c < n_chunks; ++c) corder[c] = c;
-    std::stable_sort(corder.begin(), corder.end(), [&](int a, int b) { return maxlen[a] > maxlen[b]; });
+    corder.resize(size_t(n_chunks));
+    for (int c = 0; c < n_chunks; ++c) corder[size_t(c)] = c;
+    std::stable_sort(corder.begin(), corder.end(),
+                     [&](int x, int y) { return maxlen[size_t(x)] > maxlen[size_t(y)]; });
+    d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
+    d_tag = reinterpret_cast<const uint32_t*>(w + L.tag);
+  } else if (!direct || !d_bytes || !d_tag) {
+    if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
+    if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
+  }
+  // the chunk copies and their flags on the copy stream, which starts after
+  // everything queued on `stream` so far (earlier users of the workspace, the
+  // flag resets); `copied` is recorded after the last one
+  // after: an event already recorded on `stream` before any kernel that waits
+  // on the chunks (else one is recorded now)
+  auto enqueue_chunks = [&](cudaEvent_t after) {
+    if (!after) {
+      after = pp->start;
+      if (e == cudaSuccess) e = cudaEventRecord(after, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, after, 0);
+    const WriteValue32Fn wv = write_value32();
     for (int c : corder) {
       if (e != cudaSuccess) break;
       // the copied range is widened to 32-event boundaries (whole cache lines:
       // a boundary line is written by both neighbours, with the same bytes)
-      const int64_t ev0 = h_off[firsts[c]] & ~int64_t(31);
-      const int64_t ev1 = std::min<int64_t>(R.E, (h_off[firsts[c + 1]] + 31) & ~int64_t(31));
+      const int64_t ev0 = h_off[firsts[size_t(c)]] & ~int64_t(31);
+      const int64_t ev1 = std::min<int64_t>(R.E, (h_off[firsts[size_t(c) + 1]] + 31) & ~int64_t(31));
       if (ev1 > ev0) {
         e = cudaMemcpyAsync(w + L.bytes + 8 * size_t(ev0), h_bytes + ev0, 8 * size_t(ev1 - ev0),
                             cudaMemcpyHostToDevice, pp->cs);
@@ -589,20 +635,14 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
         e = cudaMemcpyAsync(chunk_flag + c, &ones[size_t(c)], sizeof(uint32_t), cudaMemcpyHostToDevice, pp->cs);
       }
     }
-    // every copy and flag write is queued before the kernel that waits on them
     if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
-    d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
-    d_tag = reinterpret_cast<const uint32_t*>(w + L.tag);
-  } else if (!direct || !d_bytes || !d_tag) {
-    if (!d_bytes) { cp(L.bytes, h_bytes, 8 * size_t(R.E)); d_bytes = reinterpret_cast<int64_t*>(w + L.bytes); }
-    if (!d_tag) { cp(L.tag, h_tag, 4 * size_t(R.E)); d_tag = reinterpret_cast<uint32_t*>(w + L.tag); }
-  }
+  };
   // processing order of the replay: longest first, ties in caller order (as
-  // xm_load_traces); computed while the first chunks are in flight
+  // xm_load_traces)
   std::vector<uint32_t> order(size_t(R.T));
   for (int64_t i = 0; i < R.T; ++i) order[size_t(i)] = uint32_t(i);
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+    return h_off[x + 1] - h_off[x] > h_off[y + 1] - h_off[y];
   });
   cp(L.order, order.data(), 4 * size_t(R.T));
   if (h_capacity) cp(L.cap, h_capacity, 8 * size_t(R.T));
@@ -623,6 +663,97 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
   int launches = 0;
   xm_lifecycle* d_rec = reinterpret_cast<xm_lifecycle*>(w + L.rec);
+  xm_batch b{};
+  b.bytes = reinterpret_cast<const int64_t*>(w + L.wbytes);
+  b.tag = reinterpret_cast<const uint32_t*>(w + L.wtag);
+  b.off = reinterpret_cast<const int64_t*>(w + L.woff);
+  b.n_ids = reinterpret_cast<const uint32_t*>(w + L.wnids);
+  b.order = reinterpret_cast<const uint32_t*>(w + L.order);
+  b.capacity = h_capacity ? reinterpret_cast<const uint64_t*>(w + L.cap) : nullptr;
+  b.n_traces = R.T;
+  b.n_events = R.E;
+  b.max_ids = R.max_ids;
+  b.max_events = R.max_events;
+  xm_result* d_out = reinterpret_cast<xm_result*>(w + L.out);
+  // Overlapped replay (the default for batches that fill the GPU): the loader
+  // runs on `loader_sms` SMs (one 32-warp CTA each, on the library's loader
+  // stream), longest trace first among those whose chunk has landed, and
+  // appends each finished trace to a completion queue; the replay runs on the
+  // other SMs from the start, its i-th pull taking the queue's i-th entry, so
+  // traces replay while the rest is still crossing PCIe; a second replay
+  // launch on the loader's SMs follows the loader and shares the first one's
+  // work counter. The two kernels cannot share an SM (registers), so each CTA
+  // holds a whole SM. The chunk copies are queued after the launches (the
+  // kernels wait on their flags), so the host's API calls overlap the GPU.
+  const ReplayPlan plan = plan_replay(&b, cfg);
+  int dev_sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+  }
+  const char* ov = std::getenv("XM_RAW_OVERLAP");                      // tooling: "0" = off
+  const char* lsm = std::getenv("XM_RAW_LOADER_SMS");                  // tooling
+  const int loader_sms = lsm ? std::atoi(lsm) : kRawLoaderSms;
+  const bool overlap = streamed && !(ov && ov[0] == '0') && plan.ctas >= dev_sms &&
+                       loader_sms >= 1 && loader_sms < dev_sms && L.total - L.scratch >= plan.scratch_bytes;
+  if (overlap) {
+    uint32_t* loaded = reinterpret_cast<uint32_t*>(w + L.loaded);
+    void* k2s = w + L.scratch;
+    // both modules loaded before either kernel runs: a lazy module load at a
+    // launch may wait for the running kernels, which here wait on the chunk
+    // copies queued after the launches
+    int pe = preload_loader();
+    if (!pe) pe = preload_replay();
+    if (pe) return set_error(XM_ECUDA, std::string("xm_simulate_raw: module load: ") +
+                                           cudaGetErrorString(cudaError_t(pe)));
+    e = cudaMemsetAsync(loaded, 0, 4 * size_t(R.T + 1), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(k2s, 0, 256, st);       // the replay's counters
+    if (e == cudaSuccess) e = cudaEventRecord(pp->meta, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->ls, pp->meta, 0);
+    if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw: ") + cudaGetErrorString(e));
+    int ek = launch_loader(d_bytes, d_tag, reinterpret_cast<const int64_t*>(w + L.off), R.T, R.E,
+                           R.max_events, w + L.k5, d_rec, reinterpret_cast<const uint32_t*>(w + L.order),
+                           reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
+                           reinterpret_cast<int64_t*>(w + L.woff), reinterpret_cast<uint32_t*>(w + L.wnids),
+                           pp->ls, &launches, chunk_first, chunk_flag, n_chunks,
+                           reinterpret_cast<const uint32_t*>(w + L.pos), loaded, loader_sms,
+                           reinterpret_cast<uint32_t*>(static_cast<char*>(k2s) + 4 * 24));
+    if (!ek) ek = launch_replay(&b, cfg, u, plan, k2s, d_out, st, &launches, nullptr, loaded,
+                                dev_sms - loader_sms, false);
+    if (!ek) ek = launch_replay(&b, cfg, u, plan, k2s, d_out, pp->ls, &launches, nullptr, loaded,
+                                loader_sms, false);
+    enqueue_chunks(pp->meta);    // also when a launch failed: `copied` must exist
+    // `stream` resumes after the loader's stream and the copies, also on failure
+    const cudaError_t e1 = cudaEventRecord(pp->ldone, pp->ls);
+    const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(st, pp->ldone, 0) : e1;
+    const cudaError_t e3 = cudaStreamWaitEvent(st, pp->copied, 0);
+    if (ek) return set_error(XM_ECUDA, std::string("xm_simulate_raw launch: ") + cudaGetErrorString(cudaError_t(ek)));
+    if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess || e3 != cudaSuccess)
+      return set_error(XM_ECUDA, std::string("stream wait: ") + cudaGetErrorString(e2 != cudaSuccess ? e2 : e3));
+    launch_counter() = launches;
+    std::vector<xm_lifecycle> rec(size_t(R.T));
+    uint32_t stall = 0;
+    e = cudaMemcpyAsync(h_out, d_out, sizeof(xm_result) * size_t(R.T), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(rec.data(), d_rec, sizeof(xm_lifecycle) * size_t(R.T), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&stall, static_cast<char*>(k2s) + 4 * 24, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw D2H: ") + cudaGetErrorString(e));
+    if (stall)
+      return set_error(XM_ECUDA, "xm_simulate_raw: the loader made no progress (too few free SMs for "
+                                 "the overlapped loader; set XM_RAW_OVERLAP=0)");
+    return raw_verdicts(rec, R.T, bad_trace);
+  }
+  if (streamed) {
+    // sequential: every copy and flag write is queued before the loader that
+    // waits on them
+    enqueue_chunks(nullptr);
+    if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw H2D: ") + cudaGetErrorString(e));
+  }
   int ek = launch_loader(d_bytes, d_tag, reinterpret_cast<const int64_t*>(w + L.off), R.T, R.E,
                          R.max_events, w + L.k5, d_rec, reinterpret_cast<const uint32_t*>(w + L.order),
                          reinterpret_cast<int64_t*>(w + L.wbytes), reinterpret_cast<uint32_t*>(w + L.wtag),
@@ -638,18 +769,6 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
       return set_error(XM_ECUDA, std::string("stream wait: ") + cudaGetErrorString(e2));
   }
   if (ek) return set_error(XM_ECUDA, std::string("xm_simulate_raw loader: ") + cudaGetErrorString(cudaError_t(ek)));
-  xm_batch b{};
-  b.bytes = reinterpret_cast<const int64_t*>(w + L.wbytes);
-  b.tag = reinterpret_cast<const uint32_t*>(w + L.wtag);
-  b.off = reinterpret_cast<const int64_t*>(w + L.woff);
-  b.n_ids = reinterpret_cast<const uint32_t*>(w + L.wnids);
-  b.order = reinterpret_cast<const uint32_t*>(w + L.order);
-  b.capacity = h_capacity ? reinterpret_cast<const uint64_t*>(w + L.cap) : nullptr;
-  b.n_traces = R.T;
-  b.n_events = R.E;
-  b.max_ids = R.max_ids;
-  b.max_events = R.max_events;
-  xm_result* d_out = reinterpret_cast<xm_result*>(w + L.out);
   rc = simulate(&b, cfg, w + L.scratch, L.total - L.scratch, d_out, stream, nullptr);
   launch_counter() += launches;
   if (rc) return rc;
@@ -660,18 +779,5 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     e = cudaMemcpyAsync(rec.data(), d_rec, sizeof(xm_lifecycle) * size_t(R.T), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_simulate_raw D2H: ") + cudaGetErrorString(e));
-  for (int64_t t = 0; t < R.T; ++t) {
-    const xm_lifecycle& r = rec[size_t(t)];
-    const char* m = r.n_invalid ? "zero-byte or >= 2^40 request (SPEC.md:231)"
-                  : r.n_reopened ? "alloc of a live id (SPEC.md:249)"
-                  : r.n_orphan ? "free of a non-live id (SPEC.md:258)"
-                  : r.n_mismatch ? "free size differs from the alloc's request (SPEC.md:258)"
-                  : r.n_ids > (1u << 27) ? "more than 2^27 live blocks" : nullptr;
-    if (m) {
-      if (bad_trace) *bad_trace = t;
-      return set_error(XM_EINVAL, std::string("xm_simulate_raw: trace ") + std::to_string(t) + ": " + m);
-    }
-  }
-  clear_error();
-  return XM_OK;
+  return raw_verdicts(rec, R.T, bad_trace);
 }

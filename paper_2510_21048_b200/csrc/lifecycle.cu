@@ -84,16 +84,26 @@ struct LParams {
   const uint32_t* chunk_first;            // loader mode, streamed input: [n_chunks + 1]
   const uint32_t* chunk_flag;             // first trace of each upload chunk, and its
   int n_chunks;                           // "landed" flag (0 until copied); or null
+  const uint32_t* pull;                   // loader mode, overlapped replay: traces are
+                                          // pulled in stored order (pull[k] = caller
+                                          // trace of stored k); or null (caller order)
+  uint32_t* stall;                        // overlapped mode: set when a chunk never lands
+                                          // (or the replay gave up); every waiter bails
+  uint32_t* loaded;                       // ... and each finished trace is appended to
+                                          // a completion queue: loaded[n_traces] is its
+                                          // tail, loaded[i] = stored index + 1 (release)
+                                          // once its wire events and n_ids are written
 };
 
 __device__ __forceinline__ uint32_t hash_addr(uint64_t a, uint32_t bits) {
   return uint32_t((a * 0x9E3779B97F4A7C15ull) >> (64 - bits));
 }
 
-__global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
+template <int kW>
+__global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
   const uint32_t lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const uint32_t slot = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t slot = blockIdx.x * kW + (threadIdx.x >> 5);
   Slot* T = P.tables + (size_t(slot) << P.hbits);
   uint32_t* ids = P.idstacks + size_t(slot) * P.max_events;
   for (;;) {
@@ -101,28 +111,44 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
     if (lane == 0) k = atomicAdd(P.work, 1u);
     k = __shfl_sync(kFull, k, 0);
     if (int64_t(k) >= P.n_traces) break;
-    if (P.chunk_flag) {                     // wait until trace k's chunk has landed
-      int lo = 0, hi = P.n_chunks - 1;      // the chunk c with first[c] <= k < first[c+1]
+    const unsigned t = P.pull ? P.pull[k] : k;   // the caller's trace
+    if (P.chunk_flag) {                     // wait until trace t's chunk has landed
+      int lo = 0, hi = P.n_chunks - 1;      // the chunk c with first[c] <= t < first[c+1]
       while (lo < hi) {
         const int m = (lo + hi + 1) >> 1;
-        if (P.chunk_first[m] <= k) lo = m; else hi = m - 1;
+        if (P.chunk_first[m] <= t) lo = m; else hi = m - 1;
       }
       uint32_t nap = 256;
+      unsigned long long t0 = 0;
+      bool gave_up = false;
       for (;;) {
         uint32_t r = 0;
         if (lane == 0)
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.chunk_flag + lo) : "memory");
         if (__shfl_sync(kFull, r, 0) != 0) break;
+        if (P.stall) {                      // overlapped: bounded wait (XM_LOADED_TIMEOUT_NS)
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          now = __shfl_sync(kFull, now, 0);
+          const uint32_t sv = __shfl_sync(kFull, *(volatile uint32_t*)P.stall, 0);
+          if (t0 == 0) t0 = now;
+          if (sv != 0 || now - t0 > 4000000000ull) {
+            if (lane == 0) atomicExch(P.stall, 1u);
+            gave_up = true;
+            break;
+          }
+        }
         __nanosleep(nap);
         nap = min(nap * 2, 4096u);
       }
       __syncwarp();
+      if (gave_up) break;
     }
-    const unsigned gen = k + 1;
-    const int64_t e0 = P.off[k];
-    const uint32_t sk = P.wire_off ? P.pos[k] : 0u;
+    const unsigned gen = t + 1;
+    const int64_t e0 = P.off[t];
+    const uint32_t sk = P.pull ? k : (P.wire_off ? P.pos[t] : 0u);
     const int64_t wire0 = P.wire_off ? P.wire_off[sk] : 0;
-    const int n = int(P.off[k + 1] - e0);
+    const int n = int(P.off[t + 1] - e0);
     // this trace's table: the first 2^hb slots of the warp's region, 2^hb > n
     // (at most n distinct addresses, so a free slot always exists; with about
     // half the instants allocations and addresses reused, the load stays well
@@ -295,13 +321,24 @@ __global__ void __launch_bounds__(32 * kWarps) k_reconstruct(LParams P) {
       r.max_open = max_open;
       r.n_ids = fresh;
       r.n_reopened = n_reopen;
-      P.rec[k] = r;
+      P.rec[t] = r;
       // direct wire output: a trace with any verdict (its wire events are not
       // the trace) gets n_ids 0, which the replay refuses (XM_T_INVALID)
       if (P.w_nids)
         P.w_nids[sk] = (n_orphan | n_mism | n_inv | n_reopen) || fresh > (1u << 27) ? 0u : fresh;
     }
     __syncwarp();
+    if (P.loaded) {
+      // publish: every lane's wire stores (and lane 0's n_ids) before the
+      // queue entry
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t at = atomicAdd(P.loaded + P.n_traces, 1u);
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.loaded + at), "r"(sk + 1u) : "memory");
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -433,7 +470,7 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   P.mismatch = d_mismatch;
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
-  k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
+  k_reconstruct<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(P);
   launch_counter() = 1;
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct: ") + cudaGetErrorString(e));
@@ -535,6 +572,14 @@ extern "C" int xm_blocks_from_instants(const xm_instants* in, const int64_t* d_t
 // ---- device loader (xm_simulate_raw): K5 keyed by raw block ids ------------------
 namespace xm_internal {
 
+// Loads the loader kernels' module now (see preload_replay).
+int preload_loader() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k_reconstruct<32>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_reconstruct<kWarps>);
+  return int(e);
+}
+
 // Scratch of the loader mode for T traces / E events / the longest trace.
 size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events) {
   xm_instants in{};
@@ -553,7 +598,8 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
                   int64_t E, uint32_t max_events, void* d_scratch, xm_lifecycle* d_rec,
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
                   uint32_t* w_nids, void* stream, int* n_launches, const uint32_t* chunk_first,
-                  const uint32_t* chunk_flag, int n_chunks, const uint32_t* d_pos) {
+                  const uint32_t* chunk_flag, int n_chunks, const uint32_t* d_pos,
+                  uint32_t* loaded, int loader_sms, uint32_t* stall) {
   xm_instants in{};
   in.n_traces = T;
   in.n_events = E;
@@ -589,7 +635,20 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
   P.chunk_first = chunk_first;
   P.chunk_flag = chunk_flag;
   P.n_chunks = n_chunks;
-  k_reconstruct<<<L.ctas, 32 * kWarps, 0, st>>>(P);
+  if (loaded && d_pos) {
+    // overlapped with the replay (xm_simulate_raw): pulled in stored order,
+    // flags published per trace, on `loader_sms` SMs -- one 32-warp CTA per SM
+    // (61K registers: no replay CTA fits beside it, nor a second one)
+    P.pull = d_order;
+    P.loaded = loaded;
+    P.stall = stall;
+    const uint32_t g = std::min<uint32_t>(uint32_t(std::max(loader_sms, 1)), L.n_slots / 32);
+    if (g >= 1) k_reconstruct<32><<<g, 32 * 32, 0, st>>>(P);
+    else k_reconstruct<kWarps><<<1, 32 * kWarps, 0, st>>>(P);
+    *n_launches += 1;
+    return int(cudaGetLastError());
+  }
+  k_reconstruct<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(P);
   if (d_pos) {                                      // written in place: no compaction
     *n_launches += 1;
     return int(cudaGetLastError());

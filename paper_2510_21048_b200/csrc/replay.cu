@@ -125,6 +125,9 @@ struct KParams {
   xm_result* out;
   uint64_t* curve;              // optional [n_events][3] memory-usage curve (NEXT-1)
   const uint32_t* ready;        // streamed input: stored traces resident so far, or null
+  const uint32_t* loaded;       // overlapped loader (xm_simulate_raw): its completion
+                                // queue, entry i = stored trace + 1 (release) once that
+                                // trace's wire events and n_ids are written; or null
   unsigned long long* timing;   // XM_TIMING builds: [T][2] globaltimer start/end
 };
 
@@ -1366,6 +1369,46 @@ __device__ void wait_ready(const uint32_t* ready, uint32_t k) {
   __syncwarp();
 }
 
+// Overlapped loader (xm_simulate_raw): the replay's i-th pull takes the i-th
+// trace the loader finished (its completion queue; the loader works
+// longest-first over the traces whose upload chunk has landed, so the replay
+// gets the longest trace that is actually loaded, never waiting on one still
+// crossing PCIe). The warp sleeps until entry i is written (acquire, pairing
+// with the loader's release, so the trace's wire events and n_ids are
+// visible) and returns stored index + 1. The loader runs on SMs of its own;
+// should it make no progress for XM_LOADED_TIMEOUT_NS (it cannot share an SM
+// with this kernel, so a device with too few free SMs would stall it), the
+// warp gives up: 0, and the launch's stall word is set (the host reports an
+// error).
+#ifndef XM_LOADED_TIMEOUT_NS
+#define XM_LOADED_TIMEOUT_NS 4000000000ull
+#endif
+__device__ uint32_t wait_loaded(const uint32_t* entry, uint32_t* stall) {
+  uint32_t nap = 256;
+  unsigned long long t0 = 0;
+  for (;;) {
+    uint32_t r;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(entry) : "memory");
+    r = __shfl_sync(kFull, r, 0);
+    if (r != 0) {
+      __syncwarp();
+      return r;
+    }
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    now = __shfl_sync(kFull, now, 0);
+    const uint32_t sv = __shfl_sync(kFull, *(volatile uint32_t*)stall, 0);
+    if (t0 == 0) t0 = now;
+    if (sv != 0 || now - t0 > XM_LOADED_TIMEOUT_NS) {   // the loader (or another waiter) gave up
+      if ((threadIdx.x & 31) == 0) atomicExch(stall, 1u);
+      __syncwarp();
+      return 0;
+    }
+    __nanosleep(nap);
+    nap = min(nap * 2, 4096u);
+  }
+}
+
 // kKnobs: the torch-knob variants (max_split_size / garbage_collection_threshold,
 // readings Q26/Q27) are a separate kernel, so the default one carries none of
 // their code or registers.
@@ -1397,14 +1440,22 @@ __global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
       break;
     }
     // stored trace k (events [off[k], off[k+1])) is the caller's trace order[k]
+    if (P.loaded) {                               // the k-th trace the loader finished
+      const uint32_t q = wait_loaded(P.loaded + k, P.counter + 24);
+      if (q == 0) {                               // the loader stalled: give up
+        ticket_release(hdr);
+        continue;
+      }
+      k = q - 1;
+    }
     const uint32_t t = P.order[k];
     const int64_t e0 = P.off[k];
     const uint32_t n = uint32_t(P.off[k + 1] - e0);
+    xm_result R;
     const uint32_t na = P.n_ids[k];
     const uint64_t cap = P.capacity ? P.capacity[t] : P.cap_default;
     if (P.ready) wait_ready(P.ready, k);
     const uint64_t cap_u = cap >> P.u.unit_shift;
-    xm_result R;
     if (na == 0 && n > 0) {                       // no ids for its events: refused
       ticket_release(hdr);                        // (held since the pull)
       if (lane == 0) {
@@ -1520,12 +1571,24 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   return p;
 }
 
+// Loads k_replay's module now (under CUDA's lazy loading a kernel's module is
+// loaded at its first launch, which may wait for running kernels -- fatal
+// when those wait on work queued after it, as in the overlapped raw path).
+int preload_replay() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k_replay<false>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_replay<true>);
+  return int(e);
+}
+
 int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
                   const ReplayPlan& plan, void* d_scratch, xm_result* d_out, void* stream,
-                  int* n_launches, const uint32_t* ready) {
+                  int* n_launches, const uint32_t* ready, const uint32_t* loaded, int ctas,
+                  bool reset) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   KParams P{};
   P.ready = ready;
+  P.loaded = loaded;
   P.bytes = b->bytes;
   P.packed = reinterpret_cast<const unsigned long long*>(b->packed);
   P.tag = b->tag;
@@ -1549,14 +1612,16 @@ int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
   P.timing = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(d_scratch) + 256 +
                                                    size_t(plan.n_arena) * plan.arena_per_warp);
 #endif
-  cudaError_t e = cudaMemsetAsync(d_scratch, 0, 256, st);
+  // reset = false: a second launch on the same work counter (xm_simulate_raw's
+  // overlapped replay), which the first launch's reset covers
+  cudaError_t e = reset ? cudaMemsetAsync(d_scratch, 0, 256, st) : cudaSuccess;
   if (e != cudaSuccess) return int(e);
   const size_t smem = kHdrBytes + size_t(plan.heap_pages) * kPage;
   const bool knobs = u.msplit_u != 0xFFFFFFFFu || u.gc_threshold > 0.0;
   auto kern = knobs ? k_replay<true> : k_replay<false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return int(e);
-  kern<<<plan.ctas, plan.warps_per_cta * 32, smem, st>>>(P);
+  kern<<<ctas > 0 ? ctas : plan.ctas, plan.warps_per_cta * 32, smem, st>>>(P);
   *n_launches += 1;
   return int(cudaGetLastError());
 }

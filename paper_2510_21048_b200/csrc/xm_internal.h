@@ -63,10 +63,16 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg);
 // Kernel launchers (replay.cu / scan.cu). Return cudaError_t as int.
 int launch_replay(const xm_batch* b, const xm_config* cfg, const UnitConfig& u,
                   const ReplayPlan& plan, void* d_scratch, xm_result* d_out, void* stream,
-                  int* n_launches, const uint32_t* ready = nullptr);
+                  int* n_launches, const uint32_t* ready = nullptr,
+                  const uint32_t* loaded = nullptr, int ctas = 0, bool reset = true);
 int launch_scan(const xm_batch* b, const UnitConfig& u, void* d_scratch, size_t scratch_bytes,
                 xm_result* d_out, void* stream, int* n_launches);
 size_t scan_scratch_bytes(const xm_batch* b);
+
+// Force-load a kernel module before kernels that wait on each other run
+// concurrently (CUDA lazy loading); return cudaError_t as int.
+int preload_replay();
+int preload_loader();
 
 // Device loader of xm_simulate_raw (lifecycle.cu): K5 keyed by raw block ids.
 size_t loader_scratch_bytes(int64_t T, int64_t E, uint32_t max_events);
@@ -75,6 +81,7 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
                   const uint32_t* d_order, int64_t* w_bytes, uint32_t* w_tag, int64_t* w_off,
                   uint32_t* w_nids, void* stream, int* n_launches,
                   const uint32_t* chunk_first = nullptr, const uint32_t* chunk_flag = nullptr,
-                  int n_chunks = 0, const uint32_t* d_pos = nullptr);
+                  int n_chunks = 0, const uint32_t* d_pos = nullptr, uint32_t* loaded = nullptr,
+                  int loader_sms = 0, uint32_t* stall = nullptr);
 
 }  // namespace xm_internal

@@ -111,3 +111,66 @@ def test_raw_streamed_equals_in_place(monkeypatch):
     h2 = _raw(b, pinned=True)
     assert (h1 == h2).all()
     assert_parity(b, h1, oracle_run(b))
+
+
+def _big_mixed(salt):
+    """More traces than the replay has warp slots (148 SMs x 14), so
+    xm_simulate_raw overlaps the loader with the replay: short fuzz traces, a
+    capacity corpus (OOMs, reclamation) and long training traces."""
+    return concat([fuzz.spec1_corpus(1800, 400, salt=salt), fuzz.capacity_corpus(400, 500, salt=salt + 1),
+                   suites.config2(), fuzz.small_size_corpus(300, 300, salt=salt + 2)])
+
+
+@pytest.mark.parametrize("loader_sms", ["1", "17", "48", "100", "147"])
+def test_raw_overlapped_replay(monkeypatch, loader_sms):
+    """The overlapped path (loader on XM_RAW_LOADER_SMS SMs publishing traces
+    as it finishes them, the replay on the rest, then a second replay launch
+    on the loader's SMs) equals the oracle and the sequential path
+    (XM_RAW_OVERLAP=0), whatever the split."""
+    b = _big_mixed(61)
+    assert b.n_traces > 148 * 14
+    monkeypatch.setenv("XM_RAW_LOADER_SMS", loader_sms)
+    h = _raw(b, pinned=True)
+    assert xm.last_launch_count() == 3             # loader + two replay launches
+    assert_parity(b, h, oracle_run(b, parallel=True))
+    monkeypatch.setenv("XM_RAW_OVERLAP", "0")
+    assert (_raw(b, pinned=True) == h).all()
+
+
+@pytest.mark.parametrize("kind", ["dup", "nonlive", "size", "zero"])
+def test_raw_overlapped_rejects(kind):
+    """A contract violation inside a batch large enough for the overlapped
+    path is reported with its trace index, as on the sequential path."""
+    b = _big_mixed(71)
+    bad = _bad(kind)
+    at = 1234
+    b = concat([b.subset(range(at)), bad.subset([3]), b.subset(range(at, b.n_traces))])
+    with pytest.raises(xm.XMemError) as e:
+        _raw(b, pinned=True)
+    assert e.value.bad_trace == at
+    assert f"trace {at}" in str(e.value)
+
+
+def test_raw_overlapped_first_call_in_fresh_process():
+    """The overlapped path's first call in a process (kernel modules not yet
+    loaded: CUDA lazy loading must not stall the concurrently running loader
+    and replay)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, paper_2510_21048_b200 as xm\n"
+            "from workloads import suites\n"
+            "b = suites.config4()\n"
+            "by = torch.from_numpy(b.bytes).pin_memory().numpy()\n"
+            "tg = torch.from_numpy(b.tag.view(np.int32)).pin_memory().numpy().view(np.uint32)\n"
+            "h, _ = xm.simulate_raw(by, tg, b.off, xm.Config(), capacity=b.capacity)\n"
+            "assert xm.last_launch_count() == 3\n"
+            "np.save('/tmp/xm_fresh_raw.npy', h)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, CUDA_MODULE_LOADING="LAZY")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    h = np.load("/tmp/xm_fresh_raw.npy")
+    b = suites.config4()
+    assert_parity(b, h, oracle_run(b, parallel=True))

@@ -1,6 +1,7 @@
 """Where xm_simulate_raw's time goes on config 4: torch.profiler (CUPTI) trace
-of one call: the kernels, the copies and the host gaps between them."""
-import os, sys, json
+of one call: the kernels (start, duration), the first and last copy, the
+host gaps."""
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2510_21048_b200 as xm
@@ -14,14 +15,14 @@ from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     xm.simulate_raw(pin_b, pin_t, b.off, xm.Config(), capacity=b.capacity, workspace=ws)
     torch.cuda.synchronize()
-evs = [e for e in prof.events() if e.device_type.name == "CUDA" or "Memcpy" in e.name or "cuda" in e.name.lower()]
-rows = []
-t0 = None
-for e in sorted(prof.events(), key=lambda e: e.time_range.start):
-    if t0 is None:
-        t0 = e.time_range.start
-    rows.append((round((e.time_range.start - t0) / 1e3, 3), round((e.time_range.end - e.time_range.start) / 1e3, 3),
-                 e.device_type.name, e.name[:60]))
-for r in rows:
-    if r[1] > 0.02 or r[2] == "CUDA":
-        print(r)
+ev = sorted(prof.events(), key=lambda e: e.time_range.start)
+t0 = ev[0].time_range.start
+cuda = [e for e in ev if e.device_type.name == "CUDA"]
+cp = [e for e in cuda if "HtoD" in e.name]
+ker = [e for e in cuda if "Memcpy" not in e.name and "Memset" not in e.name]
+f = lambda x: round((x - t0) / 1e3, 3)
+if cp:
+    print("H2D copies:", len(cp), "first start", f(cp[0].time_range.start), "last end", f(max(e.time_range.end for e in cp)))
+for e in ker:
+    print("kernel", e.name[:50], "start", f(e.time_range.start), "end", f(e.time_range.end))
+print("last event end", f(max(e.time_range.end for e in cuda)))
