@@ -504,9 +504,9 @@ def main():
         e2e = {"value": done / dt_dev_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw),
                "d2h_bytes_per_step": int(128 * batch.n_traces), "ms_per_step": dt_dev_raw * 1e3,
                "api": "xm_simulate_raw: the caller's raw arrays (page-locked host memory) "
-                      "copied to the device in 24 chunks of whole traces on a copy stream; "
-                      "the device loader (K5 keyed by raw block id: validation "
-                      "S:231/S:249/S:258, dense ids, LPT-stored wire arrays) on 24 SMs, "
+                      "copied to the device in 48 chunks of whole traces on a copy stream; "
+                      "the device loader (k_load, keyed by raw block id: validation "
+                      "S:231/S:249/S:258, dense ids, LPT-stored wire arrays) on 16 SMs, "
                       "longest first among the traces whose chunk has landed, appending each "
                       "finished trace to a completion queue; k_replay on the other SMs from "
                       "the start, popping that queue, then on the loader's SMs too -> results "

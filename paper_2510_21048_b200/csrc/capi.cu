@@ -427,8 +427,8 @@ struct RawLayout {
 };
 
 constexpr int kRawChunks = 256;         // most upload chunks of xm_simulate_raw (ready area)
-constexpr int kRawDefaultChunks = 24;   // upload chunks by default
-constexpr int kRawLoaderSms = 24;       // SMs of the overlapped loader by default
+constexpr int kRawDefaultChunks = 48;   // upload chunks by default (tuned, config 4)
+constexpr int kRawLoaderSms = 16;       // SMs of the overlapped loader by default (tuned)
 
 struct RawShape {
   int64_t T, E;

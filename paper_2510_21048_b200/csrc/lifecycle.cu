@@ -342,6 +342,217 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
   }
 }
 
+// ---- k_load: the device loader of xm_simulate_raw ------------------------------
+// The loader mode of k_reconstruct, specialised: the key is the raw block id,
+// and a valid trace has at most one open block per key, so
+// the hash slot itself holds the open block's record -- no per-allocation
+// records, no stacks of blocks per key -- and a valid trace keeps every event,
+// so event i's wire form goes straight to wire0 + i. The next tile's events
+// are loaded while the current one is matched. Slot (16 B, one load per probe
+// step): w0 raw id, w1 generation (trace + 1, 24 bits) | request bits 32-39
+// << 24, w2 dense id | stream << 28, w3 request bits 0-31; open iff the
+// request is nonzero (a close stores 0). Verdicts and tallies as k_reconstruct
+// (invalid: zero or >= 2^40 bytes; reopened: alloc of an open id; orphan: free
+// of a key with no open block; mismatch: free bytes != the alloc's).
+template <int kW>
+__global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t slot = blockIdx.x * kW + (threadIdx.x >> 5);
+  uint4* T = reinterpret_cast<uint4*>(P.tables + (size_t(slot) << P.hbits));
+  uint32_t* ids = P.idstacks + size_t(slot) * P.max_events;
+  const long long* by = reinterpret_cast<const long long*>(P.bytes);
+  for (;;) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(P.work, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (int64_t(k) >= P.n_traces) break;
+    const unsigned t = P.pull ? P.pull[k] : k;   // the caller's trace
+    if (P.chunk_flag) {                     // wait until trace t's chunk has landed
+      int lo = 0, hi = P.n_chunks - 1;
+      while (lo < hi) {
+        const int m = (lo + hi + 1) >> 1;
+        if (P.chunk_first[m] <= t) lo = m; else hi = m - 1;
+      }
+      uint32_t nap = 256;
+      unsigned long long t0 = 0;
+      bool gave_up = false;
+      for (;;) {
+        uint32_t r = 0;
+        if (lane == 0)
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.chunk_flag + lo) : "memory");
+        if (__shfl_sync(kFull, r, 0) != 0) break;
+        if (P.stall) {                      // overlapped: bounded wait
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          now = __shfl_sync(kFull, now, 0);
+          const uint32_t sv = __shfl_sync(kFull, *(volatile uint32_t*)P.stall, 0);
+          if (t0 == 0) t0 = now;
+          if (sv != 0 || now - t0 > 4000000000ull) {
+            if (lane == 0) atomicExch(P.stall, 1u);
+            gave_up = true;
+            break;
+          }
+        }
+        __nanosleep(nap);
+        nap = min(nap * 2, 4096u);
+      }
+      __syncwarp();
+      if (gave_up) break;
+    }
+    const uint32_t gen = (t + 1u) & 0xFFFFFFu;    // the host keeps T < 2^24 here
+    const int64_t e0 = P.off[t];
+    const uint32_t sk = P.pull ? k : P.pos[t];
+    const int64_t wire0 = P.wire_off[sk];
+    const int n = int(P.off[t + 1] - e0);
+    uint32_t hb = 6;
+    while ((1u << hb) < uint32_t(n) + 1u && hb < P.hbits) ++hb;
+    const uint32_t hmask = (1u << hb) - 1u;
+    for (uint32_t h = lane; h <= hmask; h += 32) T[h] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+    uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
+    unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_inv = 0, n_reopen = 0;
+    // the first tile's events; each tile loads the next one's
+    long long b_nx = 0;
+    uint32_t g_nx = 0;
+    if (int(lane) < n) {
+      b_nx = __ldcg(by + e0 + lane);
+      g_nx = __ldcg(P.tag + e0 + lane);
+    }
+    for (int base = 0; base < n; base += 32) {
+      const int li = base + int(lane);
+      const bool valid = li < n;
+      long long b = b_nx;
+      const uint32_t g = g_nx;
+      if (li + 32 < n) {
+        b_nx = __ldcg(by + e0 + li + 32);
+        g_nx = __ldcg(P.tag + e0 + li + 32);
+      }
+      if (b >= (long long)(XM_MAX_REQUEST) || b <= -(long long)(XM_MAX_REQUEST)) b = 0;
+      const uint32_t key = valid ? (g & 0x0FFFFFFFu) : (0xF0000000u | lane);   // never a raw id
+      const uint32_t s = g >> 28;
+      const bool is_alloc = valid && b > 0, is_free = valid && b < 0;
+      // ---- dense ids for this tile's allocations (ids freed before the tile) ----
+      const unsigned am = __ballot_sync(kFull, is_alloc);
+      const uint32_t na = __popc(am), ka = __popc(am & lt);
+      const uint32_t take = min(na, top);
+      uint32_t my_tag = 0;
+      if (is_alloc) my_tag = (ka < take ? ids[top - 1 - ka] : fresh + (ka - take)) | (s << 28);
+      top -= take;
+      fresh += na - take;
+      __syncwarp();
+      // ---- matching: one open block per key; a key's instants in this tile
+      // are applied in time order (round r: every key's r-th instant) ----
+      bool matched = false, reopened = false, mism = false;
+      uint32_t blk_tag = 0;
+      const unsigned grp = __match_any_sync(kFull, key);
+      const uint32_t my_rank = __popc(grp & lt);
+      const uint32_t rounds = __reduce_max_sync(kFull, valid ? uint32_t(__popc(grp)) : 0u);
+      const unsigned long long ub = static_cast<unsigned long long>(b);
+      for (uint32_t r = 0; r < rounds; ++r) {
+        const bool act = valid && b != 0 && my_rank == r;
+        uint32_t h = hash_addr(key, hb);
+        bool found = false;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (act) {
+          for (;;) {                         // read phase: my key or the first free slot
+            v = T[h];
+            if ((v.y & 0xFFFFFFu) != gen) break;
+            if (v.x == key) { found = true; break; }
+            h = (h + 1) & hmask;
+          }
+        }
+        // claim phase for allocations of new keys: lanes aiming at the same
+        // free slot -> the lowest wins, the others probe on
+        bool pend = act && is_alloc && !found;
+        while (__any_sync(kFull, pend)) {
+          const unsigned same = __match_any_sync(kFull, pend ? h : 0xFFFFFFFFu);
+          const bool win = pend && (__ffs(same) - 1) == int(lane);
+          __syncwarp();
+          if (win) T[h] = make_uint4(key, gen | (uint32_t(ub >> 32) << 24), my_tag, uint32_t(ub));
+          __syncwarp();
+          if (pend && !win) {
+            h = (h + 1) & hmask;
+            for (;;) {
+              if ((T[h].y & 0xFFFFFFu) != gen) break;
+              h = (h + 1) & hmask;
+            }
+          }
+          pend = pend && !win;
+        }
+        __syncwarp();
+        if (act) {
+          const bool is_open = found && ((v.y >> 24) | v.w) != 0u;
+          if (is_alloc) {
+            if (found) {                      // a known key: (re)opened with this block
+              reopened = is_open;
+              T[h] = make_uint4(key, gen | (uint32_t(ub >> 32) << 24), my_tag, uint32_t(ub));
+            }
+          } else if (is_open) {
+            matched = true;
+            blk_tag = v.z;
+            const unsigned long long ab = (static_cast<unsigned long long>(v.y >> 24) << 32) | v.w;
+            mism = ab != static_cast<unsigned long long>(-b);
+            T[h] = make_uint4(key, gen, v.z, 0u);    // closed
+          }
+        }
+        __syncwarp();
+      }
+      __syncwarp();
+      // ---- matched blocks' ids go back on the stack ----
+      const unsigned mm = __ballot_sync(kFull, matched);
+      if (matched) ids[top + __popc(mm & lt)] = blk_tag & 0x0FFFFFFFu;
+      top += __popc(mm);
+      // ---- the wire event in place (a valid trace keeps every event) ----
+      if (valid) {
+        P.st_bytes[wire0 + li] = b;
+        P.st_tag[wire0 + li] = is_alloc ? my_tag : blk_tag;
+      }
+      // ---- open count and tallies ----
+      int d = is_alloc ? 1 : (matched ? -1 : 0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, d, o);
+        if (int(lane) >= o) d += y;
+      }
+      const uint32_t mo = __reduce_max_sync(kFull, uint32_t(int(open) + d));
+      max_open = max(max_open, mo);
+      open = uint32_t(int(open) + __shfl_sync(kFull, d, 31));
+      n_blocks += na;
+      n_matched += __popc(mm);
+      n_orphan += __popc(__ballot_sync(kFull, is_free && !matched));
+      n_mism += __popc(__ballot_sync(kFull, mism));
+      n_inv += __popc(__ballot_sync(kFull, valid && b == 0));
+      n_reopen += __popc(__ballot_sync(kFull, reopened));
+      __syncwarp();
+    }
+    if (lane == 0) {
+      xm_lifecycle r;
+      r.n_blocks = n_blocks;
+      r.n_orphan = n_orphan;
+      r.n_mismatch = n_mism;
+      r.n_persistent = n_blocks - n_matched;
+      r.n_kept = n_blocks + n_matched;
+      r.n_invalid = n_inv;
+      r.max_open = max_open;
+      r.n_ids = fresh;
+      r.n_reopened = n_reopen;
+      P.rec[t] = r;
+      P.w_nids[sk] = (n_orphan | n_mism | n_inv | n_reopen) || fresh > (1u << 27) ? 0u : fresh;
+    }
+    __syncwarp();
+    if (P.loaded) {                         // publish (see k_reconstruct)
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t at = atomicAdd(P.loaded + P.n_traces, 1u);
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.loaded + at), "r"(sk + 1u) : "memory");
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // exclusive scan of rec[order[k]].n_kept over stored k -> woff[T+1] (one CTA)
 __global__ void __launch_bounds__(1024) k_wire_offsets(const xm_lifecycle* rec,
                                                        const uint32_t* order, int64_t T,
@@ -577,6 +788,8 @@ int preload_loader() {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, k_reconstruct<32>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_reconstruct<kWarps>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_load<32>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_load<kWarps>);
   return int(e);
 }
 
@@ -635,16 +848,31 @@ int launch_loader(const int64_t* d_bytes, const uint32_t* d_tag, const int64_t* 
   P.chunk_first = chunk_first;
   P.chunk_flag = chunk_flag;
   P.n_chunks = n_chunks;
+  // k_load where it applies (direct wire output, generations fit 24 bits;
+  // XM_LOADER=k5 forces k_reconstruct, tooling), else k_reconstruct
+  const char* lk = std::getenv("XM_LOADER");
+  const bool lean = d_pos && T < (int64_t(1) << 24) && !(lk && lk[0] == 'k');
   if (loaded && d_pos) {
     // overlapped with the replay (xm_simulate_raw): pulled in stored order,
-    // flags published per trace, on `loader_sms` SMs -- one 32-warp CTA per SM
-    // (61K registers: no replay CTA fits beside it, nor a second one)
+    // each finished trace appended to the completion queue, on `loader_sms`
+    // SMs -- one 32-warp CTA per SM (a whole SM's registers: no replay CTA
+    // fits beside it, nor a second one)
     P.pull = d_order;
     P.loaded = loaded;
     P.stall = stall;
     const uint32_t g = std::min<uint32_t>(uint32_t(std::max(loader_sms, 1)), L.n_slots / 32);
-    if (g >= 1) k_reconstruct<32><<<g, 32 * 32, 0, st>>>(P);
-    else k_reconstruct<kWarps><<<1, 32 * kWarps, 0, st>>>(P);
+    if (g >= 1) {
+      if (lean) k_load<32><<<g, 32 * 32, 0, st>>>(P);
+      else k_reconstruct<32><<<g, 32 * 32, 0, st>>>(P);
+    } else {
+      if (lean) k_load<kWarps><<<1, 32 * kWarps, 0, st>>>(P);
+      else k_reconstruct<kWarps><<<1, 32 * kWarps, 0, st>>>(P);
+    }
+    *n_launches += 1;
+    return int(cudaGetLastError());
+  }
+  if (lean) {
+    k_load<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(P);
     *n_launches += 1;
     return int(cudaGetLastError());
   }
