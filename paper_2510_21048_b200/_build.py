@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                *([f"-DXM_MAX_NAP={os.environ['XM_MAX_NAP']}"] if os.environ.get("XM_MAX_NAP") else []),
                *([f"-DXM_K1_PER_LANE={os.environ['XM_K1_PER_LANE']}"] if os.environ.get("XM_K1_PER_LANE") else []),
                *[f"-D{k}={os.environ[k]}" for k in ("XM_K1C_PER", "XM_K1C_STAGES", "XM_K1C_CTAS_PER_SM", "XM_K1C_THREADS",
-                           "XM_F_GROW_NUM", "XM_F_GROW_DEN", "XM_K1_MINB")
+                           "XM_F_GROW_NUM", "XM_F_GROW_DEN", "XM_K1_MINB", "XM_K2_THREADS", "XM_K2_WARPS", "XM_K2_UNROLL")
                  if os.environ.get(k)],
                "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-Wall", "-I", INCLUDE, "-I", CSRC, "-c", path,

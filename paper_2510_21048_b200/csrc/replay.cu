@@ -59,6 +59,15 @@
 #ifndef XM_F_GROW_DEN
 #define XM_F_GROW_DEN 1
 #endif
+#ifndef XM_K2_THREADS
+#define XM_K2_THREADS 512       // launch bound of k_replay (registers: 65536 / this)
+#endif
+#ifndef XM_K2_WARPS
+#define XM_K2_WARPS 14          // default warps (resident traces) per CTA
+#endif
+#ifndef XM_K2_UNROLL
+#define XM_K2_UNROLL 1          // events per iteration of the per-event loop (A/B)
+#endif
 #ifndef XM_HEAP_RESERVE_DIV
 #define XM_HEAP_RESERVE_DIV 24  // admission keeps 1/24 of the heap for free-list growth (tuned)
 #endif
@@ -86,6 +95,7 @@ constexpr uint32_t kKeyBits = 27;
 constexpr uint32_t kKeyMax = (1u << kKeyBits) - 1u;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr size_t kArenaBudget = XM_ARENA_BUDGET;
+constexpr int kK2Unroll = XM_K2_UNROLL;
 constexpr int kStatusOk = XM_T_OK, kStatusOom = XM_T_OOM, kStatusOverflow = XM_T_OVERFLOW;
 
 // shared-memory heap geometry
@@ -988,6 +998,7 @@ __device__ __forceinline__ int replay_trace(const KParams& P, State<L>& S, Grow&
     const uint32_t key1 = make_key(((tc >> 28) << 1) | (su <= u.small_u ? 1u : 0u), su);
 
     uint32_t j = 0;
+#pragma unroll kK2Unroll
     for (; j < cnt; ++j) {
       const uint32_t s = __shfl_sync(kFull, su, j);
       const uint32_t w = __shfl_sync(kFull, w1, j);
@@ -1413,7 +1424,7 @@ __device__ uint32_t wait_loaded(const uint32_t* entry, uint32_t* stall) {
 // readings Q26/Q27) are a separate kernel, so the default one carries none of
 // their code or registers.
 template <bool kKnobs>
-__global__ void __launch_bounds__(512, 1) k_replay(KParams P) {
+__global__ void __launch_bounds__(XM_K2_THREADS, 1) k_replay(KParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   HeapHdr* hdr = reinterpret_cast<HeapHdr*>(smem);
   unsigned char* pages = smem + kHdrBytes;
@@ -1535,8 +1546,8 @@ ReplayPlan plan_replay(const xm_batch* b, const xm_config* cfg) {
   if (cuda_usable() && cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : 14;
-  if (p.warps_per_cta > 16) p.warps_per_cta = 16;
+  p.warps_per_cta = cfg->warps_per_cta ? int(cfg->warps_per_cta) : XM_K2_WARPS;
+  if (p.warps_per_cta > XM_K2_THREADS / 32) p.warps_per_cta = XM_K2_THREADS / 32;
   if (p.warps_per_cta < 1) p.warps_per_cta = 1;
   // heap: the whole per-CTA maximum unless capped (smem_per_warp x warps)
   size_t heap = size_t(kMaxPages) * kPage;
