@@ -174,3 +174,27 @@ def test_raw_overlapped_first_call_in_fresh_process():
     h = np.load("/tmp/xm_fresh_raw.npy")
     b = suites.config4()
     assert_parity(b, h, oracle_run(b, parallel=True))
+
+
+def test_raw_overlapped_wide_layout_traces():
+    """Traces that leave the shared-memory layout (>= 64 GiB blocks, a 1 TiB
+    request) spread through a batch large enough for the overlapped path:
+    both replay launches restart them in the global arena, sharing its slots."""
+    G = 1 << 30
+    tb = TraceBuilder()
+    for r in range(40):
+        tb.alloc(0, 70 * G).alloc(1, 66 * G).free(0).free(1).alloc(2, 65 * G).alloc(3, 69 * G)
+        tb.free(2).alloc(4, 66 * G - 4096).free(3).free(4).alloc(5, 67 * G).end_trace()
+        tb.alloc(0, (1 << 40) - 1 - r).alloc(1, 512).free(1).end_trace()
+        tb.alloc(0, 100 * G).free(0).alloc(1, 150 * G).alloc(2, 40 * G).free(1).alloc(3, 120 * G)
+        tb.end_trace(capacity=200 * G)
+    wide = tb.build()
+    big = _big_mixed(81)
+    parts, step = [], big.n_traces // wide.n_traces
+    for i in range(wide.n_traces):
+        parts += [big.subset(range(i * step, (i + 1) * step)), wide.subset([i])]
+    parts.append(big.subset(range(wide.n_traces * step, big.n_traces)))
+    b = concat(parts)
+    h = _raw(b, pinned=True)
+    assert xm.last_launch_count() == 3
+    assert_parity(b, h, oracle_run(b, parallel=True))
