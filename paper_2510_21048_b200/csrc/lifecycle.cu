@@ -40,6 +40,20 @@
 
 #include "xm_internal.h"
 
+#ifdef XM_DEBUG
+#include <cstdio>
+#define XM_CHECK(cond, ...)                                   \
+  do {                                                        \
+    if (!(cond)) {                                            \
+      printf("XM_CHECK %s:%d: ", __FILE__, __LINE__);         \
+      printf(__VA_ARGS__);                                    \
+      __trap();                                               \
+    }                                                         \
+  } while (0)
+#else
+#define XM_CHECK(cond, ...) do {} while (0)
+#endif
+
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
@@ -437,6 +451,7 @@ __global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
       const uint32_t na = __popc(am), ka = __popc(am & lt);
       const uint32_t take = min(na, top);
       uint32_t my_tag = 0;
+      XM_CHECK(top <= P.max_events, "k_load: id stack %u > %u\n", top, P.max_events);
       if (is_alloc) my_tag = (ka < take ? ids[top - 1 - ka] : fresh + (ka - take)) | (s << 28);
       top -= take;
       fresh += na - take;
@@ -455,7 +470,9 @@ __global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
         bool found = false;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (act) {
+          uint32_t steps = 0;
           for (;;) {                         // read phase: my key or the first free slot
+            XM_CHECK(++steps <= hmask + 1u, "k_load: probe wrapped the table (2^%u slots)\n", hb);
             v = T[h];
             if ((v.y & 0xFFFFFFu) != gen) break;
             if (v.x == key) { found = true; break; }
@@ -503,7 +520,9 @@ __global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
       const unsigned mm = __ballot_sync(kFull, matched);
       if (matched) ids[top + __popc(mm & lt)] = blk_tag & 0x0FFFFFFFu;
       top += __popc(mm);
+      XM_CHECK(top <= P.max_events, "k_load: id stack %u > %u\n", top, P.max_events);
       // ---- the wire event in place (a valid trace keeps every event) ----
+      XM_CHECK(!valid || wire0 + li < P.wire_off[sk + 1], "k_load: wire index past trace %u\n", sk);
       if (valid) {
         P.st_bytes[wire0 + li] = b;
         P.st_tag[wire0 + li] = is_alloc ? my_tag : blk_tag;

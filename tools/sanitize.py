@@ -62,4 +62,16 @@ r["m_peak_meas1"] = 1 << 30
 r["m_peak_meas2"] = 1 << 30
 xm.metrics(r)                                                                  # metrics
 torch.cuda.synchronize()
+# raw path with the loader overlapped with the replay (> 148 x 14 traces). The
+# kernels wait on each other, so a tool that serialises kernels makes the
+# bounded waits give up (an XMemError, reported here) instead of hanging.
+ob_ = fuzz.spec1_corpus(2300, 24, salt=9)
+pb = torch.from_numpy(ob_.bytes).pin_memory().numpy()
+pt = torch.from_numpy(ob_.tag.view(np.int32)).pin_memory().numpy().view(np.uint32)
+try:
+    xm.simulate_raw(pb, pt, ob_.off, xm.Config())                             # overlapped raw path
+    print("overlapped raw path: ok, launches", xm.last_launch_count())
+except xm.XMemError as e:
+    print("overlapped raw path: gave up under the tool:", e)
+torch.cuda.synchronize()
 print("sanitize run done")
