@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (act) {
           uint32_t steps = 0;
+          (void)steps;
           for (;;) {                         // read phase: my key or the first free slot
             XM_CHECK(++steps <= hmask + 1u, "k_load: probe wrapped the table (2^%u slots)\n", hb);
             v = T[h];
