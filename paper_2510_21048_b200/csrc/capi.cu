@@ -429,6 +429,7 @@ struct RawLayout {
 constexpr int kRawChunks = 256;         // most upload chunks of xm_simulate_raw (ready area)
 constexpr int kRawDefaultChunks = 48;   // upload chunks by default (tuned, config 4)
 constexpr int kRawLoaderSms = 16;       // SMs of the overlapped loader by default (tuned)
+constexpr int kRawFlagEvery = 1;        // landed count published after every n-th chunk
 
 struct RawShape {
   int64_t T, E;
@@ -451,7 +452,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.woff = p; p += al(8 * (T + 1));
   L.wnids = p; p += al(4 * T);
   L.out = p; p += al(sizeof(xm_result) * T);
-  L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 1));   // chunk firsts + flags
+  L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 2));   // chunk firsts, landed + ranks
   L.pos = p; p += al(4 * T);                                        // caller -> stored index
   L.loaded = p; p += al(4 * (T + 1));                               // completion queue + tail
   L.scratch = p;
@@ -564,7 +565,8 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   int n_chunks = 0;
   Pipe* pp = nullptr;
   static thread_local std::vector<uint32_t> firsts;    // outlive the async copies
-  static thread_local std::vector<uint32_t> ones;
+  static thread_local std::vector<uint32_t> ones;      // chunk ranks (upload)
+  static thread_local std::vector<uint32_t> counts;    // landed-count values (fallback copies)
   std::vector<int> corder;
   if (streamed) {
     // chunks: whole traces up to about (c+1)/n of the events (n: XM_RAW_CHUNKS,
@@ -590,13 +592,19 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     n_chunks = int(firsts.size());
     firsts.push_back(uint32_t(R.T));
     cp(L.ready, firsts.data(), sizeof(uint32_t) * firsts.size());
-    if (e == cudaSuccess) e = cudaMemsetAsync(chunk_flag, 0, sizeof(uint32_t) * kRawChunks, st);
     if (e == cudaSuccess) e = get_pipe(&pp);
-    ones.assign(kRawChunks, 1u);
     corder.resize(size_t(n_chunks));
     for (int c = 0; c < n_chunks; ++c) corder[size_t(c)] = c;
     std::stable_sort(corder.begin(), corder.end(),
                      [&](int x, int y) { return maxlen[size_t(x)] > maxlen[size_t(y)]; });
+    // chunk_flag[0]: chunks landed so far (0 now); [1 + c]: chunk c's rank in
+    // the copy order. ones[i] = i + 1 (the landed count's values, for the
+    // fallback copy where the driver lacks cuStreamWriteValue32)
+    ones.assign(size_t(kRawChunks) + 1, 0u);
+    for (int i = 0; i < n_chunks; ++i) ones[size_t(1 + corder[size_t(i)])] = uint32_t(i);
+    cp(size_t(reinterpret_cast<char*>(chunk_flag) - w), ones.data(), sizeof(uint32_t) * (size_t(n_chunks) + 1));
+    counts.resize(size_t(kRawChunks) + 1);
+    for (int i = 0; i <= kRawChunks; ++i) counts[size_t(i)] = uint32_t(i);
     d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
     d_tag = reinterpret_cast<const uint32_t*>(w + L.tag);
   } else if (!direct || !d_bytes || !d_tag) {
@@ -615,6 +623,12 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     }
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, after, 0);
     const WriteValue32Fn wv = write_value32();
+    // the landed count is published after every `every`-th chunk (and the
+    // last): fewer stream memory operations between the copies (XM_RAW_FLAG_EVERY,
+    // tooling)
+    const char* fe = std::getenv("XM_RAW_FLAG_EVERY");
+    const int every = fe ? std::max(1, std::atoi(fe)) : kRawFlagEvery;
+    int landed = 0;
     for (int c : corder) {
       if (e != cudaSuccess) break;
       // the copied range is widened to 32-event boundaries (whole cache lines:
@@ -629,10 +643,14 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
                               cudaMemcpyHostToDevice, pp->cs);
       }
       if (e != cudaSuccess) break;
+      ++landed;
+      if (landed % every != 0 && landed != n_chunks) continue;
       if (wv) {
-        if (wv(pp->cs, reinterpret_cast<unsigned long long>(chunk_flag + c), 1u, 0) != 0) e = cudaErrorUnknown;
+        if (wv(pp->cs, reinterpret_cast<unsigned long long>(chunk_flag), uint32_t(landed), 0) != 0)
+          e = cudaErrorUnknown;
       } else {
-        e = cudaMemcpyAsync(chunk_flag + c, &ones[size_t(c)], sizeof(uint32_t), cudaMemcpyHostToDevice, pp->cs);
+        e = cudaMemcpyAsync(chunk_flag, &counts[size_t(landed)], sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            pp->cs);
       }
     }
     if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
