@@ -318,17 +318,26 @@ int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_con
  * >= 2^40 request S:231, alloc of a live id S:249, free of a non-live id or
  * with another size S:258; a free replays on its block's alloc stream) and
  * xm_simulate_host's results, without the host loader: the events go to the
- * device as they are (read in place over PCIe when page-locked, else copied
- * into d_ws), K5's matching kernel keyed by the raw block id (one open block
- * per id in a valid trace) validates every trace and renumbers its ids
- * densely while writing the wire arrays longest first, and k_replay replays
- * them. Synchronous; h_out[n_traces] HOST, caller order.
+ * device as they are (page-locked: DMA-copied into d_ws in chunks of whole
+ * traces, longest-traces-first, on a library-owned copy stream; pageable:
+ * copied first), the device loader k_load (keyed by the raw block id: one
+ * open block per id in a valid trace) validates every trace and renumbers its
+ * ids densely while writing the wire arrays longest first, and k_replay
+ * replays them. Page-locked batches that fill the GPU (>= SMs x 14 traces)
+ * run OVERLAPPED: the loader on 16 SMs of its own (library-owned stream), the
+ * replay on the others from the start, taking traces as the loader finishes
+ * them, then on the loader's SMs (env XM_RAW_OVERLAP=0: loader, then
+ * replay). The overlapped mode needs those SMs free of other work: a loader
+ * that makes no progress for 4 s makes the call fail with XM_ECUDA instead
+ * of hanging. Synchronous; h_out[n_traces] HOST, caller order; the results
+ * are identical in every mode.
  *   capacity: HOST [n_traces] or NULL (cfg->capacity).  d_ws: DEVICE,
  *   >= xm_raw_ws_bytes(off, n_traces, cfg) (~52 B per event).
  * Errors: XM_EINVAL / XM_ERANGE with *bad_trace = the first invalid caller
  * trace (its results, and those of every other trace, are still written but
- * meaningless for it); XM_ENOMEM; XM_ECUDA. XM_FULL mode only. Traces longer
- * than 2^31-1 events: XM_ERANGE.
+ * meaningless for it); XM_ENOMEM; XM_ECUDA (also: the overlapped loader made
+ * no progress). XM_FULL mode only. Traces longer than 2^31-1 events:
+ * XM_ERANGE.
  */
 size_t xm_raw_ws_bytes(const int64_t* off, int64_t n_traces, const xm_config* cfg);
 int xm_simulate_raw(const int64_t* bytes, const uint32_t* tag, const int64_t* off, int64_t n_traces,
