@@ -598,8 +598,8 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     std::stable_sort(corder.begin(), corder.end(),
                      [&](int x, int y) { return maxlen[size_t(x)] > maxlen[size_t(y)]; });
     // chunk_flag[0]: chunks landed so far (0 now); [1 + c]: chunk c's rank in
-    // the copy order. ones[i] = i + 1 (the landed count's values, for the
-    // fallback copy where the driver lacks cuStreamWriteValue32)
+    // the copy order (uploaded from `ones`). counts[i] = i: the landed count's
+    // values, for the fallback copy where the driver lacks cuStreamWriteValue32
     ones.assign(size_t(kRawChunks) + 1, 0u);
     for (int i = 0; i < n_chunks; ++i) ones[size_t(1 + corder[size_t(i)])] = uint32_t(i);
     cp(size_t(reinterpret_cast<char*>(chunk_flag) - w), ones.data(), sizeof(uint32_t) * (size_t(n_chunks) + 1));
