@@ -39,6 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             path = os.path.abspath(os.environ["XM_REPLAY_SRC"])
         if src == "scan.cu" and os.environ.get("XM_SCAN_SRC"):       # A/B tooling
             path = os.path.abspath(os.environ["XM_SCAN_SRC"])
+        if src == "lifecycle.cu" and os.environ.get("XM_LIFECYCLE_SRC"):   # A/B tooling
+            path = os.path.abspath(os.environ["XM_LIFECYCLE_SRC"])
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", *(["-DXM_DEBUG"] if DEBUG else []), *(["-DXM_TRACE"] if os.environ.get("XM_TRACE") else []), *(["-DXM_TIMING"] if TIMING else []),
                *([f"-DXM_HEAP_RESERVE_DIV={os.environ['XM_HEAP_RESERVE_DIV']}"] if os.environ.get("XM_HEAP_RESERVE_DIV") else []),
                *([f"-DXM_F_INIT_DIV={os.environ['XM_F_INIT_DIV']}"] if os.environ.get("XM_F_INIT_DIV") else []),

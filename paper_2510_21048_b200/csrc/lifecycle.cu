@@ -182,19 +182,39 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
     uint32_t top = 0, fresh = 0, max_open = 0, open = 0;
     unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0,
                        n_reopen = 0;
+    // the tile's instants are loaded one tile ahead (registers), so a tile's
+    // matching does not start behind its own loads
+    const long long* __restrict__ ib = reinterpret_cast<const long long*>(P.bytes) + e0;
+    const unsigned long long* __restrict__ ia =
+        P.tag ? nullptr : reinterpret_cast<const unsigned long long*>(P.addr) + e0;
+    const uint32_t* __restrict__ ig = P.tag ? P.tag + e0 : nullptr;
+    const uint8_t* __restrict__ is = P.stream ? P.stream + e0 : nullptr;
+    // (address or raw tag, bytes, stream) of instant i
+#define XM_K5_LOAD(i, A, B, S)                                              \
+    do {                                                                   \
+      B = __ldcg(ib + (i));                                                \
+      if (ig) {                                                            \
+        const uint32_t g_ = __ldcg(ig + (i));                              \
+        A = uint64_t(g_ & 0x0FFFFFFFu);                                    \
+        S = g_ >> 28;                                                      \
+      } else {                                                             \
+        A = __ldcg(ia + (i));                                              \
+        S = is ? uint32_t(__ldcg(is + (i))) : 0u;                          \
+      }                                                                    \
+    } while (0)
+    uint64_t a_nx = 0;
+    int64_t b_nx = 0;
+    uint32_t s_nx = 0;
+    if (int(lane) < n) XM_K5_LOAD(int(lane), a_nx, b_nx, s_nx);
     for (int base = 0; base < n; base += 32) {
       const int li = base + int(lane);
       const bool valid = li < n;
-      uint64_t a = valid ? (P.tag ? 0ull : P.addr[e0 + li]) : ~0ull - lane;
-      int64_t b = valid ? __ldcg(reinterpret_cast<const long long*>(P.bytes) + e0 + li) : 0;
+      uint64_t a = valid ? a_nx : ~0ull - lane;
+      int64_t b = valid ? b_nx : 0;
+      uint32_t s = valid ? s_nx : 0u;
+      if (li + 32 < n) XM_K5_LOAD(li + 32, a_nx, b_nx, s_nx);
       // |bytes| >= XM_MAX_REQUEST is out of the replay's range: invalid like 0
       if (b >= int64_t(XM_MAX_REQUEST) || b <= -int64_t(XM_MAX_REQUEST)) b = 0;
-      uint32_t s = (valid && P.stream) ? P.stream[e0 + li] : 0u;
-      if (P.tag) {                          // loader mode: the raw block id is the key
-        const uint32_t g = valid ? __ldcg(P.tag + e0 + li) : 0u;
-        a = valid ? uint64_t(g & 0x0FFFFFFFu) : a;
-        s = g >> 28;
-      }
       const bool is_alloc = b > 0, is_free = b < 0;
       // ---- dense ids for this tile's allocations (ids freed before the tile) ----
       const unsigned am = __ballot_sync(kFull, is_alloc);
@@ -359,6 +379,8 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
     }
   }
 }
+
+#undef XM_K5_LOAD
 
 // ---- k_load: the device loader of xm_simulate_raw ------------------------------
 // The loader mode of k_reconstruct, specialised: the key is the raw block id,
