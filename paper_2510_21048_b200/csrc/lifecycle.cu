@@ -106,6 +106,7 @@ struct LParams {
                                           // trace of stored k); or null (caller order)
   uint32_t* stall;                        // overlapped mode: set when a chunk never lands
                                           // (or the replay gave up); every waiter bails
+  const uint32_t* pull_count;             // with pull: the number of entries (device), or null
   uint32_t* loaded;                       // ... and each finished trace is appended to
                                           // a completion queue: loaded[n_traces] is its
                                           // tail, loaded[i] = stored index + 1 (release)
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
     unsigned k = 0;
     if (lane == 0) k = atomicAdd(P.work, 1u);
     k = __shfl_sync(kFull, k, 0);
-    if (int64_t(k) >= P.n_traces) break;
+    if (int64_t(k) >= P.n_traces || (P.pull_count && k >= *P.pull_count)) break;
     const unsigned t = P.pull ? P.pull[k] : k;   // the caller's trace
     if (P.chunk_flag) {                     // wait until trace t's chunk has landed
       int lo = 0, hi = P.n_chunks - 1;      // the chunk c with first[c] <= t < first[c+1]
@@ -377,6 +378,214 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
       }
       __syncwarp();
     }
+  }
+}
+
+// ---- k_reconstruct_smem: K5 with its per-trace state in shared memory --------
+// The same matching as k_reconstruct (general mode: addresses, LIFO stacks per
+// address, the same dense-id assignment and outputs), but each warp's hash
+// table (address -> top open block), block records and free-id stack live in
+// shared memory, so the probes and record reads are shared-memory round trips
+// and the only global traffic is the instants, the per-instant outputs and
+// the staging. Records are indexed by dense id (at most one open block per
+// id): w0 = block below (id + 1, 0 none) | stream << 28, w1 = its event index,
+// w2/w3 = its request bytes. The table is never cleared: a slot belongs to the
+// current trace iff its generation does (a warp-local count, cleared once at
+// start). A trace needing more than kSRecs dense ids or more than 3/4 of the
+// table's slots stops and is queued (ovf) for k_reconstruct, which rewrites
+// every output of it.
+constexpr int kSW = 4;                      // warps per CTA (one CTA per SM)
+constexpr uint32_t kSTable = 2048;          // table slots per warp (16 B)
+constexpr uint32_t kSRecs = 1024;           // dense ids per warp (16 B records + 4 B stack)
+constexpr size_t kSWarpBytes = size_t(kSTable) * 16 + size_t(kSRecs) * 20;
+constexpr size_t kSSmem = kSW * kSWarpBytes;
+
+__global__ void __launch_bounds__(32 * kSW, 1) k_reconstruct_smem(LParams P, uint32_t* ovf,
+                                                                  uint32_t* ovf_count) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t w = threadIdx.x >> 5;
+  uint4* T = reinterpret_cast<uint4*>(sm + size_t(w) * kSWarpBytes);
+  uint4* Rr = T + kSTable;
+  uint32_t* ids = reinterpret_cast<uint32_t*>(Rr + kSRecs);
+  for (uint32_t h = lane; h < kSTable; h += 32) T[h] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+  uint32_t gen = 0;
+  const uint32_t hb = 11;                   // log2 kSTable
+  const uint32_t hmask = kSTable - 1u;
+  for (;;) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(P.work, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (int64_t(k) >= P.n_traces) break;
+    const unsigned t = k;
+    ++gen;
+    const int64_t e0 = P.off[t];
+    const int n = int(P.off[t + 1] - e0);
+    uint32_t top = 0, fresh = 0, max_open = 0, open = 0, ndist = 0;
+    bool overflow = false;
+    unsigned long long n_blocks = 0, n_orphan = 0, n_mism = 0, n_matched = 0, n_kept = 0, n_inv = 0,
+                       n_reopen = 0;
+    const long long* __restrict__ ib = reinterpret_cast<const long long*>(P.bytes) + e0;
+    const unsigned long long* __restrict__ ia = reinterpret_cast<const unsigned long long*>(P.addr) + e0;
+    const uint32_t* __restrict__ ig = nullptr;
+    const uint8_t* __restrict__ is = P.stream ? P.stream + e0 : nullptr;
+    uint64_t a_nx = 0;
+    int64_t b_nx = 0;
+    uint32_t s_nx = 0;
+    if (int(lane) < n) XM_K5_LOAD(int(lane), a_nx, b_nx, s_nx);
+    for (int base = 0; base < n; base += 32) {
+      const int li = base + int(lane);
+      const bool valid = li < n;
+      uint64_t a = valid ? a_nx : ~0ull - lane;
+      int64_t b = valid ? b_nx : 0;
+      uint32_t s = valid ? s_nx : 0u;
+      if (li + 32 < n) XM_K5_LOAD(li + 32, a_nx, b_nx, s_nx);
+      if (b >= int64_t(XM_MAX_REQUEST) || b <= -int64_t(XM_MAX_REQUEST)) b = 0;
+      const bool is_alloc = b > 0, is_free = b < 0;
+      // ---- dense ids for this tile's allocations (ids freed before the tile) ----
+      const unsigned am = __ballot_sync(kFull, is_alloc);
+      const uint32_t na = __popc(am), ka = __popc(am & lt);
+      const uint32_t take = min(na, top);
+      if (fresh + (na - take) > kSRecs) { overflow = true; break; }   // (warp-uniform)
+      uint32_t my_id = 0, my_tag = 0;
+      if (is_alloc) {
+        my_id = ka < take ? ids[top - 1 - ka] : fresh + (ka - take);
+        my_tag = my_id | (s << 28);
+        P.partner[e0 + li] = -1;
+        P.mismatch[e0 + li] = 0;
+      }
+      top -= take;
+      fresh += na - take;
+      __syncwarp();
+      // ---- matching (LIFO per address), rounds as in k_reconstruct ----
+      bool matched = false, reopened = false;
+      int blk = -1;
+      uint32_t blk_tag = 0;
+      long long blk_bytes = 0;
+      const unsigned grp = __match_any_sync(kFull, a);
+      const uint32_t my_rank = __popc(grp & lt);
+      const uint32_t rounds = __reduce_max_sync(kFull, valid ? uint32_t(__popc(grp)) : 0u);
+      for (uint32_t r = 0; r < rounds; ++r) {
+        const bool act = valid && b != 0 && my_rank == r;
+        uint32_t h = hash_addr(a, hb);
+        bool found = false;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (act) {
+          for (;;) {
+            v = T[h];
+            if (v.w != gen) break;
+            if ((uint64_t(v.y) << 32 | v.x) == a) { found = true; break; }
+            h = (h + 1) & hmask;
+          }
+        }
+        bool pend = act && is_alloc && !found;
+        ndist += __popc(__ballot_sync(kFull, pend));
+        if (ndist > kSTable / 4 * 3) { overflow = true; break; }   // (warp-uniform)
+        while (__any_sync(kFull, pend)) {
+          const unsigned same = __match_any_sync(kFull, pend ? h : 0xFFFFFFFFu);
+          const bool win = pend && (__ffs(same) - 1) == int(lane);
+          __syncwarp();
+          if (win) T[h] = make_uint4(uint32_t(a), uint32_t(a >> 32), 0u, gen);
+          __syncwarp();
+          if (pend && !win) {
+            h = (h + 1) & hmask;
+            for (;;) {
+              if (T[h].w != gen) break;
+              h = (h + 1) & hmask;
+            }
+          }
+          pend = pend && !win;
+        }
+        __syncwarp();
+        if (act) {
+          const uint32_t tp = found ? v.z : 0u;          // top open block (id + 1)
+          if (is_alloc) {
+            reopened = tp != 0u;
+            const unsigned long long ub = static_cast<unsigned long long>(b);
+            Rr[my_id] = make_uint4(tp | (s << 28), uint32_t(li), uint32_t(ub), uint32_t(ub >> 32));
+            T[h].z = my_id + 1u;
+          } else if (tp != 0u) {
+            const uint4 rr = Rr[tp - 1u];
+            T[h].z = rr.x & 0x0FFFFFFFu;
+            blk = int(rr.y);
+            blk_tag = (tp - 1u) | (rr.x & 0xF0000000u);
+            blk_bytes = static_cast<long long>((static_cast<unsigned long long>(rr.w) << 32) | rr.z);
+            matched = true;
+          }
+        }
+        __syncwarp();
+      }
+      if (overflow) break;
+      __syncwarp();
+      // ---- per-instant outputs ----
+      bool mism = false;
+      if (is_free && matched) mism = blk_bytes != -b;
+      if (is_free) {
+        P.partner[e0 + li] = matched ? blk : -1;
+        if (matched) P.partner[e0 + blk] = li;
+        P.mismatch[e0 + li] = mism ? 1 : 0;
+      } else if (valid && b == 0) {
+        P.partner[e0 + li] = -1;
+        P.mismatch[e0 + li] = 0;
+      }
+      __syncwarp();
+      // ---- matched blocks' ids go back on the stack ----
+      const unsigned mm = __ballot_sync(kFull, matched);
+      if (matched) ids[top + __popc(mm & lt)] = blk_tag & 0x0FFFFFFFu;
+      top += __popc(mm);
+      // ---- staging: kept events, compacted within the trace ----
+      const bool kept = is_alloc || matched;
+      const unsigned km = __ballot_sync(kFull, kept);
+      if (kept) {
+        const int64_t dst = e0 + int64_t(n_kept) + __popc(km & lt);
+        if (is_alloc) {
+          P.st_bytes[dst] = b;
+          P.st_tag[dst] = my_tag;
+        } else {
+          P.st_bytes[dst] = -blk_bytes;
+          P.st_tag[dst] = blk_tag;
+        }
+      }
+      int d = is_alloc ? 1 : (matched ? -1 : 0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, d, o);
+        if (int(lane) >= o) d += y;
+      }
+      const uint32_t mo = __reduce_max_sync(kFull, uint32_t(int(open) + d));
+      max_open = max(max_open, mo);
+      open = uint32_t(int(open) + __shfl_sync(kFull, d, 31));
+      n_blocks += na;
+      n_matched += __popc(mm);
+      n_kept += __popc(km);
+      n_orphan += __popc(__ballot_sync(kFull, is_free && !matched));
+      n_mism += __popc(__ballot_sync(kFull, mism));
+      n_inv += __popc(__ballot_sync(kFull, valid && b == 0));
+      n_reopen += __popc(__ballot_sync(kFull, reopened));
+      __syncwarp();
+    }
+    __syncwarp();
+    if (overflow) {                          // k_reconstruct redoes this trace
+      if (lane == 0) ovf[atomicAdd(ovf_count, 1u)] = t;
+      __syncwarp();
+      continue;
+    }
+    if (lane == 0) {
+      xm_lifecycle r;
+      r.n_blocks = n_blocks;
+      r.n_orphan = n_orphan;
+      r.n_mismatch = n_mism;
+      r.n_persistent = n_blocks - n_matched;
+      r.n_kept = n_kept;
+      r.n_invalid = n_inv;
+      r.max_open = max_open;
+      r.n_ids = fresh;
+      r.n_reopened = n_reopen;
+      P.rec[t] = r;
+    }
+    __syncwarp();
   }
 }
 
@@ -646,7 +855,7 @@ __global__ void k_wire_compact(const int64_t* __restrict__ off, const int64_t* _
 
 struct Layout {
   uint32_t hbits, n_slots, ctas;
-  size_t tables, stacks, arec, st_bytes, st_tag, total;
+  size_t tables, stacks, arec, st_bytes, st_tag, ovf, total;
 };
 
 Layout layout(const xm_instants* in) {
@@ -678,6 +887,7 @@ Layout layout(const xm_instants* in) {
   L.arec = o; o += al(E * sizeof(ARec));
   L.st_bytes = o; o += al(E * 8);
   L.st_tag = o; o += al(E * 4);
+  L.ovf = o; o += al(size_t(in->n_traces > 0 ? in->n_traces : 1) * 4);   // k_reconstruct_smem overflow
   L.total = o;
   return L;
 }
@@ -728,8 +938,30 @@ extern "C" int xm_reconstruct(const xm_instants* in, void* d_scratch, size_t scr
   P.mismatch = d_mismatch;
   P.rec = d_rec;
   P.work = reinterpret_cast<unsigned int*>(base);
-  k_reconstruct<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(P);
-  launch_counter() = 1;
+  // XM_K5=smem: the shared-memory pass first (one CTA per SM), then
+  // k_reconstruct over the traces it could not hold (header word 1 counts
+  // them, word 2 is the second pass's work counter)
+  const char* k5 = getenv("XM_K5");
+  if (k5 && k5[0] == 's') {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaFuncSetAttribute(k_reconstruct_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSSmem));
+    if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct: ") + cudaGetErrorString(e));
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(base);
+    uint32_t* ovf = reinterpret_cast<uint32_t*>(base + L.ovf);
+    const int64_t g = std::min<int64_t>(sms, (in->n_traces + kSW - 1) / kSW);
+    k_reconstruct_smem<<<unsigned(g > 0 ? g : 1), 32 * kSW, kSSmem, st>>>(P, ovf, hdr + 1);
+    LParams Q = P;
+    Q.pull = ovf;
+    Q.pull_count = hdr + 1;
+    Q.work = hdr + 2;
+    k_reconstruct<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(Q);
+    launch_counter() = 2;
+  } else {
+    k_reconstruct<kWarps><<<L.ctas, 32 * kWarps, 0, st>>>(P);
+    launch_counter() = 1;
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(XM_ECUDA, std::string("xm_reconstruct: ") + cudaGetErrorString(e));
   return XM_OK;

@@ -149,3 +149,27 @@ def test_out_of_range_instants_are_invalid():
     p = partner.cpu().numpy()
     assert p[0] == 3 and p[3] == 0 and p[1] == -1 and p[2] == -1
     assert wb.bytes[:wb.n_events].cpu().numpy().tolist() == [4096, -4096]
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_reconstruct_smem_variant(monkeypatch, k):
+    """XM_K5=smem: the shared-memory pass (and k_reconstruct on the traces it
+    cannot hold) gives the same partners, mismatches, tallies, dense ids and
+    wire form, checked against the oracle as the default kernel is."""
+    monkeypatch.setenv("XM_K5", "smem")
+    _check(_corpora()[k])
+
+
+def test_reconstruct_smem_variant_config4_shaped(monkeypatch):
+    """... on config-4-shaped instants, where the longest traces overflow the
+    shared-memory budget and take the second pass, and against the default
+    kernel output for output."""
+    b = suites.config4()
+    idx = np.linspace(0, b.n_traces - 1, 300).astype(int)
+    ins = instants.from_batch(b.subset(idx), salt=5, p_orphan=0.001, p_mismatch=0.001, p_lost=0.002)
+    d = xm.DeviceInstants.from_host(ins.addr, ins.bytes, ins.stream, ins.off)
+    p0, m0, r0, _ = xm.reconstruct(d)
+    monkeypatch.setenv("XM_K5", "smem")
+    p1, m1, r1, _ = xm.reconstruct(d)
+    assert (p0.cpu() == p1.cpu()).all() and (m0.cpu() == m1.cpu()).all() and (r0 == r1).all()
+    _check(ins)
