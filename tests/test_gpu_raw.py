@@ -198,3 +198,43 @@ def test_raw_overlapped_wide_layout_traces():
     h = _raw(b, pinned=True)
     assert xm.last_launch_count() == 3
     assert_parity(b, h, oracle_run(b, parallel=True))
+
+
+def _reused_ids(n_traces, seed):
+    """Traces whose raw block ids are reused after their block is freed (the
+    contract forbids only the alloc of a LIVE id), with 28-bit ids
+    spread over the id space and random streams."""
+    rng = np.random.default_rng(seed)
+    tb = TraceBuilder()
+    for _ in range(n_traces):
+        pool = rng.choice(1 << 28, size=int(rng.integers(3, 12)), replace=False)
+        live = {}
+        for _ in range(int(rng.integers(20, 200))):
+            free_ids = [i for i in pool if i not in live]
+            if live and (not free_ids or rng.random() < 0.45):
+                bid = list(live)[int(rng.integers(len(live)))]
+                tb.free(int(bid), stream=int(live.pop(bid)))
+            else:
+                bid = free_ids[int(rng.integers(len(free_ids)))]
+                st = int(rng.integers(0, 3))
+                live[bid] = st
+                tb.alloc(int(bid), int(rng.integers(1, 64 << 20)), stream=st)
+        for bid in list(live):
+            tb.free(int(bid), stream=live.pop(bid))
+        tb.end_trace()
+    return tb.build()
+
+
+@pytest.mark.parametrize("overlapped", [False, True])
+def test_raw_reused_block_ids(monkeypatch, overlapped):
+    """Raw ids reused after their free: the loader reopens a closed key (k_load)
+    and the replay matches the oracle and the host loader's path; sequential
+    and overlapped, and with K5's loader (XM_LOADER=k5)."""
+    b = _reused_ids(2300 if overlapped else 300, seed=7 + int(overlapped))
+    h = _raw(b, pinned=True)
+    assert xm.last_launch_count() == (3 if overlapped else 2)
+    assert_parity(b, h, oracle_run(b, parallel=overlapped))
+    hd, _ = gpu_run(b)
+    assert (h == hd).all()
+    monkeypatch.setenv("XM_LOADER", "k5")
+    assert (_raw(b, pinned=True) == h).all()
