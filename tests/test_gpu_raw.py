@@ -238,3 +238,17 @@ def test_raw_reused_block_ids(monkeypatch, overlapped):
     assert (h == hd).all()
     monkeypatch.setenv("XM_LOADER", "k5")
     assert (_raw(b, pinned=True) == h).all()
+
+
+@pytest.mark.parametrize("variant", ["div4", "d3", "knobs"])
+def test_raw_overlapped_variants(variant):
+    """The allocator variants through the overlapped path (the knobs run the
+    separate k_replay<true> instantiation in both replay launches)."""
+    b = _big_mixed(91)
+    cfg, ora = {"div4": (xm.Config(roundup_power2_divisions=4), dict(div=4)),
+                "d3": (xm.Config(reclaim_policy=1), dict(reclaim=1)),
+                "knobs": (xm.Config(max_split_size=24 << 20, garbage_collection_threshold=0.5),
+                          dict(msplit=24 << 20, gc=0.5))}[variant]
+    h = _raw(b, cfg, pinned=True)
+    assert xm.last_launch_count() == 3
+    assert_parity(b, h, oracle_run(b, parallel=True, **ora))
