@@ -323,11 +323,12 @@ int xm_simulate_host(const xm_traces* tr, const uint64_t* capacity, const xm_con
  * copied first), the device loader k_load (keyed by the raw block id: one
  * open block per id in a valid trace) validates every trace and renumbers its
  * ids densely while writing the wire arrays longest first, and k_replay
- * replays them. Page-locked batches that fill the GPU (>= SMs x 14 traces)
- * run OVERLAPPED: the loader on 16 SMs of its own (library-owned stream), the
- * replay on the others from the start, taking traces as the loader finishes
- * them, then on the loader's SMs (env XM_RAW_OVERLAP=0: loader, then
- * replay). The overlapped mode needs those SMs free of other work: a loader
+ * replays them. Page-locked batches of >= 16 traces run OVERLAPPED: the
+ * replay takes traces as the loader (on SMs of its own, library-owned stream)
+ * finishes them -- for a batch that fills the GPU (>= SMs x 14 traces) the
+ * loader has 16 SMs and a second replay launch follows it onto them; for a
+ * smaller one the replay has the SMs it needs and the loader all the others
+ * (env XM_RAW_OVERLAP=0: loader, then replay). The overlapped mode needs those SMs free of other work: a loader
  * that makes no progress for 4 s makes the call fail with XM_ECUDA instead
  * of hanging. Synchronous; h_out[n_traces] HOST, caller order; the results
  * are identical in every mode.

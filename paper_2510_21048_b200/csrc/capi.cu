@@ -430,6 +430,7 @@ constexpr int kRawChunks = 256;         // most upload chunks of xm_simulate_raw
 constexpr int kRawDefaultChunks = 48;   // upload chunks by default (tuned, config 4)
 constexpr int kRawLoaderSms = 16;       // SMs of the overlapped loader by default (tuned)
 constexpr int kRawFlagEvery = 1;        // landed count published after every n-th chunk
+constexpr int64_t kRawOverlapMinTraces = 16;   // smallest batch run overlapped (measured)
 
 struct RawShape {
   int64_t T, E;
@@ -713,9 +714,15 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   }
   const char* ov = std::getenv("XM_RAW_OVERLAP");                      // tooling: "0" = off
   const char* lsm = std::getenv("XM_RAW_LOADER_SMS");                  // tooling
-  const int loader_sms = lsm ? std::atoi(lsm) : kRawLoaderSms;
-  const bool overlap = streamed && !(ov && ov[0] == '0') && plan.ctas >= dev_sms &&
-                       loader_sms >= 1 && loader_sms < dev_sms && L.total - L.scratch >= plan.scratch_bytes;
+  // a batch that fills the GPU: the loader on loader_sms SMs, the replay on
+  // the rest and then on the loader's; a smaller one (>= kRawOverlapMinTraces
+  // traces: below that the streams' synchronisation costs more than the
+  // overlap saves -- one 486-event trace: 0.59 vs 0.47 ms): the replay on the
+  // SMs it needs (plan.ctas), the loader on all the others, no second launch
+  const bool big = plan.ctas >= dev_sms;
+  const int loader_sms = big ? (lsm ? std::atoi(lsm) : kRawLoaderSms) : dev_sms - plan.ctas;
+  const bool overlap = streamed && !(ov && ov[0] == '0') && loader_sms >= 1 && loader_sms < dev_sms &&
+                       R.T >= kRawOverlapMinTraces && L.total - L.scratch >= plan.scratch_bytes;
   if (overlap) {
     uint32_t* loaded = reinterpret_cast<uint32_t*>(w + L.loaded);
     void* k2s = w + L.scratch;
@@ -739,9 +746,10 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
                            reinterpret_cast<const uint32_t*>(w + L.pos), loaded, loader_sms,
                            reinterpret_cast<uint32_t*>(static_cast<char*>(k2s) + 4 * 24));
     if (!ek) ek = launch_replay(&b, cfg, u, plan, k2s, d_out, st, &launches, nullptr, loaded,
-                                dev_sms - loader_sms, false);
-    if (!ek) ek = launch_replay(&b, cfg, u, plan, k2s, d_out, pp->ls, &launches, nullptr, loaded,
-                                loader_sms, false);
+                                big ? dev_sms - loader_sms : plan.ctas, false);
+    if (!ek && big)
+      ek = launch_replay(&b, cfg, u, plan, k2s, d_out, pp->ls, &launches, nullptr, loaded,
+                         loader_sms, false);
     enqueue_chunks(pp->meta);    // also when a launch failed: `copied` must exist
     // `stream` resumes after the loader's stream and the copies, also on failure
     const cudaError_t e1 = cudaEventRecord(pp->ldone, pp->ls);
