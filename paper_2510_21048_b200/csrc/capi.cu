@@ -245,8 +245,9 @@ HostLayout host_layout(const xm_traces_info& I, const xm_config* cfg, bool with_
 struct Pipe {
   int dev = -1;
   cudaStream_t cs = nullptr;        // copies
+  cudaStream_t cs2 = nullptr;       // xm_simulate_raw's second copy stream (chunks alternate)
   cudaStream_t ls = nullptr;        // xm_simulate_raw's loader (overlapped with the replay)
-  cudaEvent_t start = nullptr, copied = nullptr, meta = nullptr, ldone = nullptr;
+  cudaEvent_t start = nullptr, copied = nullptr, meta = nullptr, ldone = nullptr, copied2 = nullptr;
 };
 thread_local Pipe g_pipe;
 
@@ -264,6 +265,8 @@ cudaError_t get_pipe(Pipe** out) {
     if ((e = cudaStreamCreateWithFlags(&q.ls, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&q.meta, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&q.ldone, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&q.cs2, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&q.copied2, cudaEventDisableTiming)) != cudaSuccess) return e;
     p = q;   // a previous device's objects are leaked, not destroyed under another context
   }
   *out = &p;
@@ -431,6 +434,7 @@ constexpr int kRawDefaultChunks = 48;   // upload chunks by default (tuned, conf
 constexpr int kRawLoaderSms = 16;       // SMs of the overlapped loader by default (tuned)
 constexpr int kRawFlagEvery = 1;        // landed count published after every n-th chunk
 constexpr int64_t kRawOverlapMinTraces = 16;   // smallest batch run overlapped (measured)
+constexpr int kRawCopyStreams = 1;      // copy streams the upload chunks alternate over
 
 struct RawShape {
   int64_t T, E;
@@ -453,7 +457,7 @@ RawLayout raw_layout(const RawShape& R, const xm_config* cfg) {
   L.woff = p; p += al(8 * (T + 1));
   L.wnids = p; p += al(4 * T);
   L.out = p; p += al(sizeof(xm_result) * T);
-  L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 2));   // chunk firsts, landed + ranks
+  L.ready = p; p += al(sizeof(uint32_t) * (2 * kRawChunks + 3));   // chunk firsts, 2 landed counts, ranks
   L.pos = p; p += al(4 * T);                                        // caller -> stored index
   L.loaded = p; p += al(4 * (T + 1));                               // completion queue + tail
   L.scratch = p;
@@ -568,6 +572,7 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
   static thread_local std::vector<uint32_t> firsts;    // outlive the async copies
   static thread_local std::vector<uint32_t> ones;      // chunk ranks (upload)
   static thread_local std::vector<uint32_t> counts;    // landed-count values (fallback copies)
+  int n_cs = 1;                                        // copy streams the chunks alternate over
   std::vector<int> corder;
   if (streamed) {
     // chunks: whole traces up to about (c+1)/n of the events (n: XM_RAW_CHUNKS,
@@ -598,12 +603,17 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
     for (int c = 0; c < n_chunks; ++c) corder[size_t(c)] = c;
     std::stable_sort(corder.begin(), corder.end(),
                      [&](int x, int y) { return maxlen[size_t(x)] > maxlen[size_t(y)]; });
-    // chunk_flag[0]: chunks landed so far (0 now); [1 + c]: chunk c's rank in
-    // the copy order (uploaded from `ones`). counts[i] = i: the landed count's
-    // values, for the fallback copy where the driver lacks cuStreamWriteValue32
-    ones.assign(size_t(kRawChunks) + 1, 0u);
-    for (int i = 0; i < n_chunks; ++i) ones[size_t(1 + corder[size_t(i)])] = uint32_t(i);
-    cp(size_t(reinterpret_cast<char*>(chunk_flag) - w), ones.data(), sizeof(uint32_t) * (size_t(n_chunks) + 1));
+    // chunk_flag[0] / [1]: chunks landed so far on copy stream 0 / 1 (0 now);
+    // [2 + c]: chunk c's stream << 31 | rank in that stream's copy order
+    // (uploaded from `ones`); the i-th chunk in copy order goes to stream
+    // i % n_cs. counts[i] = i: the landed counts' values, for the fallback
+    // copy where the driver lacks cuStreamWriteValue32
+    const char* ncs = std::getenv("XM_RAW_COPY_STREAMS");                // tooling: 1 or 2
+    n_cs = (ncs && ncs[0] == '2') ? 2 : kRawCopyStreams;
+    ones.assign(size_t(kRawChunks) + 2, 0u);
+    for (int i = 0; i < n_chunks; ++i)
+      ones[size_t(2 + corder[size_t(i)])] = (uint32_t(i % n_cs) << 31) | uint32_t(i / n_cs);
+    cp(size_t(reinterpret_cast<char*>(chunk_flag) - w), ones.data(), sizeof(uint32_t) * (size_t(n_chunks) + 2));
     counts.resize(size_t(kRawChunks) + 1);
     for (int i = 0; i <= kRawChunks; ++i) counts[size_t(i)] = uint32_t(i);
     d_bytes = reinterpret_cast<const int64_t*>(w + L.bytes);
@@ -623,37 +633,45 @@ extern "C" int xm_simulate_raw(const int64_t* h_bytes, const uint32_t* h_tag, co
       if (e == cudaSuccess) e = cudaEventRecord(after, st);
     }
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pp->cs, after, 0);
+    if (e == cudaSuccess && n_cs > 1) e = cudaStreamWaitEvent(pp->cs2, after, 0);
     const WriteValue32Fn wv = write_value32();
     // the landed count is published after every `every`-th chunk (and the
     // last): fewer stream memory operations between the copies (XM_RAW_FLAG_EVERY,
     // tooling)
     const char* fe = std::getenv("XM_RAW_FLAG_EVERY");
     const int every = fe ? std::max(1, std::atoi(fe)) : kRawFlagEvery;
-    int landed = 0;
+    int landed[2] = {0, 0};
+    int pos = 0;
     for (int c : corder) {
       if (e != cudaSuccess) break;
+      const int sidx = pos % n_cs;
+      ++pos;
+      cudaStream_t cst = sidx ? pp->cs2 : pp->cs;
       // the copied range is widened to 32-event boundaries (whole cache lines:
       // a boundary line is written by both neighbours, with the same bytes)
       const int64_t ev0 = h_off[firsts[size_t(c)]] & ~int64_t(31);
       const int64_t ev1 = std::min<int64_t>(R.E, (h_off[firsts[size_t(c) + 1]] + 31) & ~int64_t(31));
       if (ev1 > ev0) {
         e = cudaMemcpyAsync(w + L.bytes + 8 * size_t(ev0), h_bytes + ev0, 8 * size_t(ev1 - ev0),
-                            cudaMemcpyHostToDevice, pp->cs);
+                            cudaMemcpyHostToDevice, cst);
         if (e == cudaSuccess)
           e = cudaMemcpyAsync(w + L.tag + 4 * size_t(ev0), h_tag + ev0, 4 * size_t(ev1 - ev0),
-                              cudaMemcpyHostToDevice, pp->cs);
+                              cudaMemcpyHostToDevice, cst);
       }
       if (e != cudaSuccess) break;
-      ++landed;
-      if (landed % every != 0 && landed != n_chunks) continue;
+      const int lc = ++landed[sidx];
+      const int last_here = (n_chunks - 1 - sidx) / n_cs + 1;   // chunks on this stream
+      if (lc % every != 0 && lc != last_here) continue;
       if (wv) {
-        if (wv(pp->cs, reinterpret_cast<unsigned long long>(chunk_flag), uint32_t(landed), 0) != 0)
+        if (wv(cst, reinterpret_cast<unsigned long long>(chunk_flag + sidx), uint32_t(lc), 0) != 0)
           e = cudaErrorUnknown;
       } else {
-        e = cudaMemcpyAsync(chunk_flag, &counts[size_t(landed)], sizeof(uint32_t), cudaMemcpyHostToDevice,
-                            pp->cs);
+        e = cudaMemcpyAsync(chunk_flag + sidx, &counts[size_t(lc)], sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            cst);
       }
     }
+    if (e == cudaSuccess && n_cs > 1) e = cudaEventRecord(pp->copied2, pp->cs2);
+    if (e == cudaSuccess && n_cs > 1) e = cudaStreamWaitEvent(pp->cs, pp->copied2, 0);
     if (e == cudaSuccess) e = cudaEventRecord(pp->copied, pp->cs);
   };
   // processing order of the replay: longest first, ties in caller order (as

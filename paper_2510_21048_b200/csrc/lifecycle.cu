@@ -96,10 +96,11 @@ struct LParams {
   const uint32_t* pos;                    // offsets (stored order), caller -> stored
   uint32_t* w_nids;                       // index, n_ids out (0 = invalid); or null
   const uint32_t* chunk_first;            // loader mode, streamed input: [n_chunks + 1]
-  const uint32_t* chunk_flag;             // first trace of each upload chunk; [0] the
-                                          // number of chunks landed (copy order, written
-                                          // stream-ordered after them), [1 + c] chunk c's
-                                          // rank in the copy order; or null
+  const uint32_t* chunk_flag;             // first trace of each upload chunk; [0], [1]
+                                          // the chunks landed so far on copy stream 0 / 1
+                                          // (written stream-ordered after them), [2 + c]
+                                          // chunk c's stream << 31 | its rank in that
+                                          // stream's copy order; or null
   int n_chunks;
   const uint32_t* pull;                   // loader mode, overlapped replay: traces are
                                           // pulled in stored order (pull[k] = caller
@@ -136,14 +137,17 @@ __global__ void __launch_bounds__(32 * kW) k_reconstruct(LParams P) {
         const int m = (lo + hi + 1) >> 1;
         if (P.chunk_first[m] <= t) lo = m; else hi = m - 1;
       }
-      const uint32_t need = P.chunk_flag[1 + lo];
+      // chunk lo's copy stream (bit 31) and its rank in that stream's order
+      const uint32_t cr = P.chunk_flag[2 + lo];
+      const uint32_t need = cr & 0x7FFFFFFFu;
+      const uint32_t* landed = P.chunk_flag + (cr >> 31);
       uint32_t nap = 256;
       unsigned long long t0 = 0;
       bool gave_up = false;
       for (;;) {
         uint32_t r = 0;
         if (lane == 0)
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.chunk_flag) : "memory");
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(landed) : "memory");
         if (__shfl_sync(kFull, r, 0) > need) break;   // chunks landed so far > its rank
         if (P.stall) {                      // overlapped: bounded wait (XM_LOADED_TIMEOUT_NS)
           unsigned long long now;
@@ -623,14 +627,17 @@ __global__ void __launch_bounds__(32 * kW) k_load(LParams P) {
         const int m = (lo + hi + 1) >> 1;
         if (P.chunk_first[m] <= t) lo = m; else hi = m - 1;
       }
-      const uint32_t need = P.chunk_flag[1 + lo];
+      // chunk lo's copy stream (bit 31) and its rank in that stream's order
+      const uint32_t cr = P.chunk_flag[2 + lo];
+      const uint32_t need = cr & 0x7FFFFFFFu;
+      const uint32_t* landed = P.chunk_flag + (cr >> 31);
       uint32_t nap = 256;
       unsigned long long t0 = 0;
       bool gave_up = false;
       for (;;) {
         uint32_t r = 0;
         if (lane == 0)
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(P.chunk_flag) : "memory");
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(landed) : "memory");
         if (__shfl_sync(kFull, r, 0) > need) break;   // chunks landed so far > its rank
         if (P.stall) {                      // overlapped: bounded wait
           unsigned long long now;
