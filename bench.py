@@ -472,7 +472,7 @@ def main():
 
         # the headline: xm_simulate_raw on the caller's raw arrays in page-locked
         # host memory (pinned once, as a user's input buffers would be): the
-        # device validates, renumbers and replays (K5-loader -> K2) every step
+        # device validates, renumbers and replays (k_load overlapped with k_replay) every step
         pin_b = torch.from_numpy(np.ascontiguousarray(batch.bytes)).pin_memory().numpy()
         pin_t = torch.from_numpy(np.ascontiguousarray(batch.tag).view(np.int32)).pin_memory() \
             .numpy().view(np.uint32)
